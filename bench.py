@@ -1,0 +1,371 @@
+"""Benchmark: MST edges/s for dendrogram construction on B200 (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload config4]
+    python bench.py --impl reference ...        # the reference CPU path (oracle port)
+
+A step = one full `rank_edges + pandora` (the timed scope of `dendromst
+build`, cli.py:82-85) over one synthetic MST of BASELINE.json's shape,
+inputs resident in HBM: sort of the weights, maxIncident, all contraction
+levels, chain walk, chain sort and link.  Default workload = config 4
+(random spanning tree n = 128M, tied weights), the configuration the
+headline metric is quoted on.  N > 1 runs N independent replicas (one tree
+per GPU, no collective on the data path: "replicas only").
+
+`e2e` is the same metric through the public API with HOST buffers: pinned
+int32 u, v + float64 w copied in, orig_of / heights / edge_parent /
+vertex_parent copied out, every step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MST edges/sec for dendrogram build on 1 B200 (n=128M); % of HBM roofline"
+UNIT = "edges/s"
+
+WORKLOADS = {
+    # name: (generator, n, description)
+    "config4": ("tied", 128_000_000,
+                "config4: random spanning tree n=128M, tied weights w in {0..4095} (float64), seed 0"),
+    "config4u": ("random", 128_000_000,
+                 "config4 companion: random spanning tree n=128M, uniform weights, seed 0"),
+    "config3-path": ("path", 16_000_000, "config3: path n=16M, monotone weights (single chain)"),
+    "config3-caterpillar": ("caterpillar", 16_000_000,
+                            "config3: caterpillar n=16M, monotone weights (single chain)"),
+    "random16M": ("random", 16_000_000, "random spanning tree n=16M, uniform weights (config3 reference point)"),
+    "config5-tree": ("random", 8_000_000, "config5 unit: random spanning tree n=8M, uniform weights"),
+    "config1": ("random", 100_000, "config1: random spanning tree n=100k, uniform weights, seed 0"),
+}
+
+# Algorithmic HBM bytes per launch of each kernel kind.  n = edges of
+# the launch's view; int32 ids/ranks = 4 B, float64 = 8 B.
+BYTES_PER_EDGE = {
+    "sort1_hist": 8,          # read w
+    "sort1_pass_first": 20,   # read w 8; write key 8 + id 4
+    "sort1_pass_mid": 24,     # read key+id 12; write 12
+    "sort1_pass_final": 48,   # read 12; gather u,v 8; write orig_of 4, heights 8, euv 8; 2 atomics 8
+    "sort2_pass": 16,         # read key+rank 8; write 8
+    "walk": 17,               # ret 1 + eu 4 + map 4 + smi 4 + key 4
+    "link": 12,               # read key+rank 8; scatter 4
+}
+
+
+def pipeline_bytes(n: int, S: int) -> int:
+    """SURVEY.md §8d byte model: B_alg = 403 n + 98 S, S = sum_{k>=1} n_k."""
+    return 403 * n + 98 * S
+
+
+def load_peaks() -> tuple[float, str]:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        rows = []
+        for line in (getattr(self, "out", "") or "").splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                try:
+                    rows.append(parts)
+                except Exception:
+                    pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[3 + i]
+                          and "Not" not in r[3 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_input(workload: str, n_override: int | None, seed: int):
+    from paper_2401_06089_b200 import synth
+    gen, n, desc = WORKLOADS[workload]
+    if n_override:
+        n = n_override
+    nv, u, v, w = synth.GENERATORS[gen](n, seed=seed)
+    return nv, u, v, w, desc
+
+
+def cpu_reference_rate(workload: str, n_sample: int, repeats: int) -> tuple[float, list[float]]:
+    """Time the oracle port of rank_edges + pandora (single core) on a sample."""
+    from oracle import dendro_oracle as O
+    from paper_2401_06089_b200 import synth
+    gen, _, _ = WORKLOADS[workload]
+    nv, u, v, w = synth.GENERATORS[gen](n_sample, seed=0)
+    times = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        O.build(nv, u, v, w)
+        times.append(time.perf_counter() - t0)
+    return n_sample / statistics.median(times), times
+
+
+def run_reference(args) -> None:
+    ws, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    _, n_full, desc = WORKLOADS[args.workload]
+    n_sample = min(args.ref_sample, args.n or n_full)
+    O_warm = max(args.warmup, 0)
+    from oracle import dendro_oracle as O
+    from paper_2401_06089_b200 import synth
+    gen, _, _ = WORKLOADS[args.workload]
+    nv, u, v, w = synth.GENERATORS[gen](n_sample, seed=0)
+    for _ in range(O_warm):
+        O.build(nv, u, v, w)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.build(nv, u, v, w)
+        times.append(time.perf_counter() - t0)
+    mean = sum(times) / len(times)
+    value = n_sample / mean
+    sample = (f"{n_sample} edges of the {args.workload} shape per step (bounded sample of the "
+              f"n={n_full} workload); oracle port of rank_edges+pandora, numpy + C union-find")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * mean,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+int64",
+        "data": "synthetic",
+        "config": {"workload": desc, "n_edges_sample": n_sample, "parallelism": "single core"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample,
+                         "host_cpus": os.cpu_count()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def run_b200(args) -> None:
+    import torch
+    ws, rank, local = dist_setup()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    from paper_2401_06089_b200 import BuildResult, DendrogramBuilder, _lib
+    from paper_2401_06089_b200.build import build as build_lib
+    if rank == 0:
+        build_lib()
+    if ws > 1:
+        torch.distributed.barrier()
+
+    nv, u, v, w, desc = make_input(args.workload, args.n, seed=rank)
+    n = int(u.shape[0])
+    builder = DendrogramBuilder(dev)
+    du = torch.from_numpy(u).to(dev)
+    dv = torch.from_numpy(v).to(dev)
+    dw = torch.from_numpy(w).to(dev)
+    out = BuildResult(orig_of=torch.empty(n, dtype=torch.int32, device=dev),
+                      heights=torch.empty(n, dtype=torch.float64, device=dev),
+                      edge_parent=torch.empty(n, dtype=torch.int32, device=dev),
+                      vertex_parent=torch.empty(nv, dtype=torch.int32, device=dev))
+    stream = torch.cuda.current_stream(dev)
+
+    def step(profile=False):
+        return builder.build(nv, du, dv, dw, out=out, profile=profile)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # ---------------- device-resident timed region ----------------
+    prof: dict[str, list] = {}
+    launches = 0
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            res = step(profile=True)
+            launches += int(res.stats.kernel_launches)
+            for k, (ms, calls) in res.stats.kernel_profile().items():
+                p = prof.setdefault(k, [0.0, 0])
+                p[0] += ms
+                p[1] += calls
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    if ws > 1:
+        torch.distributed.barrier()
+    ms_step = e0.elapsed_time(e1) / args.steps
+    stats = res.stats
+    counts = stats.view_kind_counts()
+    S = sum(c[3] for c in counts[1:])
+
+    # ---------------- end-to-end through the public API (host buffers) ----------------
+    hu = torch.from_numpy(u).pin_memory()
+    hv = torch.from_numpy(v).pin_memory()
+    hw = torch.from_numpy(w).pin_memory()
+    ho = torch.empty(n, dtype=torch.int32).pin_memory()
+    hh = torch.empty(n, dtype=torch.float64).pin_memory()
+    he = torch.empty(n, dtype=torch.int32).pin_memory()
+    hvp = torch.empty(nv, dtype=torch.int32).pin_memory()
+
+    def e2e_step():
+        r = builder.build(nv, hu, hv, hw, out=out)  # H2D inside (non_blocking from pinned)
+        ho.copy_(r.orig_of, non_blocking=True)
+        hh.copy_(r.heights, non_blocking=True)
+        he.copy_(r.edge_parent, non_blocking=True)
+        hvp.copy_(r.vertex_parent, non_blocking=True)
+        stream.synchronize()
+
+    e2e_step()
+    e2e_steps = max(1, min(args.steps, 5))
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    f1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = f0.elapsed_time(f1) / e2e_steps
+    if not np.array_equal(he[:1000].numpy(), out.edge_parent[:1000].cpu().numpy()):
+        raise RuntimeError("e2e output mismatch")
+
+    # ---------------- max over ranks ----------------
+    t = torch.tensor([ms_step, e2e_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms_step, e2e_ms = float(t[0]), float(t[1])
+
+    if rank == 0:
+        peak, peak_src = load_peaks()
+        # dominant kernel (largest total device time in the timed region)
+        kname, (kms, kcalls) = max(prof.items(), key=lambda kv: kv[1][0])
+        per_launch_ms = kms / kcalls
+        bpe = BYTES_PER_EDGE.get(kname)
+        roof = None
+        if bpe is not None:
+            achieved = bpe * n / (per_launch_ms * 1e-3) / 1e9
+            traffic = None
+            tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+            if os.path.exists(tpath):
+                try:
+                    traffic = json.load(open(tpath)).get(args.workload, {}).get(kname)
+                except Exception:
+                    traffic = None
+            roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": traffic,
+                    "algorithmic_bytes_per_launch": bpe * n, "avg_launch_ms": per_launch_ms,
+                    "peak_source": peak_src}
+        B = pipeline_bytes(n, S)
+        pipe_ach = B / (ms_step * 1e-3) / 1e9
+        cpu = None
+        if ws == 1 and not args.no_cpu_baseline:
+            n_s = min(args.cpu_sample, n)
+            rate, times = cpu_reference_rate(args.workload, n_s, 1)
+            cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
+                   "sample": f"oracle port (numpy + C union-find, 1 core) of rank_edges+pandora on "
+                             f"{n_s} edges of the {args.workload} shape, {times[0]:.1f}s",
+                   "host_cpus": os.cpu_count()}
+        line = {
+            "metric": METRIC, "value": ws * n / (ms_step * 1e-3), "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u64-key+int32", "data": "synthetic",
+            "config": {"workload": desc, "n_edges": n, "n_vertices": nv,
+                       "per_gpu": "one independent tree per GPU (replicas)" if ws > 1 else "one tree",
+                       "l2": "inputs (16 B/edge = %.1f GB) and working set larger than the 126 MB L2"
+                             % (16 * n / 1e9) if n > 10_000_000 else "small input (L2-resident)",
+                       "parallelism": f"replicas x{ws}", "levels": stats.num_levels,
+                       "sort1_passes": stats.sort1_passes, "sort2_passes": stats.sort2_passes,
+                       "S_over_n": S / n},
+            "e2e": {"value": ws * n / (e2e_ms * 1e-3), "unit": UNIT,
+                    "h2d_bytes_per_step": n * (4 + 4 + 8),
+                    "d2h_bytes_per_step": n * (4 + 8 + 4) + nv * 4, "ms_per_step": e2e_ms},
+            "roofline": roof,
+            "pipeline_roofline": {"bound": "hbm", "achieved": pipe_ach, "peak": peak, "unit": "GB/s",
+                                  "frac": pipe_ach / peak, "algorithmic_bytes_per_step": B,
+                                  "model": "403 n + 98 S (SURVEY.md 8d)", "peak_source": peak_src,
+                                  "frac_vs_nominal_8TBs": pipe_ach / 8000.0},
+            "kernel_ms_per_step": {k: v[0] / args.steps for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])},
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="config4")
+    ap.add_argument("--n", type=int, default=None, help="override the workload's edge count")
+    ap.add_argument("--cpu-sample", type=int, default=8_000_000)
+    ap.add_argument("--ref-sample", type=int, default=2_000_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 0 or args.steps < 1:
+        raise SystemExit("bad steps/warmup")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,120 @@
+/*
+ * dmst — B200-native PANDORA dendrogram construction, C ABI.
+ *
+ * Drop-in boundary for the reference hot path of arxiv/paper_2401_06089's
+ * `dendromst` package (paths relative to /root/reference/pkg/src/dendromst/):
+ *
+ *   dmst_rank_edges  replaces  rank_edges(tree) -> RankedTree     tree_core.py:174-190
+ *   dmst_pandora     replaces  pandora(ranked) -> Dendrogram      expansion.py:148-153
+ *                              (build_incidence tree_core.py:193-199, vertex_parents
+ *                               classify.py:23-25, build_hierarchy contraction.py:186-219,
+ *                               assign_chains expansion.py:97-128, stitch_chains :131-145)
+ *   dmst_build       replaces  the timed scope of `dendromst build`:
+ *                              rank_edges + _ALGOS["pandora"]      cli.py:82-85 (`_cmd_build`)
+ *
+ * Conventions (all identical to the reference):
+ *   - rank r = position after a stable descending-weight sort; ties by
+ *     ascending original id; -0.0 ties with +0.0 (numpy `<` semantics).
+ *   - orig_of[r]       = original edge id of rank r      (RankedTree.orig_of)
+ *   - heights[r]       = w[orig_of[r]], bitwise copy      (RankedTree.w)
+ *   - edge_parent[r]   in [-1, r-1], -1 = ROOT            (Dendrogram.edge_parent)
+ *   - vertex_parent[x] = largest incident rank            (Dendrogram.vertex_parent)
+ *   Device dtypes are int32 ids/ranks and float64 weights; the Python
+ *   wrapper widens to the reference's int64.
+ *
+ * Every pointer except `level_counts`, `num_levels` and `stats` is a DEVICE
+ * pointer.  The caller allocates every device buffer, including the
+ * workspace (size from dmst_workspace_bytes); the library never allocates,
+ * frees, or keeps state between calls.  Inputs are read-only.  Work is
+ * enqueued on `stream`; the call returns after the stream has drained
+ * (the contraction level loop sizes each level from device counts).
+ * Calls on different streams with different workspaces may run
+ * concurrently; results are bit-identical across runs and streams.
+ *
+ * Return value: 0 on success, DMST_EINVAL (22) on bad sizes/pointers,
+ * DMST_ECUDA (-1) on a CUDA error; the message is in dmst_last_error()
+ * (thread-local).  The input must already be a valid spanning tree
+ * (validation is the caller's, tree_core.py:110-139, as in the reference,
+ * whose `pandora` raises nothing itself — SPEC.md:265).
+ * Limits: 1 <= n_edges < 2^30, n_vertices == n_edges + 1.
+ */
+#ifndef DMST_H
+#define DMST_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DMST_EINVAL 22
+#define DMST_ECUDA (-1)
+#define DMST_MAX_LEVELS 64
+
+#define DMST_MAX_KERNELS 16
+
+/* Per-call diagnostics (host memory, optional).  Set `profile` = 1 before
+ * the call to have every kernel bracketed by CUDA events on `stream`;
+ * kernel_ms / kernel_calls then hold per-kernel-kind device time and launch
+ * counts (names from dmst_kernel_name). */
+typedef struct dmst_stats {
+  int32_t profile;                           /* in: 1 = record per-kernel events */
+  int32_t num_levels;                        /* ContractionHierarchy.num_levels */
+  int32_t level_counts[DMST_MAX_LEVELS + 1][4]; /* view_kind_counts: (n_alpha, n_leaf, n_chain, n_k) per view 0..L */
+  int32_t view_vertices[DMST_MAX_LEVELS + 1];   /* supervertex count of every view */
+  int32_t sort1_passes;                      /* non-constant 8-bit digits sorted in the edge sort */
+  int32_t sort2_passes;                      /* digits sorted in the chain sort */
+  int32_t jump_rounds;                       /* pointer-jumping rounds over all levels */
+  int32_t kernel_launches;                   /* kernels this call enqueued */
+  float kernel_ms[DMST_MAX_KERNELS];         /* out (profile=1): device ms per kernel kind */
+  int32_t kernel_calls[DMST_MAX_KERNELS];    /* out: launches per kernel kind */
+} dmst_stats;
+
+/* Workspace size for a tree with n_edges edges. */
+size_t dmst_workspace_bytes(int64_t n_edges, int64_t n_vertices);
+
+/* rank_edges + pandora, fused (what `dendromst build` times). */
+int dmst_build(const int32_t* u, const int32_t* v, const double* w, int64_t n_edges,
+               int64_t n_vertices, int32_t* orig_of, double* heights, int32_t* edge_parent,
+               int32_t* vertex_parent, dmst_stats* stats, void* workspace,
+               size_t workspace_bytes, void* stream);
+
+/* rank_edges only: orig_of, heights and rank-order endpoints ru/rv. */
+int dmst_rank_edges(const int32_t* u, const int32_t* v, const double* w, int64_t n_edges,
+                    int64_t n_vertices, int32_t* orig_of, double* heights, int32_t* ru,
+                    int32_t* rv, void* workspace, size_t workspace_bytes, void* stream);
+
+/* pandora on an already ranked tree (ru/rv = RankedTree.u/.v). */
+int dmst_pandora(const int32_t* ru, const int32_t* rv, int64_t n_edges, int64_t n_vertices,
+                 int32_t* edge_parent, int32_t* vertex_parent, dmst_stats* stats,
+                 void* workspace, size_t workspace_bytes, void* stream);
+
+/* Debug/introspection variant of dmst_build for per-stage parity tests:
+ * additionally copies (device -> the given DEVICE buffers, each nullable)
+ *   retirement[n]  ContractionHierarchy.retirement_level (int8 values)
+ *   chain_key[n]   dense chain id per edge: 0 = root chain, else
+ *                  1 + (offset of view `level`) + anchor supervertex
+ *   chain_terminal[n], chain_level[n]  ChainAssignment.terminal / .level
+ */
+int dmst_build_debug(const int32_t* u, const int32_t* v, const double* w, int64_t n_edges,
+                     int64_t n_vertices, int32_t* orig_of, double* heights,
+                     int32_t* edge_parent, int32_t* vertex_parent, dmst_stats* stats,
+                     int8_t* retirement, int32_t* chain_key, int32_t* chain_terminal,
+                     int32_t* chain_level, void* workspace, size_t workspace_bytes,
+                     void* stream);
+
+/* Message for the last non-zero return on this thread ("" if none). */
+const char* dmst_last_error(void);
+
+/* Name of kernel kind `id` (0 <= id < DMST_MAX_KERNELS), "" if unused. */
+const char* dmst_kernel_name(int32_t id);
+
+/* Library version string. */
+const char* dmst_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DMST_H */

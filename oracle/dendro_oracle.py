@@ -1,0 +1,307 @@
+"""ORACLE / TEST INFRASTRUCTURE ONLY.
+
+CPU restatement of the reference hot path (`rank_edges` + `pandora`) of
+arxiv/paper_2401_06089's `dendromst` package, written from the reference's
+behaviour, numpy for the array work and C (oracle/uf_roots.c, the numba
+union-find's twin) for the one sequential loop.  Every function cites the
+reference file:line it restates; paths are relative to
+/root/reference/pkg/src/dendromst/.
+
+Who may import this module: tests/, __graft_entry__.smoke() and bench.py's
+CPU-baseline / `--impl reference` legs - and only as the checker or the
+timed CPU baseline.  The product path (paper_2401_06089_b200) never imports
+it and has no CPU fallback.
+
+Pinning: tests/test_oracle_golden.py checks this module against golden
+vectors produced by the UNMODIFIED reference (tests/golden/make_golden.py
+imports /root/reference/pkg/src) and against the reference's own
+known-answer tests (tests/test_*.py KATs).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+ROOT = -1  # expansion.py:20
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+
+
+def _lib():
+    """Load (building on first use) the C union-find, oracle/_build/liboracle.so."""
+    global _LIB
+    if _LIB is None:
+        path = os.path.join(_HERE, "_build", "liboracle.so")
+        if not os.path.exists(path):
+            subprocess.run(["make", "-s", "-C", _HERE], check=True)
+        lib = ctypes.CDLL(path)
+        p64 = ctypes.POINTER(ctypes.c_int64)
+        lib.oracle_uf_roots.argtypes = [ctypes.c_int64, ctypes.c_int64, p64, p64, p64]
+        lib.oracle_uf_roots.restype = None
+        _LIB = lib
+    return _LIB
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+
+
+# ----------------------------------------------------------------- tree_core
+
+@dataclass(frozen=True)
+class Ranked:
+    """RankedTree (tree_core.py:39-56) without the frozen base object."""
+    num_vertices: int
+    rank_of: np.ndarray
+    orig_of: np.ndarray
+    u: np.ndarray
+    v: np.ndarray
+    w: np.ndarray
+
+    @property
+    def num_edges(self) -> int:
+        return int(self.u.shape[0])
+
+
+def rank_edges(num_vertices: int, u, v, w) -> Ranked:
+    """tree_core.py:174-190: stable argsort of -w; ties by ascending original id."""
+    u = np.ascontiguousarray(u, dtype=np.int64)
+    v = np.ascontiguousarray(v, dtype=np.int64)
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    order = np.argsort(-w, kind="stable")                      # :180
+    rank_of = np.empty(w.shape[0], dtype=np.int64)
+    rank_of[order] = np.arange(w.shape[0])                     # :181-182
+    return Ranked(num_vertices, rank_of, order, u[order], v[order], w[order])  # :186-189
+
+
+def max_incident(num_vertices: int, u: np.ndarray, v: np.ndarray,
+                 rank: np.ndarray) -> np.ndarray:
+    """tree_core.py:193-199 / contraction.py:149-154: scatter-max of ranks, -1 init."""
+    mi = np.full(num_vertices, -1, dtype=np.int64)
+    np.maximum.at(mi, u, rank)
+    np.maximum.at(mi, v, rank)
+    return mi
+
+
+# ------------------------------------------------------------------ classify
+
+LEAF, CHAIN, ALPHA = 0, 1, 2  # classify.py:17-20
+
+
+def edge_kinds_from_ends(at_u: np.ndarray, at_v: np.ndarray) -> np.ndarray:
+    """classify.py:37-42."""
+    kinds = np.full(at_u.shape[0], CHAIN, dtype=np.int8)
+    kinds[at_u & at_v] = LEAF
+    kinds[~at_u & ~at_v] = ALPHA
+    return kinds
+
+
+def kind_counts(kinds: np.ndarray) -> tuple[int, int, int]:
+    """classify.py:45-50: (n_alpha, n_leaf, n_chain)."""
+    return (int(np.count_nonzero(kinds == ALPHA)),
+            int(np.count_nonzero(kinds == LEAF)),
+            int(np.count_nonzero(kinds == CHAIN)))
+
+
+# --------------------------------------------------------------- contraction
+
+def uf_roots(num_vertices: int, cu: np.ndarray, cv: np.ndarray) -> np.ndarray:
+    """contraction.py:53-79 (`_uf_roots`): C twin of the numba loop."""
+    cu = np.ascontiguousarray(cu, dtype=np.int64)
+    cv = np.ascontiguousarray(cv, dtype=np.int64)
+    parent = np.empty(num_vertices, dtype=np.int64)
+    _lib().oracle_uf_roots(num_vertices, cu.shape[0], _ptr(cu), _ptr(cv), _ptr(parent))
+    return parent
+
+
+def component_labels(num_vertices: int, u, v) -> np.ndarray:
+    """contraction.py:82-93: canonical labels ordered by smallest member."""
+    roots = uf_roots(num_vertices, u, v)
+    is_root = roots == np.arange(num_vertices)
+    ids = np.cumsum(is_root) - 1
+    return ids[roots]
+
+
+@dataclass
+class Level:
+    """ContractionLevel (contraction.py:106-120)."""
+    surviving_edges: np.ndarray
+    vertex_map: np.ndarray
+    super_max_incident: np.ndarray
+    super_count: int
+    edge_u: np.ndarray
+    edge_v: np.ndarray
+
+
+@dataclass
+class Hierarchy:
+    """ContractionHierarchy (contraction.py:123-146)."""
+    levels: list
+    retirement_level: np.ndarray
+    view_kind_counts: list
+    edge_u: np.ndarray
+    edge_v: np.ndarray
+    num_vertices: int
+
+    @property
+    def num_levels(self) -> int:
+        return len(self.levels)
+
+
+def contract_level(nv: int, u, v, rank, alpha: np.ndarray) -> Level:
+    """contraction.py:165-183."""
+    keep = alpha
+    vertex_map = component_labels(nv, u[~keep], v[~keep])       # :168
+    super_count = int(vertex_map.max()) + 1                     # :169
+    edge_u = vertex_map[u[keep]]                                # :170
+    edge_v = vertex_map[v[keep]]                                # :171
+    surviving = rank[keep]                                      # :172
+    smi = max_incident(super_count, edge_u, edge_v, surviving)  # :173-175
+    return Level(surviving, vertex_map, smi, super_count, edge_u, edge_v)
+
+
+def build_hierarchy(r: Ranked, mi: np.ndarray) -> Hierarchy:
+    """contraction.py:186-219: classify -> contract until a view has no alpha."""
+    n = r.num_edges
+    nv, vu, vv, vrank = r.num_vertices, r.u, r.v, np.arange(n)  # :193
+    cur_mi = mi
+    levels: list[Level] = []
+    counts: list[tuple[int, int, int, int]] = []
+    retirement = np.full(n, -1, dtype=np.int64)                 # :197
+    while True:
+        at_u = vrank == cur_mi[vu]                              # view_kinds :157-162
+        at_v = vrank == cur_mi[vv]
+        kinds = edge_kinds_from_ends(at_u, at_v)
+        counts.append((*kind_counts(kinds), int(vrank.shape[0])))  # :201
+        alpha = kinds == ALPHA
+        if levels and not alpha.any():                          # :203-205
+            retirement[vrank] = len(levels)
+            break
+        level = contract_level(nv, vu, vv, vrank, alpha)        # :206
+        retirement[vrank[~alpha]] = len(levels)                 # :207
+        levels.append(level)
+        nv, vu, vv, vrank = level.super_count, level.edge_u, level.edge_v, level.surviving_edges
+        cur_mi = level.super_max_incident                       # :210
+    return Hierarchy(levels, retirement, counts, r.u, r.v, r.num_vertices)
+
+
+# ----------------------------------------------------------------- expansion
+
+@dataclass
+class Chains:
+    """ChainAssignment (expansion.py:38-53)."""
+    terminal: np.ndarray
+    anchor: np.ndarray
+    level: np.ndarray
+
+
+def assign_chains(h: Hierarchy) -> Chains:
+    """expansion.py:97-128: earliest level whose supervertex parent is heavier."""
+    n = int(h.retirement_level.shape[0])
+    terminal = np.full(n, ROOT, dtype=np.int64)
+    anchor = np.zeros(n, dtype=np.int64)
+    level_arr = np.zeros(n, dtype=np.int64)
+    retirement = h.retirement_level
+    pending = np.arange(n)
+    comp = None
+    for k, lvl in enumerate(h.levels, start=1):
+        comp = lvl.vertex_map if comp is None else lvl.vertex_map[comp]   # :114
+        eligible = retirement[pending] < k                                # :115
+        cand = pending[eligible]
+        if cand.shape[0] == 0:
+            pending = pending[~eligible] if eligible.any() else pending
+            continue
+        sv = comp[h.edge_u[cand]]                                         # :120
+        p = lvl.super_max_incident[sv]                                    # :121
+        hit = (p >= 0) & (p < cand)                                       # :122
+        matched = cand[hit]
+        terminal[matched] = p[hit]
+        anchor[matched] = sv[hit]
+        level_arr[matched] = k
+        pending = np.concatenate([pending[~eligible], cand[~hit]])        # :127
+    return Chains(terminal, anchor, level_arr)
+
+
+def stitch_chains(c: Chains, vertex_parent: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """expansion.py:131-145: lexsort (terminal, anchor, rank); link to predecessor."""
+    n = c.terminal.shape[0]
+    ranks = np.arange(n)
+    order = np.lexsort((ranks, c.anchor, c.terminal))          # :135
+    t_s = c.terminal[order]
+    a_s = c.anchor[order]
+    head = np.ones(n, dtype=bool)
+    head[1:] = (t_s[1:] != t_s[:-1]) | (a_s[1:] != a_s[:-1])   # :138-139
+    prev = np.concatenate(([ROOT], order[:-1]))                # :140
+    parent_sorted = np.where(head, t_s, prev)                   # :141
+    edge_parent = np.empty(n, dtype=np.int64)
+    edge_parent[order] = parent_sorted                         # :142-143
+    return edge_parent, np.asarray(vertex_parent, dtype=np.int64).copy()
+
+
+def pandora(r: Ranked):
+    """expansion.py:148-153: returns (edge_parent, vertex_parent, hierarchy)."""
+    mi = max_incident(r.num_vertices, r.u, r.v, np.arange(r.num_edges))  # build_incidence
+    vp = mi.copy()                                                         # classify.py:23-25
+    h = build_hierarchy(r, mi)
+    ep, vp = stitch_chains(assign_chains(h), vp)
+    return ep, vp, h
+
+
+@dataclass
+class BuildResult:
+    orig_of: np.ndarray
+    heights: np.ndarray
+    edge_parent: np.ndarray
+    vertex_parent: np.ndarray
+    view_kind_counts: list
+    num_levels: int
+    hierarchy: Hierarchy
+
+
+def build(num_vertices: int, u, v, w) -> BuildResult:
+    """The timed scope of `dendromst build` (cli.py:82-85 in the survey's
+    numbering; /root/reference/pkg/src/dendromst/cli.py `_cmd_build`):
+    rank_edges then pandora."""
+    r = rank_edges(num_vertices, u, v, w)
+    ep, vp, h = pandora(r)
+    return BuildResult(r.orig_of, r.w, ep, vp, h.view_kind_counts, h.num_levels, h)
+
+
+# ------------------------------------------------------- sequential oracles
+
+def dendrogram_bottom_up(r: Ranked) -> tuple[np.ndarray, np.ndarray]:
+    """oracles.py:63-85: sequential union-find from lightest to heaviest edge
+    (the reference's second, independent ground truth)."""
+    n = r.num_edges
+    edge_parent = np.full(n, ROOT, dtype=np.int64)
+    vertex_parent = np.full(r.num_vertices, ROOT, dtype=np.int64)
+    parent = list(range(r.num_vertices))
+
+    def find(x):
+        root = x
+        while parent[root] != root:
+            root = parent[root]
+        while parent[x] != root:
+            parent[x], x = root, parent[x]
+        return root
+
+    latest = [ROOT] * r.num_vertices
+    u, v = r.u.tolist(), r.v.tolist()
+    for rank in range(n - 1, -1, -1):
+        for x in (u[rank], v[rank]):
+            rr = latest[find(x)]
+            if rr != ROOT:
+                edge_parent[rr] = rank
+            else:
+                vertex_parent[x] = rank
+        a, b = find(u[rank]), find(v[rank])
+        if a > b:
+            a, b = b, a
+        parent[b] = a
+        latest[find(u[rank])] = rank
+    return edge_parent, vertex_parent

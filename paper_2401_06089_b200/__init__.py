@@ -1,0 +1,13 @@
+"""B200-native PANDORA dendrogram construction (arXiv 2401.06089).
+
+MST edge arrays (u, v, w) -> rank-space dendrogram (edge_parent,
+vertex_parent) + merge heights, bit-identical to the reference
+`dendromst` package, on hand-written sm_100a CUDA kernels behind a C ABI
+(include/dmst.h).  See DESIGN.md.
+"""
+from .api import (ROOT, BuildResult, Dendrogram, DendrogramBuilder, RankedTree,
+                  build_b200, pandora_b200, rank_edges_b200, register_algorithm)
+
+__all__ = ["ROOT", "BuildResult", "Dendrogram", "DendrogramBuilder", "RankedTree",
+           "build_b200", "pandora_b200", "rank_edges_b200", "register_algorithm"]
+__version__ = "0.1.0"

@@ -1,0 +1,107 @@
+"""ctypes binding of the C ABI declared in include/dmst.h.
+
+The shared library is built in-tree (paper_2401_06089_b200/libdmst.so, by
+__graft_entry__.build() or `python -m paper_2401_06089_b200.build`).  There
+is deliberately no CPU fallback: if the library is missing this module
+raises, loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdmst.so")
+
+DMST_EINVAL = 22
+DMST_ECUDA = -1
+DMST_MAX_LEVELS = 64
+DMST_MAX_KERNELS = 16
+
+# every symbol include/dmst.h declares
+EXPORTS = (
+    "dmst_workspace_bytes",
+    "dmst_build",
+    "dmst_rank_edges",
+    "dmst_pandora",
+    "dmst_build_debug",
+    "dmst_last_error",
+    "dmst_kernel_name",
+    "dmst_version",
+)
+
+
+class DmstStats(ctypes.Structure):
+    _fields_ = [
+        ("profile", ctypes.c_int32),
+        ("num_levels", ctypes.c_int32),
+        ("level_counts", (ctypes.c_int32 * 4) * (DMST_MAX_LEVELS + 1)),
+        ("view_vertices", ctypes.c_int32 * (DMST_MAX_LEVELS + 1)),
+        ("sort1_passes", ctypes.c_int32),
+        ("sort2_passes", ctypes.c_int32),
+        ("jump_rounds", ctypes.c_int32),
+        ("kernel_launches", ctypes.c_int32),
+        ("kernel_ms", ctypes.c_float * DMST_MAX_KERNELS),
+        ("kernel_calls", ctypes.c_int32 * DMST_MAX_KERNELS),
+    ]
+
+    def kernel_profile(self) -> dict[str, tuple[float, int]]:
+        """{kernel kind: (device ms, launches)} when profile=1 was set."""
+        lib = load()
+        out = {}
+        for i in range(DMST_MAX_KERNELS):
+            if self.kernel_calls[i]:
+                out[lib.dmst_kernel_name(i).decode()] = (float(self.kernel_ms[i]), int(self.kernel_calls[i]))
+        return out
+
+    def view_kind_counts(self) -> list[tuple[int, int, int, int]]:
+        """ContractionHierarchy.view_kind_counts (contraction.py:127-131)."""
+        return [tuple(int(x) for x in self.level_counts[k])
+                for k in range(self.num_levels + 1)]
+
+
+class DmstError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i64, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_size_t
+    lib.dmst_workspace_bytes.argtypes = [i64, i64]
+    lib.dmst_workspace_bytes.restype = sz
+    lib.dmst_build.argtypes = [vp, vp, vp, i64, i64, vp, vp, vp, vp,
+                               ctypes.POINTER(DmstStats), vp, sz, vp]
+    lib.dmst_build.restype = ctypes.c_int
+    lib.dmst_build_debug.argtypes = [vp, vp, vp, i64, i64, vp, vp, vp, vp,
+                                     ctypes.POINTER(DmstStats), vp, vp, vp, vp, vp, sz, vp]
+    lib.dmst_build_debug.restype = ctypes.c_int
+    lib.dmst_rank_edges.argtypes = [vp, vp, vp, i64, i64, vp, vp, vp, vp, vp, sz, vp]
+    lib.dmst_rank_edges.restype = ctypes.c_int
+    lib.dmst_pandora.argtypes = [vp, vp, i64, i64, vp, vp, ctypes.POINTER(DmstStats), vp, sz, vp]
+    lib.dmst_pandora.restype = ctypes.c_int
+    lib.dmst_last_error.argtypes = []
+    lib.dmst_last_error.restype = ctypes.c_char_p
+    lib.dmst_kernel_name.argtypes = [ctypes.c_int32]
+    lib.dmst_kernel_name.restype = ctypes.c_char_p
+    lib.dmst_version.argtypes = []
+    lib.dmst_version.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = load().dmst_last_error().decode(errors="replace")
+        if rc == DMST_EINVAL:
+            raise ValueError(msg)
+        raise DmstError(f"dmst error {rc}: {msg}")

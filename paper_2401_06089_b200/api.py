@@ -1,0 +1,280 @@
+"""Host-side mirror of the reference hot-path interface, on the B200 path.
+
+Reference interface (paths under /root/reference/pkg/src/dendromst/):
+
+* ``rank_edges(tree: WeightedTree) -> RankedTree``      tree_core.py:174-190
+* ``pandora(tree: RankedTree) -> Dendrogram``           expansion.py:148-153
+* ``_ALGOS: dict[str, Callable[[RankedTree], Dendrogram]]``   cli.py:27-31
+* ``Dendrogram(edge_parent, vertex_parent)`` with array equality  expansion.py:56-80
+
+This module provides the same entry points running on the GPU through the
+C ABI (include/dmst.h):
+
+* :func:`rank_edges_b200` / :func:`pandora_b200` — same arguments, same
+  results, drop-in for the reference functions; :func:`pandora_b200` has
+  the ``_ALGOS`` signature and :func:`register_algorithm` installs it.
+* :func:`build_b200` — both fused, the timed scope of ``dendromst build``.
+* :class:`DendrogramBuilder` — device-resident API (torch tensors in/out,
+  reusable workspace) for callers that keep the MST in HBM.
+
+Device buffers are torch tensors (PyTorch is the allocator and stream
+provider only).  There is no CPU fallback: without a CUDA device or
+without the built library these functions raise.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+
+ROOT = -1  # expansion.py:20
+
+
+def _reference_dendrogram_type():
+    try:  # if the reference package is importable, return ITS type so == works both ways
+        from dendromst.expansion import Dendrogram as RefDendrogram  # type: ignore
+        return RefDendrogram
+    except Exception:
+        return None
+
+
+@dataclass
+class Dendrogram:
+    """Mirror of ``dendromst.expansion.Dendrogram`` (expansion.py:56-80)."""
+    edge_parent: np.ndarray
+    vertex_parent: np.ndarray
+
+    @property
+    def num_edges(self) -> int:
+        return int(self.edge_parent.shape[0])
+
+    @property
+    def num_vertices(self) -> int:
+        return int(self.vertex_parent.shape[0])
+
+    def __eq__(self, other) -> bool:
+        if not hasattr(other, "edge_parent") or not hasattr(other, "vertex_parent"):
+            return NotImplemented
+        return (np.array_equal(self.edge_parent, other.edge_parent)
+                and np.array_equal(self.vertex_parent, other.vertex_parent))
+
+
+@dataclass(frozen=True)
+class RankedTree:
+    """Mirror of ``dendromst.tree_core.RankedTree`` (tree_core.py:39-56)."""
+    base: object
+    rank_of: np.ndarray
+    orig_of: np.ndarray
+    u: np.ndarray
+    v: np.ndarray
+    w: np.ndarray
+
+    @property
+    def num_vertices(self) -> int:
+        return int(self.base.num_vertices)
+
+    @property
+    def num_edges(self) -> int:
+        return int(self.u.shape[0])
+
+
+@dataclass
+class BuildResult:
+    """Device-resident outputs of one build (rank space, like the reference)."""
+    orig_of: torch.Tensor        # int32[n]   RankedTree.orig_of
+    heights: torch.Tensor        # float64[n] RankedTree.w (merge heights)
+    edge_parent: torch.Tensor    # int32[n]   Dendrogram.edge_parent
+    vertex_parent: torch.Tensor  # int32[nv]  Dendrogram.vertex_parent
+    stats: _lib.DmstStats = field(repr=False, default=None)
+    debug: dict = field(default_factory=dict, repr=False)
+
+    @property
+    def num_levels(self) -> int:
+        return int(self.stats.num_levels)
+
+    @property
+    def view_kind_counts(self) -> list[tuple[int, int, int, int]]:
+        return self.stats.view_kind_counts()
+
+    def dendrogram(self) -> Dendrogram:
+        """Host Dendrogram with the reference's int64 dtype."""
+        return Dendrogram(self.edge_parent.cpu().numpy().astype(np.int64),
+                          self.vertex_parent.cpu().numpy().astype(np.int64))
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _device_of(device) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2401_06089_b200 needs a CUDA device (no CPU fallback)")
+    d = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if d.type != "cuda":
+        raise ValueError(f"device must be a CUDA device, got {d}")
+    if d.index is None:
+        d = torch.device("cuda", torch.cuda.current_device())
+    return d
+
+
+def _as_dev(x, dtype: torch.dtype, dev: torch.device) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=dev, non_blocking=True)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(x)).to(device=dev)
+    if t.dtype != dtype:
+        t = t.to(dtype)
+    return t.contiguous()
+
+
+class DendrogramBuilder:
+    """Reusable workspace + entry points on one device.
+
+    ``build`` takes (num_vertices, u, v, w) as torch tensors (ideally
+    int32/int32/float64 already on the device) or numpy arrays.
+    """
+
+    def __init__(self, device=None):
+        self.lib = _lib.load()
+        self.device = _device_of(device)
+        self._ws: torch.Tensor | None = None
+
+    def workspace(self, n: int, nv: int) -> torch.Tensor:
+        need = int(self.lib.dmst_workspace_bytes(n, nv))
+        if need == 0:
+            raise ValueError(f"bad sizes n={n} nv={nv}")
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = None
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def _stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def build(self, num_vertices: int, u, v, w, *, out: BuildResult | None = None,
+              debug: bool = False, profile: bool = False) -> BuildResult:
+        dev = self.device
+        with torch.cuda.device(dev):
+            u = _as_dev(u, torch.int32, dev)
+            v = _as_dev(v, torch.int32, dev)
+            w = _as_dev(w, torch.float64, dev)
+            n = int(u.shape[0])
+            nv = int(num_vertices)
+            if v.shape[0] != n or w.shape[0] != n:
+                raise ValueError("edge arrays have mismatched lengths")
+            if out is None:
+                out = BuildResult(
+                    orig_of=torch.empty(n, dtype=torch.int32, device=dev),
+                    heights=torch.empty(n, dtype=torch.float64, device=dev),
+                    edge_parent=torch.empty(n, dtype=torch.int32, device=dev),
+                    vertex_parent=torch.empty(max(nv, 0), dtype=torch.int32, device=dev))
+            ws = self.workspace(n, nv) if n >= 1 and nv >= 2 else torch.empty(1, dtype=torch.uint8, device=dev)
+            st = _lib.DmstStats()
+            st.profile = 1 if profile else 0
+            if debug:
+                dbg = {"retirement": torch.empty(n, dtype=torch.int8, device=dev),
+                       "chain_key": torch.empty(n, dtype=torch.int32, device=dev),
+                       "chain_terminal": torch.empty(n, dtype=torch.int32, device=dev),
+                       "chain_level": torch.empty(n, dtype=torch.int32, device=dev)}
+                rc = self.lib.dmst_build_debug(
+                    _ptr(u), _ptr(v), _ptr(w), n, nv, _ptr(out.orig_of), _ptr(out.heights),
+                    _ptr(out.edge_parent), _ptr(out.vertex_parent), ctypes.byref(st),
+                    _ptr(dbg["retirement"]), _ptr(dbg["chain_key"]), _ptr(dbg["chain_terminal"]),
+                    _ptr(dbg["chain_level"]), _ptr(ws), ws.numel(), self._stream())
+                out.debug = dbg
+            else:
+                rc = self.lib.dmst_build(
+                    _ptr(u), _ptr(v), _ptr(w), n, nv, _ptr(out.orig_of), _ptr(out.heights),
+                    _ptr(out.edge_parent), _ptr(out.vertex_parent), ctypes.byref(st),
+                    _ptr(ws), ws.numel(), self._stream())
+            _lib.check(rc)
+            out.stats = st
+            return out
+
+    def rank_edges(self, num_vertices: int, u, v, w):
+        """-> (orig_of, heights, ru, rv) device int32/float64 tensors."""
+        dev = self.device
+        with torch.cuda.device(dev):
+            u = _as_dev(u, torch.int32, dev)
+            v = _as_dev(v, torch.int32, dev)
+            w = _as_dev(w, torch.float64, dev)
+            n = int(u.shape[0])
+            orig_of = torch.empty(n, dtype=torch.int32, device=dev)
+            heights = torch.empty(n, dtype=torch.float64, device=dev)
+            ru = torch.empty(n, dtype=torch.int32, device=dev)
+            rv = torch.empty(n, dtype=torch.int32, device=dev)
+            ws = self.workspace(n, int(num_vertices))
+            _lib.check(self.lib.dmst_rank_edges(
+                _ptr(u), _ptr(v), _ptr(w), n, int(num_vertices), _ptr(orig_of), _ptr(heights),
+                _ptr(ru), _ptr(rv), _ptr(ws), ws.numel(), self._stream()))
+            return orig_of, heights, ru, rv
+
+    def pandora(self, num_vertices: int, ru, rv):
+        """-> (edge_parent, vertex_parent, stats) from rank-order endpoints."""
+        dev = self.device
+        with torch.cuda.device(dev):
+            ru = _as_dev(ru, torch.int32, dev)
+            rv = _as_dev(rv, torch.int32, dev)
+            n = int(ru.shape[0])
+            nv = int(num_vertices)
+            ep = torch.empty(n, dtype=torch.int32, device=dev)
+            vp = torch.empty(nv, dtype=torch.int32, device=dev)
+            ws = self.workspace(n, nv)
+            st = _lib.DmstStats()
+            _lib.check(self.lib.dmst_pandora(_ptr(ru), _ptr(rv), n, nv, _ptr(ep), _ptr(vp),
+                                             ctypes.byref(st), _ptr(ws), ws.numel(), self._stream()))
+            return ep, vp, st
+
+
+_builders: dict[int, DendrogramBuilder] = {}
+
+
+def _builder(device=None) -> DendrogramBuilder:
+    dev = _device_of(device)
+    b = _builders.get(dev.index)
+    if b is None:
+        b = _builders[dev.index] = DendrogramBuilder(dev)
+    return b
+
+
+def build_b200(num_vertices: int, u, v, w, device=None, debug: bool = False) -> BuildResult:
+    """rank_edges + pandora on the GPU (the timed scope of `dendromst build`)."""
+    return _builder(device).build(num_vertices, u, v, w, debug=debug)
+
+
+def rank_edges_b200(tree, device=None) -> RankedTree:
+    """Drop-in for ``rank_edges`` (tree_core.py:174-190) on a WeightedTree-like
+    object (``num_vertices``, ``u``, ``v``, ``w``)."""
+    orig_of, heights, ru, rv = _builder(device).rank_edges(tree.num_vertices, tree.u, tree.v, tree.w)
+    order = orig_of.cpu().numpy().astype(np.int64)
+    rank_of = np.empty_like(order)
+    rank_of[order] = np.arange(order.shape[0])
+    return RankedTree(base=tree, rank_of=rank_of, orig_of=order,
+                      u=ru.cpu().numpy().astype(np.int64), v=rv.cpu().numpy().astype(np.int64),
+                      w=heights.cpu().numpy())
+
+
+def pandora_b200(tree, device=None):
+    """Drop-in for ``pandora`` (expansion.py:148-153) with the ``_ALGOS``
+    signature: RankedTree-like (``num_vertices``, rank-order ``u``, ``v``)
+    -> Dendrogram (the reference's own class when it is importable)."""
+    ep, vp, _ = _builder(device).pandora(tree.num_vertices, tree.u, tree.v)
+    cls = _reference_dendrogram_type() or Dendrogram
+    return cls(edge_parent=ep.cpu().numpy().astype(np.int64),
+               vertex_parent=vp.cpu().numpy().astype(np.int64))
+
+
+def register_algorithm(registry: dict | None = None, name: str = "pandora_b200") -> dict:
+    """Install :func:`pandora_b200` into the reference's algorithm registry
+    (``dendromst.cli._ALGOS``, cli.py:27-31) so ``dendromst build/bench
+    --algo pandora_b200`` runs on the GPU.  The CLI builds its choices from
+    ``_ALGOS`` at parse time (cli.py:200, :218)."""
+    if registry is None:
+        from dendromst import cli  # type: ignore
+        registry = cli._ALGOS
+    registry[name] = pandora_b200
+    return registry

@@ -1,0 +1,84 @@
+// Shared device helpers for the dendrogram pipeline (sm_100a).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dmst {
+
+constexpr int kWarp = 32;
+constexpr uint32_t kFull = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Relaxed, GPU-scope 32-bit load/store for decoupled look-back words.
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Streaming (read-once) loads: evict-first in L1, no allocation priority in L2.
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T* p) { return __ldcs(p); }
+
+__device__ __forceinline__ uint32_t warp_incl_sum(uint32_t x) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(kFull, x, o);
+    if (lane_id() >= (uint32_t)o) x += y;
+  }
+  return x;
+}
+
+// Block-wide exclusive sum of one value per thread.  `scratch` needs
+// BLOCK/32 + 1 words.  Returns the exclusive prefix; *total gets the sum.
+template <int BLOCK>
+__device__ __forceinline__ uint32_t block_excl_sum(uint32_t x, uint32_t* scratch, uint32_t* total) {
+  constexpr int NW = BLOCK / 32;
+  const uint32_t w = threadIdx.x >> 5;
+  uint32_t incl = warp_incl_sum(x);
+  if (lane_id() == 31) scratch[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t s = lane_id() < (uint32_t)NW ? scratch[lane_id()] : 0u;
+    uint32_t si = warp_incl_sum(s);
+    if (lane_id() < (uint32_t)NW) scratch[lane_id()] = si - s;
+    if (lane_id() == NW - 1) scratch[NW] = si;
+  }
+  __syncthreads();
+  uint32_t r = scratch[w] + incl - x;
+  *total = scratch[NW];
+  __syncthreads();
+  return r;
+}
+
+// Decoupled look-back status words: [31:30] flag, [29:0] value (< 2^30).
+constexpr uint32_t kFlagAgg = 1u << 30;
+constexpr uint32_t kFlagPrefix = 2u << 30;
+constexpr uint32_t kValMask = (1u << 30) - 1;
+
+// Walk predecessors' status words until an inclusive prefix is found.
+// `status` is indexed [tile * stride].
+__device__ __forceinline__ uint32_t lookback(const uint32_t* status, uint32_t tile, uint32_t stride) {
+  uint32_t excl = 0;
+  int64_t j = (int64_t)tile - 1;
+  while (j >= 0) {
+    uint32_t s = ld_relaxed(status + (uint64_t)j * stride);
+    if (s == 0) continue;  // predecessor not yet published: spin
+    excl += s & kValMask;
+    if (s & kFlagPrefix) break;
+    --j;
+  }
+  return excl;
+}
+
+}  // namespace dmst

@@ -51,12 +51,14 @@ WORKLOADS = {
 # the launch's view; int32 ids/ranks = 4 B, float64 = 8 B.
 BYTES_PER_EDGE = {
     "sort1_hist": 8,          # read w
-    "sort1_pass_first": 20,   # read w 8; write key 8 + id 4
-    "sort1_pass_mid": 24,     # read key+id 12; write 12
-    "sort1_pass_final": 48,   # read 12; gather u,v 8; write orig_of 4, heights 8, euv 8; 2 atomics 8
-    "sort2_pass": 16,         # read key+rank 8; write 8
+    "sort1_pass_first": 36,   # read w 8, u 4, v 4; write key 8 + (id, u, v) 12
+    "sort1_pass_mid": 40,     # read key + payload 20; write 20
+    "sort1_pass_final": 40,   # read 20; write orig_of 4, heights 8, euv 8
+    "mi_split": 32,           # read euv 8; write 2 records x (vertex, rank, other) 12
+    "mi_apply": 40,           # read 2 records 24; mi64 read-modify-write 16
+    "sort2_pass": 16,         # read key + rank 8; write 8
     "walk": 17,               # ret 1 + eu 4 + map 4 + smi 4 + key 4
-    "link": 12,               # read key+rank 8; scatter 4
+    "link": 12,               # read key + rank 8; scatter 4
 }
 
 

@@ -67,16 +67,26 @@ constexpr uint32_t kFlagPrefix = 2u << 30;
 constexpr uint32_t kValMask = (1u << 30) - 1;
 
 // Walk predecessors' status words until an inclusive prefix is found.
-// `status` is indexed [tile * stride].
+// `status` is indexed [tile * stride].  A window of LB predecessors is
+// loaded at once (independent loads) so one look-back costs about one L2
+// round trip instead of one per predecessor.
+template <int LB = 4>
 __device__ __forceinline__ uint32_t lookback(const uint32_t* status, uint32_t tile, uint32_t stride) {
   uint32_t excl = 0;
   int64_t j = (int64_t)tile - 1;
   while (j >= 0) {
-    uint32_t s = ld_relaxed(status + (uint64_t)j * stride);
-    if (s == 0) continue;  // predecessor not yet published: spin
-    excl += s & kValMask;
-    if (s & kFlagPrefix) break;
-    --j;
+    uint32_t s[LB];
+#pragma unroll
+    for (int q = 0; q < LB; ++q) s[q] = (j - q >= 0) ? ld_relaxed(status + (uint64_t)(j - q) * stride) : kFlagPrefix;
+#pragma unroll
+    for (int q = 0; q < LB; ++q) {
+      if (j < 0) break;
+      uint32_t v = s[q];
+      while (v == 0) v = ld_relaxed(status + (uint64_t)j * stride);  // not yet published: spin
+      excl += v & kValMask;
+      if (v & kFlagPrefix) return excl;
+      --j;
+    }
   }
   return excl;
 }

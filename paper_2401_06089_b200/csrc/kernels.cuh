@@ -1,0 +1,590 @@
+// Device kernels of the dendrogram pipeline (sm_100a).  Host orchestration
+// and the C ABI are in dmst.cu.  Reference symbols are cited as
+// file:line under /root/reference/pkg/src/dendromst/.
+#pragma once
+#include "../../include/dmst.h"
+#include "common.cuh"
+#include "radix.cuh"
+
+namespace dmst {
+
+constexpr int EW_BLOCK = 256;                  // elementwise kernels
+constexpr int SEL_BLOCK = 256, SEL_ITEMS = 8;  // select-scan tiles
+constexpr int SEL_TILE = SEL_BLOCK * SEL_ITEMS;
+constexpr int CHASE_STEPS = 16;                // V2 bounded walk before pointer jumping
+
+// ------------------------------------------------------------ key codec
+// Order-preserving map of (w + 0.0) to uint64, inverted so that ascending
+// key order is descending weight; -0.0 is canonicalised to +0.0 so the two
+// tie, as numpy's comparison does (tree_core.py:180).
+__device__ __forceinline__ uint64_t desc_key(double w) {
+  uint64_t b = (uint64_t)__double_as_longlong(w);
+  if (b == 0x8000000000000000ull) b = 0;
+  uint64_t asc = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+  return ~asc;
+}
+__device__ __forceinline__ double key_to_double(uint64_t key) {
+  uint64_t asc = ~key;
+  uint64_t b = (asc >> 63) ? (asc & 0x7fffffffffffffffull) : ~asc;
+  return __longlong_as_double((long long)b);
+}
+
+// Warp-aggregated shared-memory histogram increment (uniform-digit fast path).
+__device__ __forceinline__ void hist_add(uint32_t* h, uint32_t d, bool ok, uint32_t act) {
+  uint32_t d0 = __shfl_sync(kFull, d, 0);
+  if (__all_sync(kFull, !ok || d == d0)) {
+    if (lane_id() == 0 && act) atomicAdd(h + d0, __popc(act));
+  } else if (ok) {
+    atomicAdd(h + d, 1u);
+  }
+}
+
+// ------------------------------------------------ 1. edge sort (sort #1)
+// One read of w: all eight digit histograms + the "-0.0 present" flag.
+__global__ void __launch_bounds__(256) k_sort1_hist(const double* __restrict__ w, int64_t n,
+                                                    uint32_t* __restrict__ hist,
+                                                    uint32_t* __restrict__ negzero) {
+  __shared__ uint32_t sh[8][kRadix];
+  for (int i = threadIdx.x; i < 8 * kRadix; i += blockDim.x) (&sh[0][0])[i] = 0;
+  __syncthreads();
+  bool nz = false;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
+    const int64_t i = i0 + threadIdx.x;
+    const bool ok = i < n;
+    uint64_t key = 0;
+    if (ok) {
+      double x = ld_stream(w + i);
+      nz |= (uint64_t)__double_as_longlong(x) == 0x8000000000000000ull;
+      key = desc_key(x);
+    }
+    const uint32_t act = __ballot_sync(kFull, ok);
+#pragma unroll
+    for (int p = 0; p < 8; ++p) hist_add(sh[p], (uint32_t)(key >> (8 * p)) & 0xff, ok, act);
+  }
+  if (__any_sync(kFull, nz) && lane_id() == 0) atomicOr(negzero, 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < 8 * kRadix; i += blockDim.x) {
+    uint32_t c = (&sh[0][0])[i];
+    if (c) atomicAdd(hist + i, c);
+  }
+}
+
+// First pass: key from w; payload (original id, u, v) carried through the
+// sort so the final pass needs no random gathers.
+struct Sort1FirstLoader {
+  static constexpr int NS = 3, IPE = 1;
+  __host__ __device__ static constexpr int sb(int s) { return s == 0 ? 8 : 4; }
+  const double* __restrict__ w;
+  const int32_t* __restrict__ u;
+  const int32_t* __restrict__ v;
+  __device__ __forceinline__ const void* ptr(int s) const {
+    return s == 0 ? (const void*)w : s == 1 ? (const void*)u : (const void*)v;
+  }
+  __device__ __forceinline__ uint64_t key(int64_t i) const { return desc_key(ld_stream(w + i)); }
+  __device__ __forceinline__ void load(int64_t i, uint64_t& k, Vals<3>& p) const {
+    k = desc_key(ld_stream(w + i));
+    p.w[0] = (uint32_t)i;
+    p.w[1] = (uint32_t)ld_stream(u + i);
+    p.w[2] = (uint32_t)ld_stream(v + i);
+  }
+  __device__ __forceinline__ void get(char* const* st, int li, int64_t i, uint64_t& k, Vals<3>& p) const {
+    k = desc_key(reinterpret_cast<const double*>(st[0])[li]);
+    p.w[0] = (uint32_t)i;
+    p.w[1] = reinterpret_cast<const uint32_t*>(st[1])[li];
+    p.w[2] = reinterpret_cast<const uint32_t*>(st[2])[li];
+  }
+};
+
+// Final pass: RankedTree outputs (orig_of, w by rank) + rank-order endpoints.
+struct Sort1FinalEmitter {
+  int32_t* __restrict__ orig_of;
+  double* __restrict__ heights;
+  int2* __restrict__ euv;        // rank-order endpoints (pipeline)
+  int32_t* __restrict__ ru;      // optional split copies (dmst_rank_edges)
+  int32_t* __restrict__ rv;
+  template <int N>
+  __device__ __forceinline__ void emit(const uint32_t (&dst)[N], const uint64_t (&k)[N],
+                                       const Vals<3> (&p)[N], const bool (&ok)[N]) const {
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      if (ok[i]) {
+        const uint32_t r = dst[i];
+        orig_of[r] = (int32_t)p[i].w[0];
+        heights[r] = key_to_double(k[i]);
+        if (euv) euv[r] = make_int2((int)p[i].w[1], (int)p[i].w[2]);
+        if (ru) {
+          ru[r] = (int32_t)p[i].w[1];
+          rv[r] = (int32_t)p[i].w[2];
+        }
+      }
+  }
+};
+
+// heights were decoded from canonicalised keys; restore -0.0 bit patterns.
+__global__ void k_fix_negzero(const double* __restrict__ w, const int32_t* __restrict__ orig_of,
+                              double* __restrict__ heights, int64_t n) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n && heights[r] == 0.0) heights[r] = w[orig_of[r]];
+}
+
+// dmst_pandora entry: already-ranked endpoints -> packed euv.
+__global__ void k_pack_euv(const int32_t* __restrict__ ru, const int32_t* __restrict__ rv, int64_t n,
+                           int2* __restrict__ euv) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) euv[r] = make_int2(ru[r], rv[r]);
+}
+
+// ------------------------------------------ 2. maxIncident (scatter-max)
+// mi64[x] = max over edges j incident to x of ((j + 1) << 32 | other end):
+// the largest incident rank (maxIncident, tree_core.py:193-199 /
+// contraction.py:149-154) packed with the vertex across that edge, 0 for
+// an isolated vertex.  Records (x, j+1, other) are first partitioned by the
+// top 8 bits of x with one onesweep pass, so the atomics of concurrently
+// running CTAs hit a few MB of mi64 at a time (L2-resident) instead of the
+// whole array.
+
+// Record i of edge j = i >> 1: endpoint (i & 1), payload (j + 1, other end).
+struct EdgeRecLoader {
+  static constexpr int NS = 1, IPE = 2;
+  __host__ __device__ static constexpr int sb(int) { return 8; }
+  const int2* __restrict__ euv;
+  __device__ __forceinline__ const void* ptr(int) const { return euv; }
+  __device__ __forceinline__ uint32_t key(int64_t i) const {
+    int2 e = __ldg(euv + (i >> 1));
+    return (uint32_t)((i & 1) ? e.y : e.x);
+  }
+  __device__ __forceinline__ void load(int64_t i, uint32_t& k, Vals<2>& p) const {
+    int2 e = __ldg(euv + (i >> 1));
+    const bool second = i & 1;
+    k = (uint32_t)(second ? e.y : e.x);
+    p.w[0] = (uint32_t)(i >> 1) + 1u;
+    p.w[1] = (uint32_t)(second ? e.x : e.y);
+  }
+  __device__ __forceinline__ void get(char* const* st, int li, int64_t i, uint32_t& k, Vals<2>& p) const {
+    int2 e = reinterpret_cast<const int2*>(st[0])[li >> 1];
+    const bool second = i & 1;
+    k = (uint32_t)(second ? e.y : e.x);
+    p.w[0] = (uint32_t)(i >> 1) + 1u;
+    p.w[1] = (uint32_t)(second ? e.x : e.y);
+  }
+};
+
+// Materialised records (levels >= 1): SoA (vertex, j + 1, other).
+using RecLoader = ArrayLoader<uint32_t, 2>;
+
+__device__ __forceinline__ unsigned long long pack_mi(uint32_t j1, uint32_t other) {
+  return ((unsigned long long)j1 << 32) | other;
+}
+
+// Apply partitioned records in order (a grid-stride sweep keeps the active
+// window to ~1-2 vertex buckets).
+__global__ void __launch_bounds__(256) k_mi_apply(const uint32_t* __restrict__ vtx,
+                                                  const uint32_t* __restrict__ j1,
+                                                  const uint32_t* __restrict__ oth, int64_t m,
+                                                  unsigned long long* __restrict__ mi64) {
+  constexpr int U = 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x * U + threadIdx.x; b < m; b += stride) {
+    uint32_t x[U], a[U], o[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      int64_t i = b + (int64_t)q * blockDim.x;
+      if (i < m) {
+        x[q] = ld_stream(vtx + i);
+        a[q] = ld_stream(j1 + i);
+        o[q] = ld_stream(oth + i);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      int64_t i = b + (int64_t)q * blockDim.x;
+      if (i < m) atomicMax(mi64 + x[q], pack_mi(a[q], o[q]));
+    }
+  }
+}
+
+// Direct (unpartitioned) scatter-max, for views small enough to sit in L2.
+__global__ void k_mi_direct(const int2* __restrict__ euv, int64_t n, unsigned long long* __restrict__ mi64) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) {
+    int2 e = euv[j];
+    atomicMax(mi64 + e.x, pack_mi((uint32_t)j + 1u, (uint32_t)e.y));
+    atomicMax(mi64 + e.y, pack_mi((uint32_t)j + 1u, (uint32_t)e.x));
+  }
+}
+
+// --------------------------------------------- 3. contraction (per view)
+// View k: nv vertices, ne edges (local index j, ascending global rank
+// grank[j]; view 0: grank = identity), mi64 as above.
+//
+// V1: per vertex, the maxIncident edge j (vertex_parent for view 0,
+// classify.py:23-25; super_max_incident in global ranks for views >= 1,
+// contraction.py:173-175) and the per-edge count of endpoints at which the
+// edge is maxIncident, as a 2-bit field: 2 = leaf, 1 = chain, 0 = alpha
+// (edge_kinds_from_ends, classify.py:37-42).
+__global__ void k_v1(int64_t nv, const unsigned long long* __restrict__ mi64,
+                     const int32_t* __restrict__ grank, int32_t* __restrict__ parent_out,
+                     uint32_t* __restrict__ cnt2) {
+  int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= nv) return;
+  const unsigned long long m = ld_stream(mi64 + x);
+  const uint32_t j1 = (uint32_t)(m >> 32);
+  int32_t out = -1;
+  if (j1) {
+    const uint32_t j = j1 - 1;
+    out = grank ? __ldg(grank + j) : (int32_t)j;
+    atomicAdd(cnt2 + (j >> 4), 1u << ((j & 15) * 2));
+  }
+  parent_out[x] = out;
+}
+
+__device__ __forceinline__ uint32_t leaf_bits(uint32_t w) { return (w >> 1) & 0x55555555u; }
+__device__ __forceinline__ uint32_t chain_bits(uint32_t w) { return w & 0x55555555u; }
+
+// Exclusive prefix of leaf-edge counts per 16-edge word (single pass,
+// decoupled look-back) + view totals (n_leaf, n_chain).  A supervertex is
+// numbered by the rank order of its component's leaf edge, so
+// label(leaf j) = leafpre[j >> 4] + leaves below j in its word: a lookup
+// into two L2-resident arrays (n/4 bytes each) instead of a scan over
+// vertices and a gather.
+__global__ void __launch_bounds__(256) k_leafscan(int64_t words, const uint32_t* __restrict__ cnt2,
+                                                  uint32_t* __restrict__ leafpre, uint32_t* __restrict__ status,
+                                                  uint32_t* __restrict__ tile_ctr, uint32_t* __restrict__ counts) {
+  constexpr int ITEMS = 8, TILE = 256 * ITEMS;
+  __shared__ uint32_t s_tile, s_excl;
+  __shared__ uint32_t scratch[256 / 32 + 1];
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const int64_t base = (int64_t)tile * TILE + (int64_t)threadIdx.x * ITEMS;
+  uint32_t lc[ITEMS], sum = 0, chains = 0;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    uint32_t w = base + i < words ? cnt2[base + i] : 0u;
+    lc[i] = __popc(leaf_bits(w));
+    chains += __popc(chain_bits(w));
+    sum += lc[i];
+  }
+  uint32_t total;
+  uint32_t excl = block_excl_sum<256>(sum, scratch, &total);
+  if (threadIdx.x == 0) {
+    uint32_t prev = 0;
+    if (tile == 0) {
+      st_relaxed(status, kFlagPrefix | total);
+    } else {
+      st_relaxed(status + tile, kFlagAgg | total);
+      prev = lookback(status, tile, 1);
+      st_relaxed(status + tile, kFlagPrefix | (prev + total));
+    }
+    s_excl = prev;
+    atomicAdd(counts + 0, total);
+  }
+  uint32_t ctot;
+  block_excl_sum<256>(chains, scratch, &ctot);
+  if (threadIdx.x == 0) atomicAdd(counts + 1, ctot);
+  __syncthreads();
+  uint32_t run = s_excl + excl;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    if (base + i < words) leafpre[base + i] = run;
+    run += lc[i];
+  }
+}
+
+__device__ __forceinline__ uint32_t leaf_label(const uint32_t* __restrict__ cnt2,
+                                               const uint32_t* __restrict__ leafpre, uint32_t j) {
+  const uint32_t w = cnt2[j >> 4];
+  const uint32_t below = (1u << ((j & 15) * 2)) - 1u;
+  return leafpre[j >> 4] + __popc(leaf_bits(w) & below);
+}
+
+// V2: chase maxIncident pointers to the component's leaf edge (ranks grow
+// strictly along the chase; the leaf edge is the component's lightest
+// edge) and label the vertex with that leaf's number: vertex_map
+// (component_labels + contract_level, contraction.py:82-93, :165-169).
+// Vertices still unresolved after CHASE_STEPS (deep in-trees: chains)
+// store ~y (y = the vertex where the chase stopped) and go to pointer jumping.
+__global__ void k_v2(int64_t nv, const unsigned long long* __restrict__ mi64,
+                     const uint32_t* __restrict__ cnt2, const uint32_t* __restrict__ leafpre,
+                     int32_t* __restrict__ vm, int32_t* __restrict__ active, uint32_t* __restrict__ active_cnt) {
+  const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool unresolved = false;
+  if (x < nv) {
+    unsigned long long m = ld_stream(mi64 + x);
+    uint32_t j = (uint32_t)(m >> 32) - 1u;
+    uint32_t y = (uint32_t)m;
+    int s = 0;
+    while (m != 0ull) {  // m == 0: isolated vertex (single-vertex view), label 0
+      const uint32_t c = (cnt2[j >> 4] >> ((j & 15) * 2)) & 3u;
+      if (c == 2u) break;
+      if (++s > CHASE_STEPS) {
+        unresolved = true;
+        break;
+      }
+      m = mi64[y];
+      j = (uint32_t)(m >> 32) - 1u;
+      y = (uint32_t)m;
+    }
+    vm[x] = unresolved ? ~(int32_t)y : (m ? (int32_t)leaf_label(cnt2, leafpre, j) : 0);
+  }
+  const uint32_t msk = __ballot_sync(kFull, unresolved);
+  if (msk) {
+    uint32_t lead = __ffs(msk) - 1, b = 0;
+    if (lane_id() == lead) b = atomicAdd(active_cnt, __popc(msk));
+    b = __shfl_sync(kFull, b, lead);
+    if (unresolved) active[b + __popc(msk & lanemask_lt())] = (int32_t)x;
+  }
+}
+
+// One pointer-jumping round over unresolved vertices: vm[x] >= 0 is a label,
+// vm[x] < 0 is ~(a vertex further along the chase).  Pointers only ever
+// move forward along the chase, so in-place updates are safe.
+__global__ void k_jump(const int32_t* __restrict__ in, const uint32_t* __restrict__ in_cnt,
+                       int32_t* __restrict__ out, uint32_t* __restrict__ out_cnt, int32_t* vm) {
+  const uint32_t cnt = *in_cnt;
+  for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x; t0 < cnt; t0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = t0 + threadIdx.x;
+    bool again = false;
+    int32_t x = 0;
+    if (t < cnt) {
+      x = in[t];
+      const int32_t q = vm[~vm[x]];
+      vm[x] = q;
+      again = q < 0;
+    }
+    const uint32_t m = __ballot_sync(kFull, again);
+    if (m) {
+      uint32_t lead = __ffs(m) - 1, b = 0;
+      if (lane_id() == lead) b = atomicAdd(out_cnt, __popc(m));
+      b = __shfl_sync(kFull, b, lead);
+      if (again) out[b + __popc(m & lanemask_lt())] = x;
+    }
+  }
+}
+
+// Order-preserving select: single pass, decoupled look-back over tiles.
+// Items are warp-striped (coalesced); rank order = index order.
+template <class Sel>
+__global__ void __launch_bounds__(SEL_BLOCK)
+k_select(int64_t n, uint32_t* __restrict__ status, uint32_t* __restrict__ tile_ctr,
+         uint32_t* __restrict__ totals, Sel sel) {
+  constexpr int NW = SEL_BLOCK / 32;
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_warp[NW + 1];
+  __shared__ uint32_t s_excl;
+  __shared__ typename Sel::Shared s_sel;
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  sel.init_shared(s_sel);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const int64_t wbase = (int64_t)tile * SEL_TILE + (int64_t)warp * SEL_ITEMS * 32 + lane;
+  const uint32_t lt = lanemask_lt();
+
+  typename Sel::Item it[SEL_ITEMS];
+  uint32_t wpos[SEL_ITEMS];
+  bool flag[SEL_ITEMS];
+  uint32_t run = 0;
+#pragma unroll
+  for (int i = 0; i < SEL_ITEMS; ++i) {
+    int64_t idx = wbase + (int64_t)i * 32;
+    flag[i] = idx < n ? sel.flag(idx, it[i]) : false;
+    uint32_t b = __ballot_sync(kFull, flag[i]);
+    wpos[i] = run + __popc(b & lt);
+    run += __popc(b);
+  }
+  if (lane == 0) s_warp[warp] = run;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t c = lane < NW ? s_warp[lane] : 0;
+    uint32_t incl = warp_incl_sum(c);
+    if (lane < NW) s_warp[lane] = incl - c;
+    uint32_t total = __shfl_sync(kFull, incl, NW - 1);
+    if (lane == 0) {
+      uint32_t excl = 0;
+      if (tile == 0) {
+        st_relaxed(status, kFlagPrefix | total);
+      } else {
+        st_relaxed(status + tile, kFlagAgg | total);
+        excl = lookback(status, tile, 1);
+        st_relaxed(status + tile, kFlagPrefix | (excl + total));
+      }
+      s_excl = excl;
+      if (tile == gridDim.x - 1) totals[0] = excl + total;
+    }
+  }
+  __syncthreads();
+  const uint32_t base = s_excl + s_warp[warp];
+#pragma unroll
+  for (int i = 0; i < SEL_ITEMS; ++i) {
+    int64_t idx = wbase + (int64_t)i * 32;
+    if (idx < n) sel.emit(idx, flag[i], base + wpos[i], it[i], s_sel);
+  }
+  __syncthreads();
+  sel.flush_shared(s_sel);
+}
+
+// Retire non-alpha edges of view k at level k (contraction.py:207) and
+// compact alpha edges, in rank order, into view k+1 with endpoints remapped
+// to supervertices (:170-172).  The next view's maxIncident is either
+// scatter-maxed directly (small views) or emitted as records for the
+// multisplit + apply path.
+struct EdgeSel {
+  uint32_t* __restrict__ cnt2;       // read, then zeroed for the next view
+  const int2* __restrict__ euv;
+  const int32_t* __restrict__ grank; // null => identity (view 0)
+  const int32_t* __restrict__ vm;
+  int8_t* __restrict__ ret;
+  int2* __restrict__ euv_next;
+  int32_t* __restrict__ grank_next;
+  unsigned long long* __restrict__ mi64_next;  // direct mode (null => records)
+  uint32_t* __restrict__ rec_vtx;
+  uint32_t* __restrict__ rec_j1;
+  uint32_t* __restrict__ rec_oth;
+  int8_t level;
+  struct Item {
+    int32_t g;
+  };
+  struct Shared {};
+  __device__ __forceinline__ void init_shared(Shared&) const {}
+  __device__ __forceinline__ void flush_shared(Shared&) const {}
+  __device__ __forceinline__ bool flag(int64_t j, Item& it) const {
+    uint32_t c = (cnt2[j >> 4] >> ((j & 15) * 2)) & 3u;
+    it.g = grank ? grank[j] : (int32_t)j;
+    return c == 0;
+  }
+  __device__ __forceinline__ void emit(int64_t j, bool alpha, uint32_t pos, const Item& it, Shared&) const {
+    if ((j & 15) == 0) cnt2[j >> 4] = 0u;
+    if (!alpha) {
+      ret[it.g] = level;
+    } else {
+      int2 e = euv[j];
+      int32_t a = vm[e.x], b = vm[e.y];
+      euv_next[pos] = make_int2(a, b);
+      grank_next[pos] = it.g;
+      if (mi64_next) {
+        atomicMax(mi64_next + a, pack_mi(pos + 1u, (uint32_t)b));
+        atomicMax(mi64_next + b, pack_mi(pos + 1u, (uint32_t)a));
+      } else {
+        rec_vtx[2 * pos] = (uint32_t)a;
+        rec_j1[2 * pos] = pos + 1u;
+        rec_oth[2 * pos] = (uint32_t)b;
+        rec_vtx[2 * pos + 1] = (uint32_t)b;
+        rec_j1[2 * pos + 1] = pos + 1u;
+        rec_oth[2 * pos + 1] = (uint32_t)a;
+      }
+    }
+  }
+};
+
+// Final view (no alpha edges, contraction.py:203-205): every edge retires at L.
+__global__ void k_retire_all(int64_t n, const int32_t* __restrict__ grank, int8_t* __restrict__ ret, int8_t L) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) ret[grank ? grank[j] : j] = L;
+}
+
+// ------------------------------------------------------ 4. expansion walk
+struct LevelTable {
+  int64_t voff[DMST_MAX_LEVELS + 1];  // offset of vertex_map of view k in vm_all
+  int64_t soff[DMST_MAX_LEVELS + 2];  // offset of maxIncident (global ranks) of view k in smi_all
+  int32_t L;
+};
+
+// assign_chains (expansion.py:97-128): an edge retired at view r is tried
+// at views r+1..L; the first whose supervertex parent p satisfies
+// 0 <= p < e wins.  The chain (terminal, anchor) is encoded as the dense key
+// 1 + soff[k] + anchor (a terminal edge is a terminal only at the one level
+// it retires at, so (level, anchor) identifies the chain); 0 = root chain.
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK)
+k_walk(int64_t n, const int8_t* __restrict__ ret, const int2* __restrict__ euv,
+       const int32_t* __restrict__ vm_all, const int32_t* __restrict__ smi_all,
+       const __grid_constant__ LevelTable lt, uint32_t* __restrict__ keys,
+       uint32_t* __restrict__ hist, int digits) {
+  __shared__ uint32_t sh[4][kRadix];
+  for (int i = threadIdx.x; i < 4 * kRadix; i += BLOCK) (&sh[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * BLOCK;
+  for (int64_t e0 = (int64_t)blockIdx.x * BLOCK; e0 < n; e0 += stride) {
+    const int64_t e = e0 + threadIdx.x;
+    const bool ok = e < n;
+    uint32_t key = 0;
+    if (ok) {
+      const int r = ret[e];
+      if (r < lt.L) {
+        int32_t x = euv[e].x;
+        for (int k = 0; k < r; ++k) x = vm_all[lt.voff[k] + x];
+        for (int k = r + 1; k <= lt.L; ++k) {
+          x = vm_all[lt.voff[k - 1] + x];
+          int32_t p = smi_all[lt.soff[k] + x];
+          if (p >= 0 && p < (int32_t)e) {
+            key = (uint32_t)(1 + lt.soff[k] + x);
+            break;
+          }
+        }
+      }
+      keys[e] = key;
+    }
+    const uint32_t act = __ballot_sync(kFull, ok);
+    for (int p = 0; p < digits; ++p) hist_add(sh[p], (key >> (8 * p)) & 0xff, ok, act);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < digits * kRadix; i += BLOCK) {
+    uint32_t c = (&sh[0][0])[i];
+    if (c) atomicAdd(hist + i, c);
+  }
+}
+
+struct Sort2FirstLoader {
+  static constexpr int NS = 1, IPE = 1;
+  __host__ __device__ static constexpr int sb(int) { return 4; }
+  const uint32_t* __restrict__ keys;
+  __device__ __forceinline__ const void* ptr(int) const { return keys; }
+  __device__ __forceinline__ uint32_t key(int64_t i) const { return ld_stream(keys + i); }
+  __device__ __forceinline__ void load(int64_t i, uint32_t& k, Vals<1>& v) const {
+    k = ld_stream(keys + i);
+    v.w[0] = (uint32_t)i;
+  }
+  __device__ __forceinline__ void get(char* const* st, int li, int64_t i, uint32_t& k, Vals<1>& v) const {
+    k = reinterpret_cast<const uint32_t*>(st[0])[li];
+    v.w[0] = (uint32_t)i;
+  }
+};
+
+// stitch_chains (expansion.py:131-145): in (key, rank) order the parent of
+// an edge is its predecessor in the same chain, or the chain's terminal.
+__global__ void k_link(int64_t n, const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
+                       const int32_t* __restrict__ smi_all, int32_t* __restrict__ edge_parent) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t key = skeys[i];
+  uint32_t e = svals ? svals[i] : (uint32_t)i;
+  int32_t parent;
+  if (i > 0 && skeys[i - 1] == key)
+    parent = svals ? (int32_t)svals[i - 1] : (int32_t)(i - 1);
+  else
+    parent = key == 0 ? -1 : smi_all[key - 1];
+  edge_parent[e] = parent;
+}
+
+// Debug: ChainAssignment.terminal / .level from the dense key.
+__global__ void k_debug_chain(int64_t n, const uint32_t* __restrict__ keys,
+                              const int32_t* __restrict__ smi_all, const __grid_constant__ LevelTable lt,
+                              int32_t* __restrict__ key_out, int32_t* __restrict__ term,
+                              int32_t* __restrict__ lvl) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  uint32_t key = keys[e];
+  if (key_out) key_out[e] = (int32_t)key;
+  int32_t t = -1, l = 0;
+  if (key) {
+    t = smi_all[key - 1];
+    l = 1;
+    while (l < lt.L && (int64_t)(key - 1) >= lt.soff[l + 1]) ++l;
+  }
+  if (term) term[e] = t;
+  if (lvl) lvl[e] = l;
+}
+
+}  // namespace dmst

@@ -10,8 +10,9 @@
 //     (original id, u, v) so the last pass writes orig_of, heights (decoded
 //     from the key) and rank-order endpoints without random gathers.
 //  2. maxIncident      build_incidence       tree_core.py:193-199
-//     records (x, rank, other end) partitioned by vertex bucket (one
-//     radix pass), then L2-resident 64-bit atomicMax (k_mi_apply).
+//     records (x, rank, other end) grouped by 8192-vertex bucket with two
+//     order-free multisplit passes (bucket.cuh), then reduced per bucket in
+//     shared memory (k_mi_apply_smem, fused with V1).
 //  3. contraction      build_hierarchy       contraction.py:186-219
 //     per view k: k_v1 (maxIncident + 2-bit child counts), k_leafscan
 //     (leaf-edge numbering = supervertex ids), k_v2 (chase to the leaf
@@ -35,8 +36,6 @@ namespace dmst {
 // Radix sort geometry (sub-tile = BLOCK x ITEMS items; MINB CTAs per SM).
 // Edge sort: u64 key + 3-word payload.
 constexpr int S1_BLOCK = 256, S1_ITEMS = 6, S1_MINB = 2;
-// Multisplit of maxIncident records: u32 key + 2-word payload.
-constexpr int MS_BLOCK = 256, MS_ITEMS = 8, MS_MINB = 2;
 // Chain sort: u32 key + 1-word payload.
 constexpr int S2_BLOCK = 256, S2_ITEMS = 16, S2_MINB = 2;
 constexpr int64_t kDirectMiBytes = 24ll << 20;  // direct scatter-max below this mi64 size
@@ -77,19 +76,14 @@ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 inline unsigned grid_for(int64_t n, int block) { return (unsigned)std::max<int64_t>(1, cdiv(n, block)); }
 
-int bits_for(int64_t maxval) {  // number of bits to represent [0, maxval]
-  int b = 0;
-  while (b < 63 && (maxval >> b)) ++b;
-  return b;
-}
-int vshift_for(int64_t nv) { return std::max(0, bits_for(nv - 1) - 8); }
 
 // Workspace carve-up; the same code sizes and assigns it.
-//  R (40n B): edge sort ping-pong (keys 2x8n, payload 2x3x4n); later
-//             maxIncident records, jump lists, chain-sort buffers.
+//  R (48n B): edge sort ping-pong (keys 2x8n, payload 2x3x4n); later
+//             maxIncident records (2 x 24n), jump lists, chain-sort buffers.
 struct Workspace {
   char* R;
   uint32_t* counts;       // radix per-chunk digit counts [256][kMaxChunks]
+  uint32_t* fine;         // bucketing: counts, base, cursors (fine), cursors (coarse)
   uint32_t* small;        // counters/histograms (zeroed per use)
   int2* euv0;             // rank-order endpoints
   unsigned long long* mi64_0;
@@ -123,8 +117,9 @@ Workspace carve(int64_t n, int64_t nv, char* base) {
     return p;
   };
   const int64_t half = n / 2 + 1;
-  w.R = take(40 * n + 4096);
+  w.R = take(48 * n + 4096);
   w.counts = (uint32_t*)take(4 * kRadix * kMaxChunks);
+  w.fine = (uint32_t*)take(4 * (4 * (nv / FB + 2) + 512));
   w.small = (uint32_t*)take(4 * kSmallWords);
   w.euv0 = (int2*)take(8 * n);
   w.mi64_0 = (unsigned long long*)take(8 * nv);
@@ -314,27 +309,48 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
   }
 }
 
-// Partition m maxIncident records by vertex bucket (top 8 bits of the
-// vertex id) and apply them with L2-resident 64-bit atomicMax.
-template <class Loader>
-void mi_multisplit(Ctx& c, int64_t m, int64_t nv, Loader ld, unsigned long long* mi64) {
-  const int vshift = vshift_for(nv);
-  // partitioned records live at R[0, 12m)
-  uint32_t* rv = (uint32_t*)c.w.R;
-  uint32_t* rj = rv + m;
-  uint32_t* ro = rj + m;
-  uint32_t* const bufK[2] = {rv, rv};
-  uint32_t* const bufV[2][2] = {{rj, ro}, {rj, ro}};
-  ArrayEmitter<uint32_t, 2> fin;
-  fin.keys = rv;
-  fin.vals[0] = rj;
-  fin.vals[1] = ro;
-  run_sort<uint32_t, 2, MS_BLOCK, MS_ITEMS, MS_MINB>(c, {KK_MI_SPLIT, KK_MI_SPLIT, KK_MI_SPLIT}, m, {vshift},
-                                                     bufK, bufV, ld, fin);
-  c.zero(mi64, 8 * nv);
-  c.begin(KK_MI_APPLY);
-  k_mi_apply<<<c.persistent_grid(m, 256 * 4, 8), 256, 0, c.s>>>(rv, rj, ro, m, mi64);
+// maxIncident of a view from m records: fine-bucket histogram, two
+// order-free multisplit passes (coarse, fine) and the per-bucket shared-memory
+// reduction, which also performs V1 for the view.  `in`/`mid`/`fin` are
+// record buffers (mid and fin must not overlap the source).
+template <class Src>
+void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiApplyOut out) {
+  const uint32_t nf = (uint32_t)cdiv(nv, FB);
+  uint32_t gshift = 0;  // coarse bucket = 2^gshift fine buckets, <= 256 coarse buckets
+  while ((int64_t(nf) >> gshift) > 255) ++gshift;
+  uint32_t* counts = c.w.fine;
+  uint32_t* fine_base = counts + (nf + 2);
+  uint32_t* fine_cur = fine_base + (nf + 2);
+  uint32_t* coarse_cur = fine_cur + (nf + 2);
+  c.zero(counts, 4 * (nf + 1));
+  DMST_CUDA(cudaFuncSetAttribute(k_fine_hist<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * FH_WINDOW));
+  for (uint32_t flo = 0; flo < nf; flo += FH_WINDOW) {
+    c.begin(KK_MI_SPLIT);
+    k_fine_hist<Src><<<c.persistent_grid(m, 256, 3), 256, 4 * FH_WINDOW, c.s>>>(src, m, flo, nf, counts);
+    c.launched();
+  }
+  c.begin(KK_MI_SPLIT);
+  k_fine_scan<<<1, 1024, 0, c.s>>>(counts, nf, gshift, fine_base, fine_cur, coarse_cur);
   c.launched();
+  constexpr size_t smA = bucket_smem_bytes<false>(), smB = bucket_smem_bytes<true>();
+  DMST_CUDA(cudaFuncSetAttribute(k_bucket<false, Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA));
+  DMST_CUDA(cudaFuncSetAttribute(k_bucket<true, SoaRecSrc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smB));
+  c.begin(KK_MI_SPLIT);
+  k_bucket<false, Src><<<c.persistent_grid(m, BK_T, 3), BK_BLOCK, smA, c.s>>>(src, m, gshift, coarse_cur, mid);
+  c.launched();
+  c.begin(KK_MI_SPLIT);
+  k_bucket<true, SoaRecSrc><<<c.persistent_grid(m, BK_T, 2), BK_BLOCK, smB, c.s>>>(SoaRecSrc{mid.x, mid.j1, mid.o}, m,
+                                                                                   gshift, fine_cur, fin);
+  c.launched();
+  DMST_CUDA(cudaFuncSetAttribute(k_mi_apply_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * FB));
+  c.begin(KK_MI_APPLY);
+  k_mi_apply_smem<<<nf, 512, 8 * FB, c.s>>>(fin, fine_base, nv, out);
+  c.launched();
+}
+
+Recs recs_at(char* base, int64_t m) {
+  uint32_t* p = (uint32_t*)base;
+  return Recs{p, p + m, p + 2 * m};
 }
 
 // Full pipeline after the edge sort: euv0 (rank-order endpoints) ready.
@@ -343,9 +359,11 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
   Workspace& w = c.w;
   uint32_t* misc = w.small + SM_MISC;
 
-  // maxIncident of the input view (multisplit: 2n records generated from euv0)
-  mi_multisplit(c, 2 * n, nv, EdgeRecLoader{w.euv0}, w.mi64_0);
+  // maxIncident + V1 of the input view: 2n records generated from euv0
   c.zero(w.cnt2, 4 * (n / 16 + 2));
+  mi_buckets(c, EdgeRecSrc{w.euv0}, 2 * n, nv, recs_at(w.R, 2 * n), recs_at(w.R + 24 * n, 2 * n),
+             MiApplyOut{w.mi64_0, vertex_parent, nullptr, w.cnt2});
+  bool v1_done = true;
 
   LevelTable lt{};
   int64_t nv_k = nv, n_k = n;
@@ -358,16 +376,14 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
   uint32_t* lcnt[3] = {misc + MISC_ACTIVE0, misc + MISC_ACTIVE1, misc + MISC_ACTIVE2};
   while (true) {
     if (level >= DMST_MAX_LEVELS) invalid("too many contraction levels");
-    // V1: maxIncident edge per vertex + child counts per edge
-    int32_t* parent_out = vertex_parent;
-    if (level >= 1) {
-      lt.soff[level] = soff;
-      parent_out = w.smi_all + soff;
-      soff += nv_k;
+    // V1: maxIncident edge per vertex + child counts per edge (already done
+    // by the bucketed apply unless the view was small enough for direct atomics)
+    if (!v1_done) {
+      int32_t* parent_out = w.smi_all + lt.soff[level];
+      c.begin(KK_V1);
+      k_v1<<<grid_for(nv_k, EW_BLOCK), EW_BLOCK, 0, c.s>>>(nv_k, mi_k, grank_k, parent_out, w.cnt2);
+      c.launched();
     }
-    c.begin(KK_V1);
-    k_v1<<<grid_for(nv_k, EW_BLOCK), EW_BLOCK, 0, c.s>>>(nv_k, mi_k, grank_k, parent_out, w.cnt2);
-    c.launched();
     // leaf numbering + kind counts
     const int64_t words = n_k / 16 + 1;
     c.zero(w.sel_status, 4 * (cdiv(words, 2048) + 1));
@@ -430,8 +446,10 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     const int64_t nv_next = n_leaf, n_next = n_alpha;
     const bool direct = nv_next * 8 <= kDirectMiBytes;
     unsigned long long* mi_next = w.mi64[cur ^ 1];
-    // unpartitioned records of view level+1 at R[24n, 36n)
+    // records of view level+1: R[24n, 36n); bucketing mid buffer R[0, 12n)
     uint32_t* rec = (uint32_t*)(w.R + 24 * n);
+    lt.soff[level + 1] = soff;
+    soff += nv_next;
     if (direct) c.zero(mi_next, 8 * nv_next);
     EdgeSel es;
     es.cnt2 = w.cnt2;
@@ -456,8 +474,14 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
                                                                 misc + MISC_SELTOT, es);
       c.launched();
     }
-    if (!direct && n_next > 0)
-      mi_multisplit(c, 2 * n_next, nv_next, RecLoader{es.rec_vtx, {es.rec_j1, es.rec_oth}}, mi_next);
+    v1_done = false;
+    if (!direct && n_next > 0) {
+      const int64_t m = 2 * n_next;
+      mi_buckets(c, SoaRecSrc{es.rec_vtx, es.rec_j1, es.rec_oth}, m, nv_next, recs_at(w.R, m),
+                 Recs{es.rec_vtx, es.rec_j1, es.rec_oth},
+                 MiApplyOut{mi_next, w.smi_all + lt.soff[level + 1], w.grank[cur ^ 1], w.cnt2});
+      v1_done = true;
+    }
     // next view
     euv_k = w.euv[cur ^ 1];
     grank_k = w.grank[cur ^ 1];

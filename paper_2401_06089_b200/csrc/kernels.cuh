@@ -5,6 +5,7 @@
 #include "../../include/dmst.h"
 #include "common.cuh"
 #include "radix.cuh"
+#include "bucket.cuh"
 
 namespace dmst {
 

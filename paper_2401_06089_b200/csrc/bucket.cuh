@@ -249,51 +249,35 @@ struct MiApplyOut {
 
 __global__ void __launch_bounds__(512) k_mi_apply_smem(Recs rec, const uint32_t* __restrict__ fine_base,
                                                        int64_t nv, MiApplyOut out) {
-  extern __shared__ uint32_t sm[];
-  uint32_t* best = sm;       // [FB] max (j + 1)
-  uint32_t* other = sm + FB; // [FB]
+  extern __shared__ unsigned long long smi[];  // [FB] max ((j + 1) << 32 | other)
   const uint32_t f = blockIdx.x;
   const int64_t v0 = (int64_t)f << FB_BITS;
-  for (int i = threadIdx.x; i < FB; i += blockDim.x) best[i] = 0;
+  for (int i = threadIdx.x; i < FB; i += blockDim.x) smi[i] = 0ull;
   __syncthreads();
   const uint32_t rb = fine_base[f], re = fine_base[f + 1];
   constexpr int U = 8;
   const uint32_t step = blockDim.x * U;
   for (uint32_t b = rb + threadIdx.x; b < re; b += step) {
-    uint32_t xl[U], jj[U];
+    uint32_t xl[U];
+    unsigned long long pk[U];
 #pragma unroll
     for (int q = 0; q < U; ++q) {
       const uint32_t i = b + q * blockDim.x;
       xl[q] = i < re ? ld_stream(rec.x + i) - (uint32_t)v0 : 0u;
-      jj[q] = i < re ? ld_stream(rec.j1 + i) : 0u;
+      pk[q] = i < re ? ((unsigned long long)ld_stream(rec.j1 + i) << 32) | ld_stream(rec.o + i) : 0ull;
     }
 #pragma unroll
     for (int q = 0; q < U; ++q)
-      if (jj[q]) atomicMax(&best[xl[q]], jj[q]);
-  }
-  __syncthreads();
-  for (uint32_t b = rb + threadIdx.x; b < re; b += step) {
-    uint32_t xl[U], jj[U], oo[U];
-#pragma unroll
-    for (int q = 0; q < U; ++q) {
-      const uint32_t i = b + q * blockDim.x;
-      xl[q] = i < re ? rec.x[i] - (uint32_t)v0 : 0u;
-      jj[q] = i < re ? rec.j1[i] : 0u;
-      oo[q] = i < re ? rec.o[i] : 0u;
-    }
-#pragma unroll
-    for (int q = 0; q < U; ++q)
-      if (jj[q] && jj[q] == best[xl[q]]) other[xl[q]] = oo[q];
+      if (pk[q]) atomicMax(&smi[xl[q]], pk[q]);
   }
   __syncthreads();
   const int lim = nv - v0 < FB ? (int)(nv - v0) : FB;
   for (int i = threadIdx.x; i < lim; i += blockDim.x) {
-    const uint32_t b = best[i];
+    const unsigned long long m = smi[i];
+    const uint32_t b = (uint32_t)(m >> 32);
     int32_t par = -1;
-    unsigned long long m = 0;
     if (b) {
       const uint32_t j = b - 1;
-      m = ((unsigned long long)b << 32) | other[i];
       par = out.grank ? __ldg(out.grank + j) : (int32_t)j;
       atomicAdd(out.cnt2 + (j >> 4), 1u << ((j & 15) * 2));
     }

@@ -268,33 +268,32 @@ void run_sort(Ctx& c, const int (&kinds)[3], int64_t n, const std::vector<int>& 
   }
 }
 
-// Digits whose histogram is not concentrated in one bin.
-void active_digits(const std::vector<uint32_t>& h, int digits, int64_t n, std::vector<int>& shifts) {
-  shifts.clear();
-  for (int d = 0; d < digits; ++d) {
-    bool constant = false;
-    for (int b = 0; b < kRadix; ++b)
-      if (h[d * kRadix + b] == (uint32_t)n) constant = true;
-    if (!constant) shifts.push_back(8 * d);
-  }
+// Radix digits (8-bit, at bit offsets 0, 8, ...) that are not constant
+// across all keys, from the AND / OR of every key.
+std::vector<int> active_digits(uint64_t key_and, uint64_t key_or, int digits) {
+  std::vector<int> shifts;
+  for (int d = 0; d < digits; ++d)
+    if (((key_and ^ key_or) >> (8 * d)) & 0xff) shifts.push_back(8 * d);
+  return shifts;
 }
 
 // Sort #1 (rank_edges): orig_of, heights, euv (and/or ru, rv).
 void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int64_t n,
                Sort1FinalEmitter em, int* passes_out) {
-  uint32_t* hist = c.w.small + SM_HIST1;
+  unsigned long long* and_or = (unsigned long long*)(c.w.small + SM_HIST1);
   uint32_t* negzero = c.w.small + SM_MISC + MISC_NEGZERO;
-  c.zero(hist, 8 * kRadix * 4);
+  const unsigned long long init[2] = {~0ull, 0ull};
+  DMST_CUDA(cudaMemcpyAsync(and_or, init, 16, cudaMemcpyHostToDevice, c.s));
   c.zero(negzero, 4);
   c.begin(KK_SORT1_HIST);
-  k_sort1_hist<<<c.persistent_grid(n, 256, 8), 256, 0, c.s>>>(w, n, hist, negzero);
+  k_key_reduce<<<c.persistent_grid(n, 256 * 4, 8), 256, 0, c.s>>>(w, n, and_or, negzero);
   c.launched();
-  std::vector<uint32_t> h(8 * kRadix + 1);
-  c.to_host(h.data(), hist, 8 * kRadix * 4);
-  c.to_host(h.data() + 8 * kRadix, negzero, 4);
+  unsigned long long ao[2];
+  uint32_t nz = 0;
+  c.to_host(ao, and_or, 16);
+  c.to_host(&nz, negzero, 4);
   c.sync();
-  std::vector<int> shifts;
-  active_digits(h, 8, n, shifts);
+  const std::vector<int> shifts = active_digits(ao[0], ao[1], 8);
   if (passes_out) *passes_out = (int)shifts.size();
   char* R = c.w.R;
   uint64_t* const bufK[2] = {(uint64_t*)R, (uint64_t*)(R + 8 * n)};
@@ -302,7 +301,7 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
   uint32_t* const bufV[2][3] = {{vb, vb + n, vb + 2 * n}, {vb + 3 * n, vb + 4 * n, vb + 5 * n}};
   run_sort<uint64_t, 3, S1_BLOCK, S1_ITEMS, S1_MINB>(c, {KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL}, n,
                                                      shifts, bufK, bufV, Sort1FirstLoader{w, u, v}, em);
-  if (h[8 * kRadix]) {
+  if (nz) {
     c.begin(KK_OTHER);
     k_fix_negzero<<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(w, em.orig_of, em.heights, n);
     c.launched();
@@ -342,7 +341,7 @@ void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiAp
   k_bucket<true, SoaRecSrc><<<c.persistent_grid(m, BK_T, 2), BK_BLOCK, smB, c.s>>>(SoaRecSrc{mid.x, mid.j1, mid.o}, m,
                                                                                    gshift, fine_cur, fin);
   c.launched();
-  DMST_CUDA(cudaFuncSetAttribute(k_mi_apply_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * FB));
+  DMST_CUDA(cudaFuncSetAttribute(k_mi_apply_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * FB));  // 64 KB
   c.begin(KK_MI_APPLY);
   k_mi_apply_smem<<<nf, 512, 8 * FB, c.s>>>(fin, fine_base, nv, out);
   c.launched();
@@ -499,16 +498,14 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     st->jump_rounds = jump_rounds;
   }
 
-  // expansion walk -> chain keys (+ digit histograms)
-  const uint64_t max_key = (uint64_t)soff;  // keys in [0, soff]
-  int digits = 1;
-  while (digits < 4 && (max_key >> (8 * digits))) ++digits;
-  uint32_t* hist2 = w.small + SM_HIST2;
+  // expansion walk -> chain keys (+ AND / OR of all keys for digit skipping)
+  uint32_t* key_ao = w.small + SM_HIST2;
   uint32_t* keys = (uint32_t*)w.R;
-  c.zero(hist2, 4 * kRadix * 4);
+  const uint32_t kinit[2] = {~0u, 0u};
+  DMST_CUDA(cudaMemcpyAsync(key_ao, kinit, 8, cudaMemcpyHostToDevice, c.s));
   c.begin(KK_WALK);
   k_walk<256><<<c.persistent_grid(n, 256, 8), 256, 0, c.s>>>(n, w.ret, w.euv0, w.vm_all, w.smi_all, lt, keys,
-                                                              hist2, digits);
+                                                              key_ao);
   c.launched();
   if (dbg_ret) DMST_CUDA(cudaMemcpyAsync(dbg_ret, w.ret, n, cudaMemcpyDeviceToDevice, c.s));
   if (dbg_key || dbg_term || dbg_lvl) {
@@ -516,11 +513,10 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     k_debug_chain<<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(n, keys, w.smi_all, lt, dbg_key, dbg_term, dbg_lvl);
     c.launched();
   }
-  std::vector<uint32_t> h(4 * kRadix);
-  c.to_host(h.data(), hist2, 4 * kRadix * 4);
+  uint32_t kao[2];
+  c.to_host(kao, key_ao, 8);
   c.sync();
-  std::vector<int> shifts;
-  active_digits(h, digits, n, shifts);
+  const std::vector<int> shifts = active_digits(kao[0], kao[1], 4);
   if (st) st->sort2_passes = (int)shifts.size();
   // chain sort: keys at R[0, 4n); ping-pong A = R[4n, 12n), B = R[12n, 20n)
   const uint32_t* skeys = keys;

@@ -30,44 +30,39 @@ __device__ __forceinline__ double key_to_double(uint64_t key) {
   return __longlong_as_double((long long)b);
 }
 
-// Warp-aggregated shared-memory histogram increment (uniform-digit fast path).
-__device__ __forceinline__ void hist_add(uint32_t* h, uint32_t d, bool ok, uint32_t act) {
-  uint32_t d0 = __shfl_sync(kFull, d, 0);
-  if (__all_sync(kFull, !ok || d == d0)) {
-    if (lane_id() == 0 && act) atomicAdd(h + d0, __popc(act));
-  } else if (ok) {
-    atomicAdd(h + d, 1u);
-  }
-}
-
 // ------------------------------------------------ 1. edge sort (sort #1)
-// One read of w: all eight digit histograms + the "-0.0 present" flag.
-__global__ void __launch_bounds__(256) k_sort1_hist(const double* __restrict__ w, int64_t n,
-                                                    uint32_t* __restrict__ hist,
+// One read of w: bitwise AND / OR of all sort keys (a digit is constant
+// iff AND and OR agree on its bits -> that radix pass is skipped) and the
+// "-0.0 present" flag.
+__global__ void __launch_bounds__(256) k_key_reduce(const double* __restrict__ w, int64_t n,
+                                                    unsigned long long* __restrict__ and_or,
                                                     uint32_t* __restrict__ negzero) {
-  __shared__ uint32_t sh[8][kRadix];
-  for (int i = threadIdx.x; i < 8 * kRadix; i += blockDim.x) (&sh[0][0])[i] = 0;
-  __syncthreads();
+  uint64_t a = ~0ull, o = 0ull;
   bool nz = false;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
-    const int64_t i = i0 + threadIdx.x;
-    const bool ok = i < n;
-    uint64_t key = 0;
-    if (ok) {
-      double x = ld_stream(w + i);
-      nz |= (uint64_t)__double_as_longlong(x) == 0x8000000000000000ull;
-      key = desc_key(x);
-    }
-    const uint32_t act = __ballot_sync(kFull, ok);
+  constexpr int U = 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x * U + threadIdx.x; b < n; b += stride) {
+    double x[U];
 #pragma unroll
-    for (int p = 0; p < 8; ++p) hist_add(sh[p], (uint32_t)(key >> (8 * p)) & 0xff, ok, act);
+    for (int q = 0; q < U; ++q) {
+      const int64_t i = b + (int64_t)q * blockDim.x;
+      x[q] = i < n ? ld_stream(w + i) : w[0];
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      nz |= (uint64_t)__double_as_longlong(x[q]) == 0x8000000000000000ull;
+      const uint64_t k = desc_key(x[q]);
+      a &= k;
+      o |= k;
+    }
   }
-  if (__any_sync(kFull, nz) && lane_id() == 0) atomicOr(negzero, 1u);
-  __syncthreads();
-  for (int i = threadIdx.x; i < 8 * kRadix; i += blockDim.x) {
-    uint32_t c = (&sh[0][0])[i];
-    if (c) atomicAdd(hist + i, c);
+  const uint32_t alo = __reduce_and_sync(kFull, (uint32_t)a), ahi = __reduce_and_sync(kFull, (uint32_t)(a >> 32));
+  const uint32_t olo = __reduce_or_sync(kFull, (uint32_t)o), ohi = __reduce_or_sync(kFull, (uint32_t)(o >> 32));
+  const bool anz = __any_sync(kFull, nz);
+  if (lane_id() == 0) {
+    atomicAnd(and_or, ((unsigned long long)ahi << 32) | alo);
+    atomicOr(and_or + 1, ((unsigned long long)ohi << 32) | olo);
+    if (anz) atomicOr(negzero, 1u);
   }
 }
 
@@ -502,10 +497,8 @@ __global__ void __launch_bounds__(BLOCK)
 k_walk(int64_t n, const int8_t* __restrict__ ret, const int2* __restrict__ euv,
        const int32_t* __restrict__ vm_all, const int32_t* __restrict__ smi_all,
        const __grid_constant__ LevelTable lt, uint32_t* __restrict__ keys,
-       uint32_t* __restrict__ hist, int digits) {
-  __shared__ uint32_t sh[4][kRadix];
-  for (int i = threadIdx.x; i < 4 * kRadix; i += BLOCK) (&sh[0][0])[i] = 0;
-  __syncthreads();
+       uint32_t* __restrict__ and_or) {
+  uint32_t ka = ~0u, ko = 0u;
   const int64_t stride = (int64_t)gridDim.x * BLOCK;
   for (int64_t e0 = (int64_t)blockIdx.x * BLOCK; e0 < n; e0 += stride) {
     const int64_t e = e0 + threadIdx.x;
@@ -526,14 +519,15 @@ k_walk(int64_t n, const int8_t* __restrict__ ret, const int2* __restrict__ euv,
         }
       }
       keys[e] = key;
+      ka &= key;
+      ko |= key;
     }
-    const uint32_t act = __ballot_sync(kFull, ok);
-    for (int p = 0; p < digits; ++p) hist_add(sh[p], (key >> (8 * p)) & 0xff, ok, act);
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < digits * kRadix; i += BLOCK) {
-    uint32_t c = (&sh[0][0])[i];
-    if (c) atomicAdd(hist + i, c);
+  ka = __reduce_and_sync(kFull, ka);
+  ko = __reduce_or_sync(kFull, ko);
+  if (lane_id() == 0) {
+    atomicAnd(and_or, ka);
+    atomicOr(and_or + 1, ko);
   }
 }
 

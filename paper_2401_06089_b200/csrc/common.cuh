@@ -30,6 +30,18 @@ __device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
 template <typename T>
 __device__ __forceinline__ T ld_stream(const T* p) { return __ldcs(p); }
 
+// Loads of small tables that should stay L2-resident (evict_last policy).
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint32_t ld_keep(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
 __device__ __forceinline__ uint32_t warp_incl_sum(uint32_t x) {
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {

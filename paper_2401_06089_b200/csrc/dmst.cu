@@ -37,7 +37,7 @@ namespace dmst {
 // Edge sort: u64 key + 3-word payload.
 constexpr int S1_BLOCK = 256, S1_ITEMS = 6, S1_MINB = 2;
 // Chain sort: u32 key + 1-word payload.
-constexpr int S2_BLOCK = 256, S2_ITEMS = 16, S2_MINB = 2;
+constexpr int S2_BLOCK = 256, S2_ITEMS = 16, S2_MINB = 2, S2_BITS = 8;  // 9-bit digits measured slower (shorter runs)
 constexpr int64_t kDirectMiBytes = 24ll << 20;  // direct scatter-max below this mi64 size
 
 enum KernelKind {
@@ -95,6 +95,7 @@ struct Workspace {
   int32_t* grank[2];
   int32_t* vm_all;        // vertex maps of views 0..L-1
   int32_t* smi_all;       // maxIncident (global ranks) of views 1..L
+  int2* lvl_all;          // walk table: (vertex_map, maxIncident) of views 1..L
   uint32_t* sel_status;   // select/leafscan look-back words
   size_t bytes;
 };
@@ -118,7 +119,7 @@ Workspace carve(int64_t n, int64_t nv, char* base) {
   };
   const int64_t half = n / 2 + 1;
   w.R = take(48 * n + 4096);
-  w.counts = (uint32_t*)take(4 * kRadix * kMaxChunks);
+  w.counts = (uint32_t*)take(4 * 1024 * (kMaxChunks + 4));
   w.fine = (uint32_t*)take(4 * (4 * (nv / FB + 2) + 512));
   w.small = (uint32_t*)take(4 * kSmallWords);
   w.euv0 = (int2*)take(8 * n);
@@ -133,6 +134,7 @@ Workspace carve(int64_t n, int64_t nv, char* base) {
   }
   w.vm_all = (int32_t*)take(4 * (2 * nv + DMST_MAX_LEVELS + 2));
   w.smi_all = (int32_t*)take(4 * (nv + DMST_MAX_LEVELS + 2));
+  w.lvl_all = (int2*)take(8 * (nv + DMST_MAX_LEVELS + 2));
   w.sel_status = (uint32_t*)take(4 * (cdiv(std::max(nv, n), SEL_TILE) + 2));
   w.bytes = off + 256;
   return w;
@@ -206,11 +208,11 @@ struct Ctx {
 };
 
 // One radix pass: upsweep (per-chunk digit counts), chunk scan, downsweep.
-template <typename K, int VW, int BLOCK, int ITEMS, int MINB, class Loader, class Emitter>
+template <typename K, int VW, int BLOCK, int ITEMS, int MINB, int BITS, class Loader, class Emitter>
 void radix_pass(Ctx& c, int kind, int64_t n, int shift, Loader ld, Emitter em) {
-  using S = DownSmem<K, VW, BLOCK, ITEMS, Loader>;
+  using S = DownSmem<K, VW, BLOCK, ITEMS, Loader, BITS>;
   constexpr int T = S::T;
-  auto kern = k_downsweep<K, VW, BLOCK, ITEMS, MINB, Loader, Emitter>;
+  auto kern = k_downsweep<K, VW, BLOCK, ITEMS, MINB, Loader, Emitter, BITS>;
   DMST_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes()));
   SweepArgs a;
   a.n = n;
@@ -219,14 +221,15 @@ void radix_pass(Ctx& c, int kind, int64_t n, int shift, Loader ld, Emitter em) {
   a.chunk = cdiv(cdiv(n, G), T) * T;
   G = cdiv(n, a.chunk);
   a.G = (uint32_t)G;
+  a.GS = (uint32_t)((G + 3) & ~int64_t(3));
   a.counts = c.w.counts;
   a.prof = nullptr;
-  c.zero(a.counts, 4 * kRadix * G);
+  c.zero(a.counts, 4 * (size_t(1) << BITS) * a.GS);
   c.begin(KK_UPSWEEP);
-  k_upsweep<Loader><<<(unsigned)(G * kUpSplit), 256, 0, c.s>>>(a, ld);
+  k_upsweep<BITS, Loader><<<(unsigned)(G * kUpSplit), 256, 0, c.s>>>(a, ld);
   c.launched();
   c.begin(KK_UPSWEEP);
-  k_chunk_scan<<<1, 1024, 0, c.s>>>(a.counts, (int64_t)kRadix * G);
+  k_chunk_scan<BITS><<<1, 256, 0, c.s>>>(a.counts, a.GS);
   c.launched();
   c.begin(kind);
   kern<<<(unsigned)G, BLOCK, S::bytes(), c.s>>>(a, ld, em);
@@ -236,7 +239,7 @@ void radix_pass(Ctx& c, int kind, int64_t n, int shift, Loader ld, Emitter em) {
 // Multi-pass driver over the non-constant digits (bit offsets `shifts`).
 // Ping-pong SoA buffers bufK[2], bufV[2][VW]; first/last passes use the given
 // loader/emitter.
-template <typename K, int VW, int BLOCK, int ITEMS, int MINB, class FirstLoader, class FinalEmitter>
+template <typename K, int VW, int BLOCK, int ITEMS, int MINB, int BITS, class FirstLoader, class FinalEmitter>
 void run_sort(Ctx& c, const int (&kinds)[3], int64_t n, const std::vector<int>& shifts,
               K* const (&bufK)[2], uint32_t* const (&bufV)[2][VW], FirstLoader first,
               FinalEmitter final_em) {
@@ -258,22 +261,23 @@ void run_sort(Ctx& c, const int (&kinds)[3], int64_t n, const std::vector<int>& 
       ldr.vals[q] = bufV[in][q];
     }
     if (P == 1)
-      radix_pass<K, VW, BLOCK, ITEMS, MINB>(c, kinds[2], n, shifts[p], first, final_em);
+      radix_pass<K, VW, BLOCK, ITEMS, MINB, BITS>(c, kinds[2], n, shifts[p], first, final_em);
     else if (p == 0)
-      radix_pass<K, VW, BLOCK, ITEMS, MINB>(c, kinds[0], n, shifts[p], first, mid);
+      radix_pass<K, VW, BLOCK, ITEMS, MINB, BITS>(c, kinds[0], n, shifts[p], first, mid);
     else if (p == P - 1)
-      radix_pass<K, VW, BLOCK, ITEMS, MINB>(c, kinds[2], n, shifts[p], ldr, final_em);
+      radix_pass<K, VW, BLOCK, ITEMS, MINB, BITS>(c, kinds[2], n, shifts[p], ldr, final_em);
     else
-      radix_pass<K, VW, BLOCK, ITEMS, MINB>(c, kinds[1], n, shifts[p], ldr, mid);
+      radix_pass<K, VW, BLOCK, ITEMS, MINB, BITS>(c, kinds[1], n, shifts[p], ldr, mid);
   }
 }
 
-// Radix digits (8-bit, at bit offsets 0, 8, ...) that are not constant
-// across all keys, from the AND / OR of every key.
-std::vector<int> active_digits(uint64_t key_and, uint64_t key_or, int digits) {
+// Radix digits (BITS wide, at bit offsets 0, BITS, ...) that are not
+// constant across all keys, from the AND / OR of every key.
+std::vector<int> active_digits(uint64_t key_and, uint64_t key_or, int bits, int key_bits) {
   std::vector<int> shifts;
-  for (int d = 0; d < digits; ++d)
-    if (((key_and ^ key_or) >> (8 * d)) & 0xff) shifts.push_back(8 * d);
+  const uint64_t mask = (1ull << bits) - 1;
+  for (int sft = 0; sft < key_bits; sft += bits)
+    if (((key_and ^ key_or) >> sft) & mask) shifts.push_back(sft);
   return shifts;
 }
 
@@ -293,13 +297,13 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
   c.to_host(ao, and_or, 16);
   c.to_host(&nz, negzero, 4);
   c.sync();
-  const std::vector<int> shifts = active_digits(ao[0], ao[1], 8);
+  const std::vector<int> shifts = active_digits(ao[0], ao[1], 8, 64);
   if (passes_out) *passes_out = (int)shifts.size();
   char* R = c.w.R;
   uint64_t* const bufK[2] = {(uint64_t*)R, (uint64_t*)(R + 8 * n)};
   uint32_t* vb = (uint32_t*)(R + 16 * n);
   uint32_t* const bufV[2][3] = {{vb, vb + n, vb + 2 * n}, {vb + 3 * n, vb + 4 * n, vb + 5 * n}};
-  run_sort<uint64_t, 3, S1_BLOCK, S1_ITEMS, S1_MINB>(c, {KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL}, n,
+  run_sort<uint64_t, 3, S1_BLOCK, S1_ITEMS, S1_MINB, 8>(c, {KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL}, n,
                                                      shifts, bufK, bufV, Sort1FirstLoader{w, u, v}, em);
   if (nz) {
     c.begin(KK_OTHER);
@@ -392,8 +396,16 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     k_leafscan<<<grid_for(words, 2048), 256, 0, c.s>>>(words, w.cnt2, w.leafpre, w.sel_status,
                                                        misc + MISC_LSCTR, misc + MISC_COUNTS);
     c.launched();
-    uint32_t counts[2];
+    // V2: supervertex labels (vertex_map).  Runs before the host reads the
+    // counts (one sync per level); on the final view its result is unused.
+    int32_t* vm = w.vm_all + voff;
+    c.zero(misc + MISC_ACTIVE0, 12);
+    c.begin(KK_V2);
+    k_v2<<<grid_for(nv_k, EW_BLOCK), EW_BLOCK, 0, c.s>>>(nv_k, mi_k, w.cnt2, w.leafpre, vm, lists[0], lcnt[0]);
+    c.launched();
+    uint32_t counts[3];
     c.to_host(counts, misc + MISC_COUNTS, 8);
+    c.to_host(counts + 2, lcnt[0], 4);
     c.sync();
     const int64_t n_leaf = counts[0], n_chain = counts[1];
     const int64_t n_alpha = n_k - n_leaf - n_chain;
@@ -412,17 +424,9 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
       }
       break;
     }
-    // V2: supervertex labels (vertex_map)
-    int32_t* vm = w.vm_all + voff;
     lt.voff[level] = voff;
     voff += nv_k;
-    c.zero(misc + MISC_ACTIVE0, 12);
-    c.begin(KK_V2);
-    k_v2<<<grid_for(nv_k, EW_BLOCK), EW_BLOCK, 0, c.s>>>(nv_k, mi_k, w.cnt2, w.leafpre, vm, lists[0], lcnt[0]);
-    c.launched();
-    uint32_t pending;
-    c.to_host(&pending, lcnt[0], 4);
-    c.sync();
+    uint32_t pending = counts[2];
     if (pending) {
       // pointer jumping over the unresolved vertices
       const int32_t* in = lists[0];
@@ -503,8 +507,13 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
   uint32_t* keys = (uint32_t*)w.R;
   const uint32_t kinit[2] = {~0u, 0u};
   DMST_CUDA(cudaMemcpyAsync(key_ao, kinit, 8, cudaMemcpyHostToDevice, c.s));
+  if (soff > 0) {
+    c.begin(KK_OTHER);
+    k_pack_levels<<<grid_for(soff, EW_BLOCK), EW_BLOCK, 0, c.s>>>(soff, w.vm_all, w.smi_all, lt, w.lvl_all);
+    c.launched();
+  }
   c.begin(KK_WALK);
-  k_walk<256><<<c.persistent_grid(n, 256, 8), 256, 0, c.s>>>(n, w.ret, w.euv0, w.vm_all, w.smi_all, lt, keys,
+  k_walk<256><<<c.persistent_grid(n, 256, 8), 256, 0, c.s>>>(n, w.ret, w.euv0, w.vm_all, w.lvl_all, lt, keys,
                                                               key_ao);
   c.launched();
   if (dbg_ret) DMST_CUDA(cudaMemcpyAsync(dbg_ret, w.ret, n, cudaMemcpyDeviceToDevice, c.s));
@@ -516,7 +525,7 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
   uint32_t kao[2];
   c.to_host(kao, key_ao, 8);
   c.sync();
-  const std::vector<int> shifts = active_digits(kao[0], kao[1], 4);
+  const std::vector<int> shifts = active_digits(kao[0], kao[1], S2_BITS, 32);
   if (st) st->sort2_passes = (int)shifts.size();
   // chain sort: keys at R[0, 4n); ping-pong A = R[4n, 12n), B = R[12n, 20n)
   const uint32_t* skeys = keys;
@@ -529,7 +538,7 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     ArrayEmitter<uint32_t, 1> fin;
     fin.keys = bufK[lastb];
     fin.vals[0] = bufV[lastb][0];
-    run_sort<uint32_t, 1, S2_BLOCK, S2_ITEMS, S2_MINB>(c, {KK_SORT2_PASS, KK_SORT2_PASS, KK_SORT2_PASS}, n,
+    run_sort<uint32_t, 1, S2_BLOCK, S2_ITEMS, S2_MINB, S2_BITS>(c, {KK_SORT2_PASS, KK_SORT2_PASS, KK_SORT2_PASS}, n,
                                                        shifts, bufK, bufV, Sort2FirstLoader{keys}, fin);
     skeys = fin.keys;
     svals = fin.vals[0];

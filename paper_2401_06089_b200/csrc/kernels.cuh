@@ -289,10 +289,10 @@ __global__ void __launch_bounds__(256) k_leafscan(int64_t words, const uint32_t*
 }
 
 __device__ __forceinline__ uint32_t leaf_label(const uint32_t* __restrict__ cnt2,
-                                               const uint32_t* __restrict__ leafpre, uint32_t j) {
-  const uint32_t w = cnt2[j >> 4];
+                                               const uint32_t* __restrict__ leafpre, uint32_t j, uint64_t pol) {
+  const uint32_t w = ld_keep(cnt2 + (j >> 4), pol);
   const uint32_t below = (1u << ((j & 15) * 2)) - 1u;
-  return leafpre[j >> 4] + __popc(leaf_bits(w) & below);
+  return ld_keep(leafpre + (j >> 4), pol) + __popc(leaf_bits(w) & below);
 }
 
 // V2: chase maxIncident pointers to the component's leaf edge (ranks grow
@@ -305,6 +305,7 @@ __global__ void k_v2(int64_t nv, const unsigned long long* __restrict__ mi64,
                      const uint32_t* __restrict__ cnt2, const uint32_t* __restrict__ leafpre,
                      int32_t* __restrict__ vm, int32_t* __restrict__ active, uint32_t* __restrict__ active_cnt) {
   const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t pol = l2_keep_policy();
   bool unresolved = false;
   if (x < nv) {
     unsigned long long m = ld_stream(mi64 + x);
@@ -312,17 +313,17 @@ __global__ void k_v2(int64_t nv, const unsigned long long* __restrict__ mi64,
     uint32_t y = (uint32_t)m;
     int s = 0;
     while (m != 0ull) {  // m == 0: isolated vertex (single-vertex view), label 0
-      const uint32_t c = (cnt2[j >> 4] >> ((j & 15) * 2)) & 3u;
+      const uint32_t c = (ld_keep(cnt2 + (j >> 4), pol) >> ((j & 15) * 2)) & 3u;
       if (c == 2u) break;
       if (++s > CHASE_STEPS) {
         unresolved = true;
         break;
       }
-      m = mi64[y];
+      m = __ldcs(mi64 + y);
       j = (uint32_t)(m >> 32) - 1u;
       y = (uint32_t)m;
     }
-    vm[x] = unresolved ? ~(int32_t)y : (m ? (int32_t)leaf_label(cnt2, leafpre, j) : 0);
+    __stcs(vm + x, unresolved ? ~(int32_t)y : (m ? (int32_t)leaf_label(cnt2, leafpre, j, pol) : 0));
   }
   const uint32_t msk = __ballot_sync(kFull, unresolved);
   if (msk) {
@@ -447,7 +448,7 @@ struct EdgeSel {
   __device__ __forceinline__ void flush_shared(Shared&) const {}
   __device__ __forceinline__ bool flag(int64_t j, Item& it) const {
     uint32_t c = (cnt2[j >> 4] >> ((j & 15) * 2)) & 3u;
-    it.g = grank ? grank[j] : (int32_t)j;
+    it.g = grank ? __ldcs(grank + j) : (int32_t)j;
     return c == 0;
   }
   __device__ __forceinline__ void emit(int64_t j, bool alpha, uint32_t pos, const Item& it, Shared&) const {
@@ -455,10 +456,10 @@ struct EdgeSel {
     if (!alpha) {
       ret[it.g] = level;
     } else {
-      int2 e = euv[j];
+      int2 e = __ldcs(euv + j);
       int32_t a = vm[e.x], b = vm[e.y];
-      euv_next[pos] = make_int2(a, b);
-      grank_next[pos] = it.g;
+      __stcs(euv_next + pos, make_int2(a, b));
+      __stcs(grank_next + pos, it.g);
       if (mi64_next) {
         atomicMax(mi64_next + a, pack_mi(pos + 1u, (uint32_t)b));
         atomicMax(mi64_next + b, pack_mi(pos + 1u, (uint32_t)a));
@@ -492,33 +493,44 @@ struct LevelTable {
 // 0 <= p < e wins.  The chain (terminal, anchor) is encoded as the dense key
 // 1 + soff[k] + anchor (a terminal edge is a terminal only at the one level
 // it retires at, so (level, anchor) identifies the chain); 0 = root chain.
+// Walk table of views 1..L: lvl[soff[k] + x] = (vertex_map_k[x] (-1 for the
+// final view), maxIncident_k[x]) so each level of the walk is one 8-B hop.
+__global__ void k_pack_levels(int64_t total, const int32_t* __restrict__ vm_all,
+                              const int32_t* __restrict__ smi_all, const __grid_constant__ LevelTable lt,
+                              int2* __restrict__ lvl) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  int k = 1;
+  while (k < lt.L && i >= lt.soff[k + 1]) ++k;
+  const int32_t next = k < lt.L ? vm_all[lt.voff[k] + (i - lt.soff[k])] : -1;
+  __stcs(lvl + i, make_int2(next, smi_all[i]));
+}
+
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK)
 k_walk(int64_t n, const int8_t* __restrict__ ret, const int2* __restrict__ euv,
-       const int32_t* __restrict__ vm_all, const int32_t* __restrict__ smi_all,
+       const int32_t* __restrict__ vm0, const int2* __restrict__ lvl,
        const __grid_constant__ LevelTable lt, uint32_t* __restrict__ keys,
        uint32_t* __restrict__ and_or) {
   uint32_t ka = ~0u, ko = 0u;
   const int64_t stride = (int64_t)gridDim.x * BLOCK;
   for (int64_t e0 = (int64_t)blockIdx.x * BLOCK; e0 < n; e0 += stride) {
     const int64_t e = e0 + threadIdx.x;
-    const bool ok = e < n;
-    uint32_t key = 0;
-    if (ok) {
-      const int r = ret[e];
+    if (e < n) {
+      uint32_t key = 0;
+      const int r = __ldcs(ret + e);
       if (r < lt.L) {
-        int32_t x = euv[e].x;
-        for (int k = 0; k < r; ++k) x = vm_all[lt.voff[k] + x];
-        for (int k = r + 1; k <= lt.L; ++k) {
-          x = vm_all[lt.voff[k - 1] + x];
-          int32_t p = smi_all[lt.soff[k] + x];
-          if (p >= 0 && p < (int32_t)e) {
+        int32_t x = vm0[__ldcs(euv + e).x];  // view-1 supervertex
+        for (int k = 1; k <= lt.L; ++k) {
+          const int2 t = lvl[lt.soff[k] + x];
+          if (k > r && t.y >= 0 && t.y < (int32_t)e) {
             key = (uint32_t)(1 + lt.soff[k] + x);
             break;
           }
+          x = t.x;
         }
       }
-      keys[e] = key;
+      __stcs(keys + e, key);
       ka &= key;
       ko |= key;
     }

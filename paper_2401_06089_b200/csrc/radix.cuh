@@ -35,9 +35,9 @@ struct Vals {
   uint32_t w[VW];
 };
 
-template <typename K>
+template <int BITS = kRadixBits, typename K>
 __device__ __forceinline__ uint32_t digit_of(K key, int shift) {
-  return (uint32_t)(key >> shift) & (kRadix - 1);
+  return (uint32_t)(key >> shift) & ((1u << BITS) - 1u);
 }
 
 // ----------------------------------------------------------- PTX helpers
@@ -139,7 +139,8 @@ struct SweepArgs {
   int64_t chunk;          // items per CTA (multiple of the downsweep sub-tile)
   int shift;              // digit bit offset
   uint32_t G;             // number of chunks (= CTAs)
-  uint32_t* counts;       // [256][G] digit-major (upsweep out, scan in/out)
+  uint32_t GS;            // row stride of counts (G rounded up to a multiple of 4)
+  uint32_t* counts;       // [256][GS] digit-major (upsweep out, scan in/out)
   unsigned long long* prof;  // optional: per-CTA phase time sums [G][8] (tools/sortbench)
 };
 
@@ -152,12 +153,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
 constexpr int kMaxChunks = 148 * 4;  // downsweep CTAs (chunks) per pass, upper bound
 constexpr int kUpSplit = 4;  // upsweep CTAs per chunk (counts accumulate atomically)
 
-template <class Loader>
+template <int BITS, class Loader>
 __global__ void __launch_bounds__(256) k_upsweep(SweepArgs a, Loader ld) {
-  __shared__ uint32_t h[8][kRadix];  // per-warp histograms
+  constexpr int R = 1 << BITS, BPT = R / 256;
+  __shared__ uint32_t h[8][R];  // per-warp histograms
   const uint32_t warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int w = 0; w < 8; ++w) h[w][threadIdx.x] = 0;
+  for (int w = 0; w < 8; ++w)
+#pragma unroll
+    for (int q = 0; q < BPT; ++q) h[w][q * 256 + threadIdx.x] = 0;
   __syncthreads();
   const uint32_t chunk_id = blockIdx.x / kUpSplit, part = blockIdx.x % kUpSplit;
   const int64_t cbeg = (int64_t)chunk_id * a.chunk;
@@ -172,7 +176,7 @@ __global__ void __launch_bounds__(256) k_upsweep(SweepArgs a, Loader ld) {
     for (int q = 0; q < U; ++q) {
       const int64_t i = i0 + q * 256 + threadIdx.x;
       ok[q] = i < end;
-      d[q] = ok[q] ? digit_of(ld.key(i), a.shift) : 0u;
+      d[q] = ok[q] ? digit_of<BITS>(ld.key(i), a.shift) : 0u;
     }
 #pragma unroll
     for (int q = 0; q < U; ++q) {
@@ -186,33 +190,56 @@ __global__ void __launch_bounds__(256) k_upsweep(SweepArgs a, Loader ld) {
     }
   }
   __syncthreads();
-  uint32_t c = 0;
 #pragma unroll
-  for (int w = 0; w < 8; ++w) c += h[w][threadIdx.x];
-  if (c) atomicAdd(a.counts + (uint64_t)threadIdx.x * a.G + chunk_id, c);
+  for (int q = 0; q < BPT; ++q) {
+    const uint32_t b = q * 256 + threadIdx.x;
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) c += h[w][b];
+    if (c) atomicAdd(a.counts + (uint64_t)b * a.GS + chunk_id, c);
+  }
 }
 
-// Exclusive scan of counts[256 * G] in place (digit-major => global offsets).
-__global__ void __launch_bounds__(1024) k_chunk_scan(uint32_t* counts, int64_t total) {
-  __shared__ uint32_t scratch[1024 / 32 + 1];
-  const int64_t per = (total + 1023) / 1024;
-  const int64_t b = (int64_t)threadIdx.x * per, e = min(total, b + per);
+// Exclusive scan of counts[R][GS] in place, digit-major => the global
+// output offset of every (digit, chunk).  Thread t owns rows t*BPT.. (vector loads).
+template <int BITS>
+__global__ void __launch_bounds__(256) k_chunk_scan(uint32_t* counts, uint32_t GS) {
+  constexpr int BPT = (1 << BITS) / 256;
+  __shared__ uint32_t scratch[256 / 32 + 1];
+  const uint32_t nq = GS / 4;
   uint32_t s = 0;
-#pragma unroll 16
-  for (int64_t i = b; i < e; ++i) s += counts[i];
+#pragma unroll
+  for (int r = 0; r < BPT; ++r) {
+    const uint4* row = reinterpret_cast<const uint4*>(counts + (uint64_t)(threadIdx.x * BPT + r) * GS);
+#pragma unroll 8
+    for (uint32_t q = 0; q < nq; ++q) {
+      const uint4 v = row[q];
+      s += v.x + v.y + v.z + v.w;
+    }
+  }
   uint32_t tot;
-  uint32_t run = block_excl_sum<1024>(s, scratch, &tot);
-#pragma unroll 16
-  for (int64_t i = b; i < e; ++i) {
-    const uint32_t c = counts[i];
-    counts[i] = run;
-    run += c;
+  uint32_t run = block_excl_sum<256>(s, scratch, &tot);
+#pragma unroll
+  for (int r = 0; r < BPT; ++r) {
+    uint4* row = reinterpret_cast<uint4*>(counts + (uint64_t)(threadIdx.x * BPT + r) * GS);
+#pragma unroll 8
+    for (uint32_t q = 0; q < nq; ++q) {
+      const uint4 v = row[q];
+      uint4 o;
+      o.x = run;
+      o.y = o.x + v.x;
+      o.z = o.y + v.y;
+      o.w = o.z + v.z;
+      run = o.w + v.w;
+      row[q] = o;
+    }
   }
 }
 
 // ------------------------------------------------------------- downsweep
-template <typename K, int VW, int BLOCK, int ITEMS, class Loader>
+template <typename K, int VW, int BLOCK, int ITEMS, class Loader, int BITS = kRadixBits>
 struct DownSmem {
+  static constexpr int R = 1 << BITS;
   static constexpr int T = BLOCK * ITEMS;
   static constexpr int NW = BLOCK / 32;
   static constexpr int NS = Loader::NS;
@@ -235,10 +262,10 @@ struct DownSmem {
   __host__ __device__ static constexpr size_t off_stage(int st) { return st * stage_bytes(); }
   __host__ __device__ static constexpr size_t off_misc() { return 2 * stage_bytes(); }
   struct Misc {
-    uint32_t whist[NW][kRadix];
-    uint32_t run[kRadix];     // running global offset per digit
-    uint32_t lstart[kRadix];
-    uint32_t gofs[kRadix];
+    uint32_t whist[NW][R];
+    uint32_t run[R];     // running global offset per digit
+    uint32_t lstart[R];
+    uint32_t gofs[R];
     uint32_t scan[NW + 1];
     uint64_t bar[2];
   };
@@ -259,7 +286,7 @@ __device__ __forceinline__ uint32_t warp_rank(uint32_t* whist, uint32_t d, bool 
     peers &= __ballot_sync(kFull, bit) ^ (bit - 1u);
   }
 #else
-  const uint32_t peers = __match_any_sync(kFull, FULL ? d : (valid ? d : 0x100u));
+  const uint32_t peers = __match_any_sync(kFull, FULL ? d : (valid ? d : 0xffffu));
 #endif
   uint32_t old = 0;
   if (FULL || valid) old = whist[d];
@@ -274,7 +301,8 @@ template <bool FULL, typename K, int VW, int BLOCK, int ITEMS, class S, class Em
 __device__ __forceinline__ void down_subtile(const SweepArgs& a, const Emitter& em, typename S::Misc& m,
                                              unsigned char* buf, K (&k)[ITEMS], Vals<VW> (&v)[ITEMS],
                                              int cnt_items) {
-  constexpr int T = S::T, NW = S::NW;
+  constexpr int T = S::T, NW = S::NW, R = S::R, BPT = R / BLOCK;
+  constexpr int BITS = R == 256 ? 8 : R == 512 ? 9 : 10;
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t lt = lanemask_lt();
   const int lbase = warp * ITEMS * 32 + lane;
@@ -282,22 +310,35 @@ __device__ __forceinline__ void down_subtile(const SweepArgs& a, const Emitter& 
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const bool valid = FULL || lbase + i * 32 < cnt_items;
-    rk[i] = warp_rank<FULL>(m.whist[warp], digit_of(k[i], a.shift), valid, lane, lt);
+    rk[i] = warp_rank<FULL>(m.whist[warp], digit_of<BITS>(k[i], a.shift), valid, lane, lt);
   }
   __syncthreads();  // (also: every thread has finished reading `buf`)
 
-  uint32_t c = 0;
+  // thread t owns digits t*BPT .. t*BPT+BPT-1 (consecutive, for the block scan)
+  uint32_t cb[BPT], csum = 0;
 #pragma unroll
-  for (int w = 0; w < NW; ++w) {
-    const uint32_t x = m.whist[w][tid];
-    m.whist[w][tid] = c;
-    c += x;
+  for (int q = 0; q < BPT; ++q) {
+    const uint32_t b = tid * BPT + q;
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const uint32_t x = m.whist[w][b];
+      m.whist[w][b] = c;
+      c += x;
+    }
+    cb[q] = c;
+    csum += c;
   }
   uint32_t total;
-  const uint32_t lstart = block_excl_sum<BLOCK>(c, m.scan, &total);
-  m.lstart[tid] = lstart;
-  m.gofs[tid] = m.run[tid] - lstart;
-  m.run[tid] += c;
+  uint32_t lstart = block_excl_sum<BLOCK>(csum, m.scan, &total);
+#pragma unroll
+  for (int q = 0; q < BPT; ++q) {
+    const uint32_t b = tid * BPT + q;
+    m.lstart[b] = lstart;
+    m.gofs[b] = m.run[b] - lstart;
+    m.run[b] += cb[q];
+    lstart += cb[q];
+  }
   __syncthreads();
 
   K* skeys = reinterpret_cast<K*>(buf);
@@ -305,7 +346,7 @@ __device__ __forceinline__ void down_subtile(const SweepArgs& a, const Emitter& 
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     if (FULL || lbase + i * 32 < cnt_items) {
-      const uint32_t d = digit_of(k[i], a.shift);
+      const uint32_t d = digit_of<BITS>(k[i], a.shift);
       const uint32_t pos = m.lstart[d] + m.whist[warp][d] + rk[i];
       skeys[pos] = k[i];
 #pragma unroll
@@ -324,21 +365,23 @@ __device__ __forceinline__ void down_subtile(const SweepArgs& a, const Emitter& 
       k[i] = skeys[sidx];
 #pragma unroll
       for (int q = 0; q < VW; ++q) v[i].w[q] = svals[q * T + sidx];
-      dst[i] = m.gofs[digit_of(k[i], a.shift)] + sidx;
+      dst[i] = m.gofs[digit_of<BITS>(k[i], a.shift)] + sidx;
     }
   }
 #pragma unroll
-  for (int w = 0; w < NW; ++w) m.whist[w][tid] = 0;
+  for (int w = 0; w < NW; ++w)
+#pragma unroll
+    for (int q = 0; q < BPT; ++q) m.whist[w][tid * BPT + q] = 0;
   em.template emit<ITEMS>(dst, k, v, ok);
   __syncthreads();
 }
 
-template <typename K, int VW, int BLOCK, int ITEMS, int MINB, class Loader, class Emitter>
+template <typename K, int VW, int BLOCK, int ITEMS, int MINB, class Loader, class Emitter, int BITS = kRadixBits>
 __global__ void __launch_bounds__(BLOCK, MINB)
 k_downsweep(SweepArgs a, Loader ld, Emitter em) {
-  static_assert(BLOCK == kRadix, "one thread per digit bin");
-  using S = DownSmem<K, VW, BLOCK, ITEMS, Loader>;
-  constexpr int T = S::T, NW = S::NW, NS = S::NS;
+  static_assert(BLOCK == 256 && (1 << BITS) % BLOCK == 0, "digit bins are owned by threads");
+  using S = DownSmem<K, VW, BLOCK, ITEMS, Loader, BITS>;
+  constexpr int T = S::T, NW = S::NW, NS = S::NS, BPT = S::R / BLOCK;
   extern __shared__ __align__(128) unsigned char smem[];
   typename S::Misc& m = *reinterpret_cast<typename S::Misc*>(smem + S::off_misc());
 
@@ -349,9 +392,13 @@ k_downsweep(SweepArgs a, Loader ld, Emitter em) {
   const int nsub = (int)((end - begin + T - 1) / T);
   const bool tma = loader_tma_ok(ld);
 
-  m.run[tid] = a.counts[(uint64_t)tid * a.G + blockIdx.x];
 #pragma unroll
-  for (int w = 0; w < NW; ++w) m.whist[w][tid] = 0;
+  for (int q = 0; q < BPT; ++q) {
+    const uint32_t b = tid * BPT + q;
+    m.run[b] = a.counts[(uint64_t)b * a.GS + blockIdx.x];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) m.whist[w][b] = 0;
+  }
   if (tid == 0) {
     mbar_init(&m.bar[0], 1);
     mbar_init(&m.bar[1], 1);

@@ -35,18 +35,18 @@ void run(int64_t n, uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint32
   a.n = n; a.shift = shift; a.counts = counts;
   int64_t G = std::min<int64_t>((n + S::T - 1) / S::T, (int64_t)sms * MINB);
   a.chunk = ((n + G - 1) / G + S::T - 1) / S::T * S::T;
-  G = (n + a.chunk - 1) / a.chunk; a.G = (uint32_t)G;
+  G = (n + a.chunk - 1) / a.chunk; a.G = (uint32_t)G; a.GS = (uint32_t)((G + 3) & ~3);
   L ld; ld.keys = k; ld.vals[0] = v;
   E em; em.keys = k2; em.vals[0] = v2;
   cudaEvent_t e[4]; for (auto& x : e) cudaEventCreate(&x);
   float up = 1e9, sc = 1e9, dn = 1e9;
   for (int r = 0; r < 4; ++r) {
     a.prof = (r == 3) ? prof : nullptr;
-    cudaMemset(counts, 0, 4 * 256 * G);
+    cudaMemset(counts, 0, 4 * 256 * a.GS);
     cudaEventRecord(e[0]);
-    k_upsweep<L><<<(unsigned)(G * kUpSplit), 256>>>(a, ld);
+    k_upsweep<8, L><<<(unsigned)(G * kUpSplit), 256>>>(a, ld);
     cudaEventRecord(e[1]);
-    k_chunk_scan<<<1, 1024>>>(counts, 256 * G);
+    k_chunk_scan<8><<<1, 256>>>(counts, a.GS);
     cudaEventRecord(e[2]);
     kern<<<(unsigned)G, 256, S::bytes()>>>(a, ld, em);
     cudaEventRecord(e[3]); cudaEventSynchronize(e[3]);

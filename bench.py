@@ -43,7 +43,9 @@ WORKLOADS = {
     "config3-caterpillar": ("caterpillar", 16_000_000,
                             "config3: caterpillar n=16M, monotone weights (single chain)"),
     "random16M": ("random", 16_000_000, "random spanning tree n=16M, uniform weights (config3 reference point)"),
-    "config5-tree": ("random", 8_000_000, "config5 unit: random spanning tree n=8M, uniform weights"),
+    "config5": ("random", 8_000_000,
+                "config5: batch of 64 independent random spanning trees n=8M (uniform weights, seeds 0..63), "
+                "tree i on GPU i mod N"),
     "config1": ("random", 100_000, "config1: random spanning tree n=100k, uniform weights, seed 0"),
 }
 
@@ -133,13 +135,46 @@ def dist_setup():
     return ws, rank, local
 
 
-def make_input(workload: str, n_override: int | None, seed: int):
+CONFIG5_TREES = 64
+
+
+def replica_plan(workload: str, world_size: int, rank: int) -> list[int]:
+    """Seeds of the trees this rank builds per step.  One tree per GPU
+    (seed = rank) for the single-tree workloads ("replicas only": a tree does
+    not shard); config 5 deals its 64 trees round-robin,
+    tree i -> GPU i mod N."""
+    if workload == "config5":
+        return [i for i in range(CONFIG5_TREES) if i % world_size == rank]
+    return [rank]
+
+
+def reduce_max(values: list[float], device=None) -> list[float]:
+    """Element-wise max over ranks (timings are reported as the slowest rank)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return list(values)
+    t = torch.tensor(values, dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.tolist()]
+
+
+def reduce_sum(values: list[float], device=None) -> list[float]:
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return list(values)
+    t = torch.tensor(values, dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return [float(x) for x in t.tolist()]
+
+
+def make_inputs(workload: str, n_override: int | None, seeds: list[int]):
     from paper_2401_06089_b200 import synth
     gen, n, desc = WORKLOADS[workload]
     if n_override:
         n = n_override
-    nv, u, v, w = synth.GENERATORS[gen](n, seed=seed)
-    return nv, u, v, w, desc
+    return [synth.GENERATORS[gen](n, seed=sd) for sd in seeds], desc
 
 
 def cpu_reference_rate(workload: str, n_sample: int, repeats: int) -> tuple[float, list[float]]:
@@ -200,27 +235,34 @@ def run_b200(args) -> None:
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
 
-    from paper_2401_06089_b200 import BuildResult, DendrogramBuilder, _lib
+    from paper_2401_06089_b200 import BuildResult, DendrogramBuilder
     from paper_2401_06089_b200.build import build as build_lib
     if rank == 0:
         build_lib()
     if ws > 1:
         torch.distributed.barrier()
 
-    nv, u, v, w, desc = make_input(args.workload, args.n, seed=rank)
-    n = int(u.shape[0])
+    seeds = replica_plan(args.workload, ws, rank)
+    trees, desc = make_inputs(args.workload, args.n, seeds)
     builder = DendrogramBuilder(dev)
-    du = torch.from_numpy(u).to(dev)
-    dv = torch.from_numpy(v).to(dev)
-    dw = torch.from_numpy(w).to(dev)
-    out = BuildResult(orig_of=torch.empty(n, dtype=torch.int32, device=dev),
-                      heights=torch.empty(n, dtype=torch.float64, device=dev),
-                      edge_parent=torch.empty(n, dtype=torch.int32, device=dev),
-                      vertex_parent=torch.empty(nv, dtype=torch.int32, device=dev))
+    n_max = max(int(t[1].shape[0]) for t in trees)
+    builder.workspace(n_max, n_max + 1)
+    dev_trees, outs = [], []
+    for nv, u, v, w in trees:
+        n = int(u.shape[0])
+        dev_trees.append((nv, torch.from_numpy(u).to(dev), torch.from_numpy(v).to(dev), torch.from_numpy(w).to(dev)))
+        outs.append(BuildResult(orig_of=torch.empty(n, dtype=torch.int32, device=dev),
+                                heights=torch.empty(n, dtype=torch.float64, device=dev),
+                                edge_parent=torch.empty(n, dtype=torch.int32, device=dev),
+                                vertex_parent=torch.empty(nv, dtype=torch.int32, device=dev)))
+    edges_rank = sum(int(t[1].shape[0]) for t in trees)
     stream = torch.cuda.current_stream(dev)
 
     def step(profile=False):
-        return builder.build(nv, du, dv, dw, out=out, profile=profile)
+        last = None
+        for (nv, du, dv, dw), out in zip(dev_trees, outs):
+            last = builder.build(nv, du, dv, dw, out=out, profile=profile)
+        return last
 
     for _ in range(args.warmup):
         step()
@@ -236,12 +278,13 @@ def run_b200(args) -> None:
     with ClockSampler(dev.index) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            res = step(profile=True)
-            launches += int(res.stats.kernel_launches)
-            for k, (ms, calls) in res.stats.kernel_profile().items():
-                p = prof.setdefault(k, [0.0, 0])
-                p[0] += ms
-                p[1] += calls
+            for (nv, du, dv, dw), out in zip(dev_trees, outs):
+                res = builder.build(nv, du, dv, dw, out=out, profile=True)
+                launches += int(res.stats.kernel_launches)
+                for k, (ms, calls) in res.stats.kernel_profile().items():
+                    p = prof.setdefault(k, [0.0, 0])
+                    p[0] += ms
+                    p[1] += calls
         e1.record(stream)
         torch.cuda.synchronize(dev)
     if ws > 1:
@@ -249,23 +292,25 @@ def run_b200(args) -> None:
     ms_step = e0.elapsed_time(e1) / args.steps
     stats = res.stats
     counts = stats.view_kind_counts()
+    n_last = int(dev_trees[-1][1].shape[0])
     S = sum(c[3] for c in counts[1:])
 
     # ---------------- end-to-end through the public API (host buffers) ----------------
-    hu = torch.from_numpy(u).pin_memory()
-    hv = torch.from_numpy(v).pin_memory()
-    hw = torch.from_numpy(w).pin_memory()
-    ho = torch.empty(n, dtype=torch.int32).pin_memory()
-    hh = torch.empty(n, dtype=torch.float64).pin_memory()
-    he = torch.empty(n, dtype=torch.int32).pin_memory()
-    hvp = torch.empty(nv, dtype=torch.int32).pin_memory()
+    host = []
+    for nv, u, v, w in trees:
+        n = int(u.shape[0])
+        host.append((nv, torch.from_numpy(u).pin_memory(), torch.from_numpy(v).pin_memory(),
+                     torch.from_numpy(w).pin_memory(), torch.empty(n, dtype=torch.int32).pin_memory(),
+                     torch.empty(n, dtype=torch.float64).pin_memory(), torch.empty(n, dtype=torch.int32).pin_memory(),
+                     torch.empty(nv, dtype=torch.int32).pin_memory()))
 
     def e2e_step():
-        r = builder.build(nv, hu, hv, hw, out=out)  # H2D inside (non_blocking from pinned)
-        ho.copy_(r.orig_of, non_blocking=True)
-        hh.copy_(r.heights, non_blocking=True)
-        he.copy_(r.edge_parent, non_blocking=True)
-        hvp.copy_(r.vertex_parent, non_blocking=True)
+        for (nv, hu, hv, hw, ho, hh, he, hvp), out in zip(host, outs):
+            r = builder.build(nv, hu, hv, hw, out=out)  # H2D inside (non_blocking from pinned)
+            ho.copy_(r.orig_of, non_blocking=True)
+            hh.copy_(r.heights, non_blocking=True)
+            he.copy_(r.edge_parent, non_blocking=True)
+            hvp.copy_(r.vertex_parent, non_blocking=True)
         stream.synchronize()
 
     e2e_step()
@@ -280,14 +325,16 @@ def run_b200(args) -> None:
     f1.record(stream)
     torch.cuda.synchronize(dev)
     e2e_ms = f0.elapsed_time(f1) / e2e_steps
-    if not np.array_equal(he[:1000].numpy(), out.edge_parent[:1000].cpu().numpy()):
+    he0 = host[0][6]
+    if not np.array_equal(he0[:1000].numpy(), outs[0].edge_parent[:1000].cpu().numpy()):
         raise RuntimeError("e2e output mismatch")
 
-    # ---------------- max over ranks ----------------
-    t = torch.tensor([ms_step, e2e_ms], dtype=torch.float64, device=dev)
-    if ws > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    ms_step, e2e_ms = float(t[0]), float(t[1])
+    # ---------------- max over ranks (time), sum over ranks (work) ----------------
+    ms_step, e2e_ms = reduce_max([ms_step, e2e_ms], device=dev)
+    (edges_total,) = reduce_sum([float(edges_rank)], device=dev)
+    h2d = sum(int(t[1].shape[0]) * 16 for t in trees)
+    d2h = sum(int(t[1].shape[0]) * 16 + int(t[0]) * 4 for t in trees)
+    h2d, d2h = reduce_sum([float(h2d), float(d2h)], device=dev)
 
     if rank == 0:
         peak, peak_src = load_peaks()
@@ -297,7 +344,8 @@ def run_b200(args) -> None:
         bpe = BYTES_PER_EDGE.get(kname)
         roof = None
         if bpe is not None:
-            achieved = bpe * n / (per_launch_ms * 1e-3) / 1e9
+            n_launch = n_last if kname not in ("mi_split", "mi_apply") else n_last
+            achieved = bpe * n_launch / (per_launch_ms * 1e-3) / 1e9
             traffic = None
             tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
             if os.path.exists(tpath):
@@ -307,33 +355,34 @@ def run_b200(args) -> None:
                     traffic = None
             roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": traffic,
-                    "algorithmic_bytes_per_launch": bpe * n, "avg_launch_ms": per_launch_ms,
+                    "algorithmic_bytes_per_launch": bpe * n_launch, "avg_launch_ms": per_launch_ms,
                     "peak_source": peak_src}
-        B = pipeline_bytes(n, S)
+        B = sum(pipeline_bytes(int(t[1].shape[0]), S) for t in trees) * ws
         pipe_ach = B / (ms_step * 1e-3) / 1e9
         cpu = None
         if ws == 1 and not args.no_cpu_baseline:
-            n_s = min(args.cpu_sample, n)
+            n_s = min(args.cpu_sample, n_last)
             rate, times = cpu_reference_rate(args.workload, n_s, 1)
             cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
                    "sample": f"oracle port (numpy + C union-find, 1 core) of rank_edges+pandora on "
                              f"{n_s} edges of the {args.workload} shape, {times[0]:.1f}s",
                    "host_cpus": os.cpu_count()}
+        n_tree = n_last
         line = {
-            "metric": METRIC, "value": ws * n / (ms_step * 1e-3), "unit": UNIT, "n_gpus": ws,
+            "metric": METRIC, "value": edges_total / (ms_step * 1e-3), "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "u64-key+int32", "data": "synthetic",
-            "config": {"workload": desc, "n_edges": n, "n_vertices": nv,
-                       "per_gpu": "one independent tree per GPU (replicas)" if ws > 1 else "one tree",
+            "higher_is_better": True, "scaling": "weak" if args.workload != "config5" else "strong",
+            "vs_baseline": None, "dtype": "u64-key+int32", "data": "synthetic",
+            "config": {"workload": desc, "n_edges": n_tree, "n_vertices": n_tree + 1,
+                       "trees_per_step": len(seeds) * ws if args.workload != "config5" else CONFIG5_TREES,
+                       "per_gpu": (f"{len(seeds)} tree(s) on rank 0; independent trees per GPU, no collective"),
                        "l2": "inputs (16 B/edge = %.1f GB) and working set larger than the 126 MB L2"
-                             % (16 * n / 1e9) if n > 10_000_000 else "small input (L2-resident)",
+                             % (16 * n_tree / 1e9) if n_tree > 10_000_000 else "working set per tree vs 126 MB L2",
                        "parallelism": f"replicas x{ws}", "levels": stats.num_levels,
                        "sort1_passes": stats.sort1_passes, "sort2_passes": stats.sort2_passes,
-                       "S_over_n": S / n},
-            "e2e": {"value": ws * n / (e2e_ms * 1e-3), "unit": UNIT,
-                    "h2d_bytes_per_step": n * (4 + 4 + 8),
-                    "d2h_bytes_per_step": n * (4 + 8 + 4) + nv * 4, "ms_per_step": e2e_ms},
+                       "S_over_n": S / n_tree},
+            "e2e": {"value": edges_total / (e2e_ms * 1e-3), "unit": UNIT,
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms},
             "roofline": roof,
             "pipeline_roofline": {"bound": "hbm", "achieved": pipe_ach, "peak": peak, "unit": "GB/s",
                                   "frac": pipe_ach / peak, "algorithmic_bytes_per_step": B,

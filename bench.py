@@ -244,9 +244,17 @@ def run_b200(args) -> None:
 
     seeds = replica_plan(args.workload, ws, rank)
     trees, desc = make_inputs(args.workload, args.n, seeds)
-    builder = DendrogramBuilder(dev)
     n_max = max(int(t[1].shape[0]) for t in trees)
-    builder.workspace(n_max, n_max + 1)
+    # several independent trees per GPU run concurrently on S streams (one host
+    # thread + builder + workspace each) so one tree's level-loop syncs overlap
+    # another tree's kernels
+    n_streams = max(1, min(args.streams, len(trees)))
+    builders = [DendrogramBuilder(dev) for _ in range(n_streams)]
+    for b in builders:
+        b.workspace(n_max, n_max + 1)
+    streams = [torch.cuda.current_stream(dev)] if n_streams == 1 else \
+        [torch.cuda.Stream(device=dev) for _ in range(n_streams)]
+    builder = builders[0]
     dev_trees, outs = [], []
     for nv, u, v, w in trees:
         n = int(u.shape[0])
@@ -258,19 +266,51 @@ def run_b200(args) -> None:
     edges_rank = sum(int(t[1].shape[0]) for t in trees)
     stream = torch.cuda.current_stream(dev)
 
-    def step(profile=False):
-        last = None
-        for (nv, du, dv, dw), out in zip(dev_trees, outs):
-            last = builder.build(nv, du, dv, dw, out=out, profile=profile)
-        return last
+    import threading
+    from concurrent.futures import ThreadPoolExecutor
+    pool = ThreadPoolExecutor(max_workers=n_streams) if n_streams > 1 else None
+    lock = threading.Lock()
+    prof: dict[str, list] = {}
+    counters = {"launches": 0}
+    last_res = [None]
+
+    def run_share(i, profile, start_evt, inputs):
+        b, s_ = builders[i], streams[i]
+        with torch.cuda.stream(s_):
+            if start_evt is not None:
+                s_.wait_event(start_evt)
+            for t in range(i, len(trees), n_streams):
+                nv, du, dv, dw = inputs[t]
+                res = b.build(nv, du, dv, dw, out=outs[t], profile=profile)
+                last_res[0] = res
+                if profile:
+                    with lock:
+                        counters["launches"] += int(res.stats.kernel_launches)
+                        for k, (ms, calls) in res.stats.kernel_profile().items():
+                            p = prof.setdefault(k, [0.0, 0])
+                            p[0] += ms
+                            p[1] += calls
+            done = torch.cuda.Event()
+            done.record(s_)
+        return done
+
+    def step(profile=False, inputs=None):
+        inputs = inputs or dev_trees
+        cur = torch.cuda.current_stream(dev)
+        start = torch.cuda.Event()
+        start.record(cur)
+        if pool is None:
+            done = [run_share(0, profile, start, inputs)]
+        else:
+            done = list(pool.map(lambda i: run_share(i, profile, start, inputs), range(n_streams)))
+        for d in done:
+            cur.wait_event(d)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
 
     # ---------------- device-resident timed region ----------------
-    prof: dict[str, list] = {}
-    launches = 0
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
@@ -278,17 +318,13 @@ def run_b200(args) -> None:
     with ClockSampler(dev.index) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            for (nv, du, dv, dw), out in zip(dev_trees, outs):
-                res = builder.build(nv, du, dv, dw, out=out, profile=True)
-                launches += int(res.stats.kernel_launches)
-                for k, (ms, calls) in res.stats.kernel_profile().items():
-                    p = prof.setdefault(k, [0.0, 0])
-                    p[0] += ms
-                    p[1] += calls
+            step(profile=True)
         e1.record(stream)
         torch.cuda.synchronize(dev)
     if ws > 1:
         torch.distributed.barrier()
+    launches = counters["launches"]
+    res = last_res[0]
     ms_step = e0.elapsed_time(e1) / args.steps
     stats = res.stats
     counts = stats.view_kind_counts()
@@ -304,13 +340,28 @@ def run_b200(args) -> None:
                      torch.empty(n, dtype=torch.float64).pin_memory(), torch.empty(n, dtype=torch.int32).pin_memory(),
                      torch.empty(nv, dtype=torch.int32).pin_memory()))
 
+    def e2e_share(i, start_evt):
+        b, s_ = builders[i], streams[i]
+        with torch.cuda.stream(s_):
+            s_.wait_event(start_evt)
+            for t in range(i, len(trees), n_streams):
+                nv, hu, hv, hw, ho, hh, he, hvp = host[t]
+                r = b.build(nv, hu, hv, hw, out=outs[t])  # H2D inside (non_blocking from pinned)
+                ho.copy_(r.orig_of, non_blocking=True)
+                hh.copy_(r.heights, non_blocking=True)
+                he.copy_(r.edge_parent, non_blocking=True)
+                hvp.copy_(r.vertex_parent, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(s_)
+        return done
+
     def e2e_step():
-        for (nv, hu, hv, hw, ho, hh, he, hvp), out in zip(host, outs):
-            r = builder.build(nv, hu, hv, hw, out=out)  # H2D inside (non_blocking from pinned)
-            ho.copy_(r.orig_of, non_blocking=True)
-            hh.copy_(r.heights, non_blocking=True)
-            he.copy_(r.edge_parent, non_blocking=True)
-            hvp.copy_(r.vertex_parent, non_blocking=True)
+        start = torch.cuda.Event()
+        start.record(stream)
+        done = [e2e_share(0, start)] if pool is None else \
+            list(pool.map(lambda i: e2e_share(i, start), range(n_streams)))
+        for d in done:
+            stream.wait_event(d)
         stream.synchronize()
 
     e2e_step()
@@ -374,6 +425,7 @@ def run_b200(args) -> None:
             "higher_is_better": True, "scaling": "weak" if args.workload != "config5" else "strong",
             "vs_baseline": None, "dtype": "u64-key+int32", "data": "synthetic",
             "config": {"workload": desc, "n_edges": n_tree, "n_vertices": n_tree + 1,
+                       "streams_per_gpu": n_streams,
                        "trees_per_step": len(seeds) * ws if args.workload != "config5" else CONFIG5_TREES,
                        "per_gpu": (f"{len(seeds)} tree(s) on rank 0; independent trees per GPU, no collective"),
                        "l2": "inputs (16 B/edge = %.1f GB) and working set larger than the 126 MB L2"
@@ -407,6 +459,7 @@ def main() -> None:
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="config4")
     ap.add_argument("--n", type=int, default=None, help="override the workload's edge count")
     ap.add_argument("--cpu-sample", type=int, default=8_000_000)
+    ap.add_argument("--streams", type=int, default=4, help="concurrent trees per GPU (multi-tree workloads)")
     ap.add_argument("--ref-sample", type=int, default=2_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -41,6 +41,13 @@ __device__ __forceinline__ uint32_t ld_keep(const uint32_t* p, uint64_t pol) {
   asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
   return v;
 }
+__device__ __forceinline__ uint2 ld_keep2(const uint2* p, uint64_t pol) {
+  uint2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+
+
 
 __device__ __forceinline__ uint32_t warp_incl_sum(uint32_t x) {
 #pragma unroll

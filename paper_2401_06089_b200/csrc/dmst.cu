@@ -88,8 +88,8 @@ struct Workspace {
   int2* euv0;             // rank-order endpoints
   unsigned long long* mi64_0;
   unsigned long long* mi64[2];  // views >= 1 (ping-pong)
-  uint32_t* cnt2;         // 2-bit child counts per edge
-  uint32_t* leafpre;      // leaf prefix per 16-edge word
+  uint32_t* cnt2;         // 2-bit child counts per edge (16 per word)
+  uint2* kw;              // (cnt2 word, leaf prefix) per 16 edges, for V2
   int8_t* ret;            // retirement level per edge
   int2* euv[2];           // view edges (ping-pong)
   int32_t* grank[2];
@@ -126,7 +126,7 @@ Workspace carve(int64_t n, int64_t nv, char* base) {
   w.mi64_0 = (unsigned long long*)take(8 * nv);
   for (int i = 0; i < 2; ++i) w.mi64[i] = (unsigned long long*)take(8 * (half + 1));
   w.cnt2 = (uint32_t*)take(4 * (n / 16 + 2));
-  w.leafpre = (uint32_t*)take(4 * (n / 16 + 2));
+  w.kw = (uint2*)take(8 * (n / 16 + 2));
   w.ret = (int8_t*)take(n);
   for (int i = 0; i < 2; ++i) {
     w.euv[i] = (int2*)take(8 * half);
@@ -393,15 +393,15 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     c.zero(misc + MISC_COUNTS, 8);
     c.zero(misc + MISC_LSCTR, 4);
     c.begin(KK_LEAFSCAN);
-    k_leafscan<<<grid_for(words, 2048), 256, 0, c.s>>>(words, w.cnt2, w.leafpre, w.sel_status,
-                                                       misc + MISC_LSCTR, misc + MISC_COUNTS);
+    k_leafscan<<<grid_for(words, 2048), 256, 0, c.s>>>(words, w.cnt2, w.kw, w.sel_status, misc + MISC_LSCTR,
+                                                       misc + MISC_COUNTS);
     c.launched();
     // V2: supervertex labels (vertex_map).  Runs before the host reads the
     // counts (one sync per level); on the final view its result is unused.
     int32_t* vm = w.vm_all + voff;
     c.zero(misc + MISC_ACTIVE0, 12);
     c.begin(KK_V2);
-    k_v2<<<grid_for(nv_k, EW_BLOCK), EW_BLOCK, 0, c.s>>>(nv_k, mi_k, w.cnt2, w.leafpre, vm, lists[0], lcnt[0]);
+    k_v2<<<grid_for(nv_k, EW_BLOCK), EW_BLOCK, 0, c.s>>>(nv_k, mi_k, w.kw, vm, lists[0], lcnt[0]);
     c.launched();
     uint32_t counts[3];
     c.to_host(counts, misc + MISC_COUNTS, 8);

@@ -241,11 +241,13 @@ __device__ __forceinline__ uint32_t chain_bits(uint32_t w) { return w & 0x555555
 // Exclusive prefix of leaf-edge counts per 16-edge word (single pass,
 // decoupled look-back) + view totals (n_leaf, n_chain).  A supervertex is
 // numbered by the rank order of its component's leaf edge, so
-// label(leaf j) = leafpre[j >> 4] + leaves below j in its word: a lookup
+// label(leaf j) = kw[j >> 4].y + leaves below j in its word: a lookup
 // into two L2-resident arrays (n/4 bytes each) instead of a scan over
 // vertices and a gather.
+// kw[w] = (cnt2[w], exclusive count of leaf edges before edge 16w): one
+// 8-B lookup gives an edge's kind and its leaf ordinal (V2).
 __global__ void __launch_bounds__(256) k_leafscan(int64_t words, const uint32_t* __restrict__ cnt2,
-                                                  uint32_t* __restrict__ leafpre, uint32_t* __restrict__ status,
+                                                  uint2* __restrict__ kw, uint32_t* __restrict__ status,
                                                   uint32_t* __restrict__ tile_ctr, uint32_t* __restrict__ counts) {
   constexpr int ITEMS = 8, TILE = 256 * ITEMS;
   __shared__ uint32_t s_tile, s_excl;
@@ -254,10 +256,11 @@ __global__ void __launch_bounds__(256) k_leafscan(int64_t words, const uint32_t*
   __syncthreads();
   const uint32_t tile = s_tile;
   const int64_t base = (int64_t)tile * TILE + (int64_t)threadIdx.x * ITEMS;
-  uint32_t lc[ITEMS], sum = 0, chains = 0;
+  uint32_t lc[ITEMS], cw[ITEMS], sum = 0, chains = 0;
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
-    uint32_t w = base + i < words ? cnt2[base + i] : 0u;
+    const uint32_t w = base + i < words ? cnt2[base + i] : 0u;
+    cw[i] = w;
     lc[i] = __popc(leaf_bits(w));
     chains += __popc(chain_bits(w));
     sum += lc[i];
@@ -283,16 +286,14 @@ __global__ void __launch_bounds__(256) k_leafscan(int64_t words, const uint32_t*
   uint32_t run = s_excl + excl;
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
-    if (base + i < words) leafpre[base + i] = run;
+    if (base + i < words) kw[base + i] = make_uint2(cw[i], run);
     run += lc[i];
   }
 }
 
-__device__ __forceinline__ uint32_t leaf_label(const uint32_t* __restrict__ cnt2,
-                                               const uint32_t* __restrict__ leafpre, uint32_t j, uint64_t pol) {
-  const uint32_t w = ld_keep(cnt2 + (j >> 4), pol);
+__device__ __forceinline__ uint32_t leaf_label(uint2 w, uint32_t j) {
   const uint32_t below = (1u << ((j & 15) * 2)) - 1u;
-  return ld_keep(leafpre + (j >> 4), pol) + __popc(leaf_bits(w) & below);
+  return w.y + __popc(leaf_bits(w.x) & below);
 }
 
 // V2: chase maxIncident pointers to the component's leaf edge (ranks grow
@@ -301,8 +302,7 @@ __device__ __forceinline__ uint32_t leaf_label(const uint32_t* __restrict__ cnt2
 // (component_labels + contract_level, contraction.py:82-93, :165-169).
 // Vertices still unresolved after CHASE_STEPS (deep in-trees: chains)
 // store ~y (y = the vertex where the chase stopped) and go to pointer jumping.
-__global__ void k_v2(int64_t nv, const unsigned long long* __restrict__ mi64,
-                     const uint32_t* __restrict__ cnt2, const uint32_t* __restrict__ leafpre,
+__global__ void k_v2(int64_t nv, const unsigned long long* __restrict__ mi64, const uint2* __restrict__ kw,
                      int32_t* __restrict__ vm, int32_t* __restrict__ active, uint32_t* __restrict__ active_cnt) {
   const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t pol = l2_keep_policy();
@@ -312,8 +312,10 @@ __global__ void k_v2(int64_t nv, const unsigned long long* __restrict__ mi64,
     uint32_t j = (uint32_t)(m >> 32) - 1u;
     uint32_t y = (uint32_t)m;
     int s = 0;
+    uint2 kwj = make_uint2(0, 0);
     while (m != 0ull) {  // m == 0: isolated vertex (single-vertex view), label 0
-      const uint32_t c = (ld_keep(cnt2 + (j >> 4), pol) >> ((j & 15) * 2)) & 3u;
+      kwj = ld_keep2(kw + (j >> 4), pol);
+      const uint32_t c = (kwj.x >> ((j & 15) * 2)) & 3u;
       if (c == 2u) break;
       if (++s > CHASE_STEPS) {
         unresolved = true;
@@ -323,7 +325,7 @@ __global__ void k_v2(int64_t nv, const unsigned long long* __restrict__ mi64,
       j = (uint32_t)(m >> 32) - 1u;
       y = (uint32_t)m;
     }
-    __stcs(vm + x, unresolved ? ~(int32_t)y : (m ? (int32_t)leaf_label(cnt2, leafpre, j, pol) : 0));
+    __stcs(vm + x, unresolved ? ~(int32_t)y : (m ? (int32_t)leaf_label(kwj, j) : 0));
   }
   const uint32_t msk = __ballot_sync(kFull, unresolved);
   if (msk) {
@@ -447,7 +449,7 @@ struct EdgeSel {
   __device__ __forceinline__ void init_shared(Shared&) const {}
   __device__ __forceinline__ void flush_shared(Shared&) const {}
   __device__ __forceinline__ bool flag(int64_t j, Item& it) const {
-    uint32_t c = (cnt2[j >> 4] >> ((j & 15) * 2)) & 3u;
+    const uint32_t c = (cnt2[j >> 4] >> ((j & 15) * 2)) & 3u;
     it.g = grank ? __ldcs(grank + j) : (int32_t)j;
     return c == 0;
   }
@@ -456,8 +458,8 @@ struct EdgeSel {
     if (!alpha) {
       ret[it.g] = level;
     } else {
-      int2 e = __ldcs(euv + j);
-      int32_t a = vm[e.x], b = vm[e.y];
+      const int2 e = __ldcs(euv + j);
+      const int32_t a = vm[e.x], b = vm[e.y];
       __stcs(euv_next + pos, make_int2(a, b));
       __stcs(grank_next + pos, it.g);
       if (mi64_next) {

@@ -291,6 +291,7 @@ __device__ __forceinline__ uint32_t warp_rank(uint32_t* whist, uint32_t d, bool 
   uint32_t old = 0;
   if (FULL || valid) old = whist[d];
   const uint32_t below = __popc(peers & lt);
+  __syncwarp();  // order all peers' reads of the counter before the leader's write
   if ((FULL || valid) && below == 0) whist[d] = old + __popc(peers);
   __syncwarp();
   return old + below;

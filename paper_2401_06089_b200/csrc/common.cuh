@@ -110,4 +110,31 @@ __device__ __forceinline__ uint32_t lookback(const uint32_t* status, uint32_t ti
   return excl;
 }
 
+// Warp-cooperative look-back (single status word per tile): lane i loads
+// predecessor tile-1-i; the nearest inclusive prefix ends the walk, the
+// aggregates in front of it are summed with a warp reduction.  Call with the
+// whole warp; every lane returns the exclusive prefix of `tile`.
+__device__ __forceinline__ uint32_t warp_lookback(const uint32_t* status, uint32_t tile) {
+  const uint32_t lane = lane_id();
+  uint32_t excl = 0;
+  int64_t j0 = (int64_t)tile - 1;
+  while (j0 >= 0) {
+    const int64_t j = j0 - lane;
+    uint32_t s = j >= 0 ? ld_relaxed(status + j) : kFlagPrefix;  // before tile 0: prefix 0
+    // wait until every lane's word is published
+    while (__any_sync(kFull, s == 0)) {
+      if (s == 0) s = ld_relaxed(status + j);
+    }
+    const uint32_t pre = __ballot_sync(kFull, (s & kFlagPrefix) != 0);
+    const uint32_t stop = pre ? __ffs(pre) - 1 : 32;  // first lane holding a prefix
+    uint32_t v = lane <= stop ? (s & kValMask) : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    excl += v;
+    if (pre) break;
+    j0 -= 32;
+  }
+  return excl;
+}
+
 }  // namespace dmst

@@ -267,17 +267,14 @@ __global__ void __launch_bounds__(256) k_leafscan(int64_t words, const uint32_t*
   }
   uint32_t total;
   uint32_t excl = block_excl_sum<256>(sum, scratch, &total);
-  if (threadIdx.x == 0) {
-    uint32_t prev = 0;
-    if (tile == 0) {
-      st_relaxed(status, kFlagPrefix | total);
-    } else {
-      st_relaxed(status + tile, kFlagAgg | total);
-      prev = lookback(status, tile, 1);
-      st_relaxed(status + tile, kFlagPrefix | (prev + total));
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) st_relaxed(status + tile, (tile == 0 ? kFlagPrefix : kFlagAgg) | total);
+    const uint32_t prev = tile == 0 ? 0u : warp_lookback(status, tile);
+    if (threadIdx.x == 0) {
+      if (tile) st_relaxed(status + tile, kFlagPrefix | (prev + total));
+      s_excl = prev;
+      atomicAdd(counts + 0, total);
     }
-    s_excl = prev;
-    atomicAdd(counts + 0, total);
   }
   uint32_t ctot;
   block_excl_sum<256>(chains, scratch, &ctot);
@@ -400,15 +397,10 @@ k_select(int64_t n, uint32_t* __restrict__ status, uint32_t* __restrict__ tile_c
     uint32_t incl = warp_incl_sum(c);
     if (lane < NW) s_warp[lane] = incl - c;
     uint32_t total = __shfl_sync(kFull, incl, NW - 1);
+    if (lane == 0) st_relaxed(status + tile, (tile == 0 ? kFlagPrefix : kFlagAgg) | total);
+    const uint32_t excl = tile == 0 ? 0u : warp_lookback(status, tile);
     if (lane == 0) {
-      uint32_t excl = 0;
-      if (tile == 0) {
-        st_relaxed(status, kFlagPrefix | total);
-      } else {
-        st_relaxed(status + tile, kFlagAgg | total);
-        excl = lookback(status, tile, 1);
-        st_relaxed(status + tile, kFlagPrefix | (excl + total));
-      }
+      if (tile) st_relaxed(status + tile, kFlagPrefix | (excl + total));
       s_excl = excl;
       if (tile == gridDim.x - 1) totals[0] = excl + total;
     }

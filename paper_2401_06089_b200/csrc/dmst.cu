@@ -107,7 +107,7 @@ constexpr int SM_HIST1 = 0, SM_GBASE1 = SM_HIST1 + 8 * kRadix, SM_HIST2 = SM_GBA
               SM_GBASE2 = SM_HIST2 + 4 * kRadix, SM_VHIST = SM_GBASE2 + 4 * kRadix,
               SM_VBASE = SM_VHIST + kRadix, SM_TILECTR = SM_VBASE + kRadix, SM_MISC = SM_TILECTR + 64;
 constexpr int MISC_NEGZERO = 0, MISC_ACTIVE0 = 1, MISC_ACTIVE1 = 2, MISC_ACTIVE2 = 3, MISC_COUNTS = 4 /*2*/,
-              MISC_SELTOT = 8 /*1*/, MISC_SELCTR = 12, MISC_LSCTR = 13;
+              MISC_NONRUL = 6, MISC_SELTOT = 8 /*1*/, MISC_SELCTR = 12, MISC_LSCTR = 13;
 
 Workspace carve(int64_t n, int64_t nv, char* base) {
   Workspace w{};
@@ -375,8 +375,9 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
   const unsigned long long* mi_k = w.mi64_0;
   int cur = 0, level = 0, jump_rounds = 0;
   int64_t voff = 0, soff = 0;
-  int32_t* lists[3] = {(int32_t*)w.R, (int32_t*)w.R + nv, (int32_t*)w.R + 2 * nv};
-  uint32_t* lcnt[3] = {misc + MISC_ACTIVE0, misc + MISC_ACTIVE1, misc + MISC_ACTIVE2};
+  // jump lists in R: rulers (+ 2 ping-pong) and non-rulers
+  int32_t* lists[4] = {(int32_t*)w.R, (int32_t*)w.R + nv, (int32_t*)w.R + 2 * nv, (int32_t*)w.R + 3 * nv};
+  uint32_t* lcnt[4] = {misc + MISC_ACTIVE0, misc + MISC_ACTIVE1, misc + MISC_ACTIVE2, misc + MISC_NONRUL};
   while (true) {
     if (level >= DMST_MAX_LEVELS) invalid("too many contraction levels");
     // V1: maxIncident edge per vertex + child counts per edge (already done
@@ -400,12 +401,15 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     // counts (one sync per level); on the final view its result is unused.
     int32_t* vm = w.vm_all + voff;
     c.zero(misc + MISC_ACTIVE0, 12);
+    c.zero(misc + MISC_NONRUL, 4);
     c.begin(KK_V2);
-    k_v2<<<grid_for(nv_k, EW_BLOCK), EW_BLOCK, 0, c.s>>>(nv_k, mi_k, w.kw, vm, lists[0], lcnt[0]);
+    k_v2<<<grid_for(nv_k, EW_BLOCK), EW_BLOCK, 0, c.s>>>(nv_k, mi_k, w.kw, vm, lists[0], lcnt[0], lists[3],
+                                                         lcnt[3]);
     c.launched();
-    uint32_t counts[3];
+    uint32_t counts[4];
     c.to_host(counts, misc + MISC_COUNTS, 8);
     c.to_host(counts + 2, lcnt[0], 4);
+    c.to_host(counts + 3, lcnt[3], 4);
     c.sync();
     const int64_t n_leaf = counts[0], n_chain = counts[1];
     const int64_t n_alpha = n_k - n_leaf - n_chain;
@@ -426,11 +430,12 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     }
     lt.voff[level] = voff;
     voff += nv_k;
-    uint32_t pending = counts[2];
-    if (pending) {
-      // pointer jumping over the unresolved vertices
-      const int32_t* in = lists[0];
-      const uint32_t* in_cnt = lcnt[0];
+    // pointer jumping: rulers first (a chain of rulers ~1/32 as long as the
+    // in-tree), then the non-rulers, whose targets are then resolved rulers
+    for (int phase = 0; phase < 2; ++phase) {
+      uint32_t pending = counts[phase == 0 ? 2 : 3];
+      const int32_t* in = lists[phase == 0 ? 0 : 3];
+      const uint32_t* in_cnt = lcnt[phase == 0 ? 0 : 3];
       int a = 1;
       while (pending) {
         c.zero(lcnt[a], 4);

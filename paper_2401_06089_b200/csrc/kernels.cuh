@@ -12,7 +12,12 @@ namespace dmst {
 constexpr int EW_BLOCK = 256;                  // elementwise kernels
 constexpr int SEL_BLOCK = 256, SEL_ITEMS = 8;  // select-scan tiles
 constexpr int SEL_TILE = SEL_BLOCK * SEL_ITEMS;
-constexpr int CHASE_STEPS = 16;                // V2 bounded walk before pointer jumping
+constexpr int CHASE_FREE = 8;    // V2 chase steps before rulers may end a chase
+constexpr int CHASE_CAP = 512;   // hard bound on one V2 chase
+
+// ~1/32 of vertices are "rulers": a long chase stops at the first ruler it
+// reaches, so pointer jumping only runs over rulers (deep in-trees: chains).
+__device__ __forceinline__ bool is_ruler(uint32_t v) { return ((v * 0x9E3779B1u) >> 27) == 0; }
 
 // ------------------------------------------------------------ key codec
 // Order-preserving map of (w + 0.0) to uint64, inverted so that ascending
@@ -297,10 +302,12 @@ __device__ __forceinline__ uint32_t leaf_label(uint2 w, uint32_t j) {
 // strictly along the chase; the leaf edge is the component's lightest
 // edge) and label the vertex with that leaf's number: vertex_map
 // (component_labels + contract_level, contraction.py:82-93, :165-169).
-// Vertices still unresolved after CHASE_STEPS (deep in-trees: chains)
-// store ~y (y = the vertex where the chase stopped) and go to pointer jumping.
+// A chase longer than CHASE_FREE steps stops at the first ruler vertex (or
+// after CHASE_CAP steps) and stores ~y (y = where it stopped); rulers and
+// non-rulers go to separate lists for pointer jumping.
 __global__ void k_v2(int64_t nv, const unsigned long long* __restrict__ mi64, const uint2* __restrict__ kw,
-                     int32_t* __restrict__ vm, int32_t* __restrict__ active, uint32_t* __restrict__ active_cnt) {
+                     int32_t* __restrict__ vm, int32_t* __restrict__ rul, uint32_t* __restrict__ rul_cnt,
+                     int32_t* __restrict__ non, uint32_t* __restrict__ non_cnt) {
   const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t pol = l2_keep_policy();
   bool unresolved = false;
@@ -314,7 +321,7 @@ __global__ void k_v2(int64_t nv, const unsigned long long* __restrict__ mi64, co
       kwj = ld_keep2(kw + (j >> 4), pol);
       const uint32_t c = (kwj.x >> ((j & 15) * 2)) & 3u;
       if (c == 2u) break;
-      if (++s > CHASE_STEPS) {
+      if (++s > CHASE_CAP || (s > CHASE_FREE && is_ruler(y))) {
         unresolved = true;
         break;
       }
@@ -324,12 +331,18 @@ __global__ void k_v2(int64_t nv, const unsigned long long* __restrict__ mi64, co
     }
     __stcs(vm + x, unresolved ? ~(int32_t)y : (m ? (int32_t)leaf_label(kwj, j) : 0));
   }
-  const uint32_t msk = __ballot_sync(kFull, unresolved);
-  if (msk) {
-    uint32_t lead = __ffs(msk) - 1, b = 0;
-    if (lane_id() == lead) b = atomicAdd(active_cnt, __popc(msk));
-    b = __shfl_sync(kFull, b, lead);
-    if (unresolved) active[b + __popc(msk & lanemask_lt())] = (int32_t)x;
+  const bool ruler = unresolved && is_ruler((uint32_t)x);
+  const bool plain = unresolved && !ruler;
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const bool mine = t == 0 ? ruler : plain;
+    const uint32_t msk = __ballot_sync(kFull, mine);
+    if (msk) {
+      uint32_t lead = __ffs(msk) - 1, b = 0;
+      if (lane_id() == lead) b = atomicAdd(t == 0 ? rul_cnt : non_cnt, __popc(msk));
+      b = __shfl_sync(kFull, b, lead);
+      if (mine) (t == 0 ? rul : non)[b + __popc(msk & lanemask_lt())] = (int32_t)x;
+    }
   }
 }
 

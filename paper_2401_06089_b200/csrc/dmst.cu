@@ -35,7 +35,7 @@ namespace dmst {
 // ----------------------------------------------------------------- config
 // Radix sort geometry (sub-tile = BLOCK x ITEMS items; MINB CTAs per SM).
 // Edge sort: u64 key + 3-word payload.
-constexpr int S1_BLOCK = 256, S1_ITEMS = 6, S1_MINB = 2;
+constexpr int S1_BLOCK = 256, S1_ITEMS = 8, S1_MINB = 2;
 // Chain sort: u32 key + 1-word payload.
 constexpr int S2_BLOCK = 256, S2_ITEMS = 16, S2_MINB = 2, S2_BITS = 8;  // 9-bit digits measured slower (shorter runs)
 constexpr int64_t kDirectMiBytes = 24ll << 20;  // direct scatter-max below this mi64 size

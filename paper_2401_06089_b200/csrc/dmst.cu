@@ -35,7 +35,7 @@ namespace dmst {
 // ----------------------------------------------------------------- config
 // Radix sort geometry (sub-tile = BLOCK x ITEMS items; MINB CTAs per SM).
 // Edge sort: u64 key + 3-word payload.
-constexpr int S1_BLOCK = 256, S1_ITEMS = 8, S1_MINB = 2;
+constexpr int S1_BLOCK = 512, S1_ITEMS = 8, S1_MINB = 1;
 // Chain sort: u32 key + 1-word payload.
 constexpr int S2_BLOCK = 256, S2_ITEMS = 16, S2_MINB = 2, S2_BITS = 8;  // 9-bit digits measured slower (shorter runs)
 constexpr int64_t kDirectMiBytes = 24ll << 20;  // direct scatter-max below this mi64 size
@@ -208,11 +208,11 @@ struct Ctx {
 };
 
 // One radix pass: upsweep (per-chunk digit counts), chunk scan, downsweep.
-template <typename K, int VW, int BLOCK, int ITEMS, int MINB, int BITS, class Loader, class Emitter>
+template <typename K, int PW, int BLOCK, int ITEMS, int MINB, int BITS, class Loader, class Emitter>
 void radix_pass(Ctx& c, int kind, int64_t n, int shift, Loader ld, Emitter em) {
-  using S = DownSmem<K, VW, BLOCK, ITEMS, Loader, BITS>;
+  using S = DownSmem<K, PW, BLOCK, ITEMS, Loader, BITS>;
   constexpr int T = S::T;
-  auto kern = k_downsweep<K, VW, BLOCK, ITEMS, MINB, Loader, Emitter, BITS>;
+  auto kern = k_downsweep<K, PW, BLOCK, ITEMS, MINB, Loader, Emitter, BITS>;
   DMST_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes()));
   SweepArgs a;
   a.n = n;
@@ -223,7 +223,6 @@ void radix_pass(Ctx& c, int kind, int64_t n, int shift, Loader ld, Emitter em) {
   a.G = (uint32_t)G;
   a.GS = (uint32_t)((G + 3) & ~int64_t(3));
   a.counts = c.w.counts;
-  a.prof = nullptr;
   c.zero(a.counts, 4 * (size_t(1) << BITS) * a.GS);
   c.begin(KK_UPSWEEP);
   k_upsweep<BITS, Loader><<<(unsigned)(G * kUpSplit), 256, 0, c.s>>>(a, ld);
@@ -237,37 +236,30 @@ void radix_pass(Ctx& c, int kind, int64_t n, int shift, Loader ld, Emitter em) {
 }
 
 // Multi-pass driver over the non-constant digits (bit offsets `shifts`).
-// Ping-pong SoA buffers bufK[2], bufV[2][VW]; first/last passes use the given
-// loader/emitter.
-template <typename K, int VW, int BLOCK, int ITEMS, int MINB, int BITS, class FirstLoader, class FinalEmitter>
+// Ping-pong buffers: keys bufK[2], AoS payload bufP[2] (PW words per item);
+// first/last passes use the given loader/emitter.
+template <typename K, int PW, int BLOCK, int ITEMS, int MINB, int BITS, class FirstLoader, class FinalEmitter>
 void run_sort(Ctx& c, const int (&kinds)[3], int64_t n, const std::vector<int>& shifts,
-              K* const (&bufK)[2], uint32_t* const (&bufV)[2][VW], FirstLoader first,
-              FinalEmitter final_em) {
+              K* const (&bufK)[2], uint32_t* const (&bufP)[2], FirstLoader first, FinalEmitter final_em) {
   const int P = (int)shifts.size();
   if (P == 0) {
     c.begin(KK_OTHER);
-    k_identity_pass<K, VW><<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(n, first, final_em);
+    k_identity_pass<K, PW, EW_BLOCK><<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(n, first, final_em);
     c.launched();
     return;
   }
   for (int p = 0; p < P; ++p) {
     const int o = p % 2, in = o ^ 1;
-    ArrayEmitter<K, VW> mid;
-    ArrayLoader<K, VW> ldr;
-    mid.keys = bufK[o];
-    ldr.keys = bufK[in];
-    for (int q = 0; q < VW; ++q) {
-      mid.vals[q] = bufV[o][q];
-      ldr.vals[q] = bufV[in][q];
-    }
+    ArrayEmitter<K, PW> mid{bufK[o], bufP[o]};
+    ArrayLoader<K, PW> ldr{bufK[in], bufP[in]};
     if (P == 1)
-      radix_pass<K, VW, BLOCK, ITEMS, MINB, BITS>(c, kinds[2], n, shifts[p], first, final_em);
+      radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[2], n, shifts[p], first, final_em);
     else if (p == 0)
-      radix_pass<K, VW, BLOCK, ITEMS, MINB, BITS>(c, kinds[0], n, shifts[p], first, mid);
+      radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[0], n, shifts[p], first, mid);
     else if (p == P - 1)
-      radix_pass<K, VW, BLOCK, ITEMS, MINB, BITS>(c, kinds[2], n, shifts[p], ldr, final_em);
+      radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[2], n, shifts[p], ldr, final_em);
     else
-      radix_pass<K, VW, BLOCK, ITEMS, MINB, BITS>(c, kinds[1], n, shifts[p], ldr, mid);
+      radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[1], n, shifts[p], ldr, mid);
   }
 }
 
@@ -302,9 +294,9 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
   char* R = c.w.R;
   uint64_t* const bufK[2] = {(uint64_t*)R, (uint64_t*)(R + 8 * n)};
   uint32_t* vb = (uint32_t*)(R + 16 * n);
-  uint32_t* const bufV[2][3] = {{vb, vb + n, vb + 2 * n}, {vb + 3 * n, vb + 4 * n, vb + 5 * n}};
+  uint32_t* const bufP[2] = {vb, vb + 3 * n};
   run_sort<uint64_t, 3, S1_BLOCK, S1_ITEMS, S1_MINB, 8>(c, {KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL}, n,
-                                                     shifts, bufK, bufV, Sort1FirstLoader{w, u, v}, em);
+                                                     shifts, bufK, bufP, Sort1FirstLoader{w, u, v}, em);
   if (nz) {
     c.begin(KK_OTHER);
     k_fix_negzero<<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(w, em.orig_of, em.heights, n);
@@ -538,15 +530,13 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
   if (!shifts.empty()) {
     uint32_t* base = (uint32_t*)w.R;
     uint32_t* const bufK[2] = {base + n, base + 3 * n};
-    uint32_t* const bufV[2][1] = {{base + 2 * n}, {base + 4 * n}};
+    uint32_t* const bufP[2] = {base + 2 * n, base + 4 * n};
     const int lastb = ((int)shifts.size() - 1) % 2;
-    ArrayEmitter<uint32_t, 1> fin;
-    fin.keys = bufK[lastb];
-    fin.vals[0] = bufV[lastb][0];
+    ArrayEmitter<uint32_t, 1> fin{bufK[lastb], bufP[lastb]};
     run_sort<uint32_t, 1, S2_BLOCK, S2_ITEMS, S2_MINB, S2_BITS>(c, {KK_SORT2_PASS, KK_SORT2_PASS, KK_SORT2_PASS}, n,
-                                                       shifts, bufK, bufV, Sort2FirstLoader{keys}, fin);
+                                                       shifts, bufK, bufP, Sort2FirstLoader{keys}, fin);
     skeys = fin.keys;
-    svals = fin.vals[0];
+    svals = fin.pay;
   }
   c.begin(KK_LINK);
   k_link<<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(n, skeys, svals, w.smi_all, edge_parent);

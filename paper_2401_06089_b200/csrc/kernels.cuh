@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) k_key_reduce(const double* __restrict__ w
 // First pass: key from w; payload (original id, u, v) carried through the
 // sort so the final pass needs no random gathers.
 struct Sort1FirstLoader {
-  static constexpr int NS = 3, IPE = 1;
+  static constexpr int NS = 3;
   __host__ __device__ static constexpr int sb(int s) { return s == 0 ? 8 : 4; }
   const double* __restrict__ w;
   const int32_t* __restrict__ u;
@@ -97,28 +97,28 @@ struct Sort1FirstLoader {
   }
 };
 
-// Final pass: RankedTree outputs (orig_of, w by rank) + rank-order endpoints.
+// Final pass: RankedTree outputs (orig_of, w by rank) + rank-order endpoints,
+// written from the sorted sub-tile (payload = (original id, u, v)).
 struct Sort1FinalEmitter {
   int32_t* __restrict__ orig_of;
   double* __restrict__ heights;
   int2* __restrict__ euv;        // rank-order endpoints (pipeline)
   int32_t* __restrict__ ru;      // optional split copies (dmst_rank_edges)
   int32_t* __restrict__ rv;
-  template <int N>
-  __device__ __forceinline__ void emit(const uint32_t (&dst)[N], const uint64_t (&k)[N],
-                                       const Vals<3> (&p)[N], const bool (&ok)[N]) const {
-#pragma unroll
-    for (int i = 0; i < N; ++i)
-      if (ok[i]) {
-        const uint32_t r = dst[i];
-        orig_of[r] = (int32_t)p[i].w[0];
-        heights[r] = key_to_double(k[i]);
-        if (euv) euv[r] = make_int2((int)p[i].w[1], (int)p[i].w[2]);
-        if (ru) {
-          ru[r] = (int32_t)p[i].w[1];
-          rv[r] = (int32_t)p[i].w[2];
-        }
+  template <int BLOCK, class Tile>
+  __device__ __forceinline__ void emit(const Tile& t) const {
+    for (int s = threadIdx.x; s < t.cnt; s += BLOCK) {
+      const uint64_t k = t.skeys[s];
+      const uint32_t r = t.gofs[digit_of<kRadixBits>(k, t.shift)] + (uint32_t)s;
+      const uint32_t* p = t.spay + 3 * s;
+      orig_of[r] = (int32_t)p[0];
+      heights[r] = key_to_double(k);
+      if (euv) euv[r] = make_int2((int)p[1], (int)p[2]);
+      if (ru) {
+        ru[r] = (int32_t)p[1];
+        rv[r] = (int32_t)p[2];
       }
+    }
   }
 };
 
@@ -140,79 +140,11 @@ __global__ void k_pack_euv(const int32_t* __restrict__ ru, const int32_t* __rest
 // mi64[x] = max over edges j incident to x of ((j + 1) << 32 | other end):
 // the largest incident rank (maxIncident, tree_core.py:193-199 /
 // contraction.py:149-154) packed with the vertex across that edge, 0 for
-// an isolated vertex.  Records (x, j+1, other) are first partitioned by the
-// top 8 bits of x with one onesweep pass, so the atomics of concurrently
-// running CTAs hit a few MB of mi64 at a time (L2-resident) instead of the
-// whole array.
-
-// Record i of edge j = i >> 1: endpoint (i & 1), payload (j + 1, other end).
-struct EdgeRecLoader {
-  static constexpr int NS = 1, IPE = 2;
-  __host__ __device__ static constexpr int sb(int) { return 8; }
-  const int2* __restrict__ euv;
-  __device__ __forceinline__ const void* ptr(int) const { return euv; }
-  __device__ __forceinline__ uint32_t key(int64_t i) const {
-    int2 e = __ldg(euv + (i >> 1));
-    return (uint32_t)((i & 1) ? e.y : e.x);
-  }
-  __device__ __forceinline__ void load(int64_t i, uint32_t& k, Vals<2>& p) const {
-    int2 e = __ldg(euv + (i >> 1));
-    const bool second = i & 1;
-    k = (uint32_t)(second ? e.y : e.x);
-    p.w[0] = (uint32_t)(i >> 1) + 1u;
-    p.w[1] = (uint32_t)(second ? e.x : e.y);
-  }
-  __device__ __forceinline__ void get(char* const* st, int li, int64_t i, uint32_t& k, Vals<2>& p) const {
-    int2 e = reinterpret_cast<const int2*>(st[0])[li >> 1];
-    const bool second = i & 1;
-    k = (uint32_t)(second ? e.y : e.x);
-    p.w[0] = (uint32_t)(i >> 1) + 1u;
-    p.w[1] = (uint32_t)(second ? e.x : e.y);
-  }
-};
-
-// Materialised records (levels >= 1): SoA (vertex, j + 1, other).
-using RecLoader = ArrayLoader<uint32_t, 2>;
+// an isolated vertex.  Large views group their records by vertex bucket
+// first (bucket.cuh); small views scatter-max directly (L2-resident).
 
 __device__ __forceinline__ unsigned long long pack_mi(uint32_t j1, uint32_t other) {
   return ((unsigned long long)j1 << 32) | other;
-}
-
-// Apply partitioned records in order (a grid-stride sweep keeps the active
-// window to ~1-2 vertex buckets).
-__global__ void __launch_bounds__(256) k_mi_apply(const uint32_t* __restrict__ vtx,
-                                                  const uint32_t* __restrict__ j1,
-                                                  const uint32_t* __restrict__ oth, int64_t m,
-                                                  unsigned long long* __restrict__ mi64) {
-  constexpr int U = 4;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
-  for (int64_t b = (int64_t)blockIdx.x * blockDim.x * U + threadIdx.x; b < m; b += stride) {
-    uint32_t x[U], a[U], o[U];
-#pragma unroll
-    for (int q = 0; q < U; ++q) {
-      int64_t i = b + (int64_t)q * blockDim.x;
-      if (i < m) {
-        x[q] = ld_stream(vtx + i);
-        a[q] = ld_stream(j1 + i);
-        o[q] = ld_stream(oth + i);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < U; ++q) {
-      int64_t i = b + (int64_t)q * blockDim.x;
-      if (i < m) atomicMax(mi64 + x[q], pack_mi(a[q], o[q]));
-    }
-  }
-}
-
-// Direct (unpartitioned) scatter-max, for views small enough to sit in L2.
-__global__ void k_mi_direct(const int2* __restrict__ euv, int64_t n, unsigned long long* __restrict__ mi64) {
-  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < n) {
-    int2 e = euv[j];
-    atomicMax(mi64 + e.x, pack_mi((uint32_t)j + 1u, (uint32_t)e.y));
-    atomicMax(mi64 + e.y, pack_mi((uint32_t)j + 1u, (uint32_t)e.x));
-  }
 }
 
 // --------------------------------------------- 3. contraction (per view)
@@ -551,7 +483,7 @@ k_walk(int64_t n, const int8_t* __restrict__ ret, const int2* __restrict__ euv,
 }
 
 struct Sort2FirstLoader {
-  static constexpr int NS = 1, IPE = 1;
+  static constexpr int NS = 1;
   __host__ __device__ static constexpr int sb(int) { return 4; }
   const uint32_t* __restrict__ keys;
   __device__ __forceinline__ const void* ptr(int) const { return keys; }

@@ -82,46 +82,77 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
 // ------------------------------------------------------------- loaders
-// A Loader has NS input streams; stream s holds elements of sb(s) bytes and
-// item i of the sort uses element i / IPE of every stream.  It provides
+// A Loader has NS input streams; stream s holds sb(s) bytes per item.  It
+// provides
 //   ptr(s)                      stream base pointer
 //   key(i)                      key of item i from global memory (upsweep)
 //   load(i, k, v)               item i from global memory (partial tiles)
 //   get(stage, li, i, k, v)     item i (local index li) from staged streams
-template <typename K, int VW>
+//
+// Between passes an item is a key array (K) plus an AoS payload array of PW
+// 32-bit words per item: a digit run of m items is then one contiguous run
+// of m * 4 * PW payload bytes instead of PW runs of 4 m bytes, which keeps
+// the scattered writes of uniformly distributed digits sector-efficient.
+template <typename K, int PW>
 struct ArrayLoader {
-  static constexpr int NS = 1 + VW, IPE = 1;
-  __host__ __device__ static constexpr int sb(int s) { return s == 0 ? (int)sizeof(K) : 4; }
+  static constexpr int NS = 2;
+  __host__ __device__ static constexpr int sb(int s) { return s == 0 ? (int)sizeof(K) : 4 * PW; }
   const K* __restrict__ keys;
-  const uint32_t* __restrict__ vals[VW];
-  __device__ __forceinline__ const void* ptr(int s) const { return s == 0 ? (const void*)keys : (const void*)vals[s - 1]; }
+  const uint32_t* __restrict__ pay;
+  __device__ __forceinline__ const void* ptr(int s) const { return s == 0 ? (const void*)keys : (const void*)pay; }
   __device__ __forceinline__ K key(int64_t i) const { return ld_stream(keys + i); }
-  __device__ __forceinline__ void load(int64_t i, K& k, Vals<VW>& v) const {
+  __device__ __forceinline__ void load(int64_t i, K& k, Vals<PW>& v) const {
     k = ld_stream(keys + i);
 #pragma unroll
-    for (int q = 0; q < VW; ++q) v.w[q] = ld_stream(vals[q] + i);
+    for (int q = 0; q < PW; ++q) v.w[q] = ld_stream(pay + i * PW + q);
   }
-  __device__ __forceinline__ void get(char* const* st, int li, int64_t, K& k, Vals<VW>& v) const {
+  __device__ __forceinline__ void get(char* const* st, int li, int64_t, K& k, Vals<PW>& v) const {
     k = reinterpret_cast<const K*>(st[0])[li];
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(st[1]) + li * PW;
+    if constexpr (PW == 2) {
+      const uint2 x = *reinterpret_cast<const uint2*>(p);
+      v.w[0] = x.x;
+      v.w[1] = x.y;
+    } else {
 #pragma unroll
-    for (int q = 0; q < VW; ++q) v.w[q] = reinterpret_cast<const uint32_t*>(st[1 + q])[li];
+      for (int q = 0; q < PW; ++q) v.w[q] = p[q];
+    }
   }
 };
 
-template <typename K, int VW>
+// A sorted sub-tile in shared memory: item s (0 <= s < cnt) has key
+// skeys[s], payload words spay[s * PW ..], and goes to global index
+// gofs[digit] + s.  Emitters write it out with coalesced per-digit runs.
+template <typename K, int PW, int BITS>
+struct TileView {
+  const K* skeys;
+  const uint32_t* spay;
+  const uint32_t* gofs;
+  int cnt;
+  int shift;
+  __device__ __forceinline__ uint32_t digit(int s) const { return digit_of<BITS>(skeys[s], shift); }
+  __device__ __forceinline__ uint32_t dst(int s) const { return gofs[digit(s)] + (uint32_t)s; }
+};
+
+template <typename K, int PW>
 struct ArrayEmitter {
   K* __restrict__ keys;
-  uint32_t* __restrict__ vals[VW];
-  template <int N>
-  __device__ __forceinline__ void emit(const uint32_t (&dst)[N], const K (&k)[N], const Vals<VW> (&v)[N],
-                                       const bool (&ok)[N]) const {
-#pragma unroll
-    for (int i = 0; i < N; ++i)
-      if (ok[i]) {
-        keys[dst[i]] = k[i];
-#pragma unroll
-        for (int q = 0; q < VW; ++q) vals[q][dst[i]] = v[i].w[q];
+  uint32_t* __restrict__ pay;
+  template <int BLOCK, class Tile>
+  __device__ __forceinline__ void emit(const Tile& t) const {
+    for (int s = threadIdx.x; s < t.cnt; s += BLOCK) {
+      const uint32_t d = t.dst(s);
+      keys[d] = t.skeys[s];
+      if constexpr (PW == 1) pay[d] = t.spay[s];
+    }
+    if constexpr (PW > 1) {
+      // payload as one word stream: word s of the sorted tile goes to
+      // global word gofs[digit] * PW + s (consecutive threads -> consecutive words)
+      for (int s = threadIdx.x; s < t.cnt * PW; s += BLOCK) {
+        const int it = s / PW;
+        pay[(uint64_t)t.gofs[t.digit(it)] * PW + s] = t.spay[s];
       }
+    }
   }
 };
 
@@ -141,14 +172,7 @@ struct SweepArgs {
   uint32_t G;             // number of chunks (= CTAs)
   uint32_t GS;            // row stride of counts (G rounded up to a multiple of 4)
   uint32_t* counts;       // [256][GS] digit-major (upsweep out, scan in/out)
-  unsigned long long* prof;  // optional: per-CTA phase time sums [G][8] (tools/sortbench)
 };
-
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 
 constexpr int kMaxChunks = 148 * 4;  // downsweep CTAs (chunks) per pass, upper bound
 constexpr int kUpSplit = 4;  // upsweep CTAs per chunk (counts accumulate atomically)
@@ -237,26 +261,26 @@ __global__ void __launch_bounds__(256) k_chunk_scan(uint32_t* counts, uint32_t G
 }
 
 // ------------------------------------------------------------- downsweep
-template <typename K, int VW, int BLOCK, int ITEMS, class Loader, int BITS = kRadixBits>
+template <typename K, int PW, int BLOCK, int ITEMS, class Loader, int BITS = kRadixBits>
 struct DownSmem {
   static constexpr int R = 1 << BITS;
   static constexpr int T = BLOCK * ITEMS;
   static constexpr int NW = BLOCK / 32;
   static constexpr int NS = Loader::NS;
   __host__ __device__ static constexpr size_t stream_bytes(int s) {
-    return ((size_t)T / Loader::IPE * Loader::sb(s) + 127) & ~size_t(127);
+    return ((size_t)T * Loader::sb(s) + 127) & ~size_t(127);
   }
   __host__ __device__ static constexpr size_t stream_off(int s) {
     size_t b = 0;
     for (int q = 0; q < s; ++q) b += stream_bytes(q);
     return b;
   }
-  // sorted sub-tile (keys, then VW value rows) is scattered in place into the
-  // stage buffer it was read from, so a buffer holds max(staged, sorted).
+  // sorted sub-tile (keys, then the AoS payload) is scattered in place into
+  // the stage buffer it was read from, so a buffer holds max(staged, sorted).
   __host__ __device__ static constexpr size_t keys_bytes() { return ((size_t)T * sizeof(K) + 127) & ~size_t(127); }
   __host__ __device__ static constexpr size_t stage_bytes() {
     const size_t staged = stream_off(NS);
-    const size_t sorted = keys_bytes() + (size_t)VW * T * 4;
+    const size_t sorted = keys_bytes() + (size_t)PW * T * 4;
     return staged > sorted ? staged : sorted;
   }
   __host__ __device__ static constexpr size_t off_stage(int st) { return st * stage_bytes(); }
@@ -275,13 +299,13 @@ struct DownSmem {
 // Stable rank of item i within its warp's items of equal digit.  Peers by
 // __match_any_sync (DMST_RANK_BALLOT selects 8 ballots instead); all peers
 // read the warp counter (broadcast), the lowest peer advances it.
-template <bool FULL>
+template <bool FULL, int BITS>
 __device__ __forceinline__ uint32_t warp_rank(uint32_t* whist, uint32_t d, bool valid, uint32_t lane,
                                               uint32_t lt) {
 #ifdef DMST_RANK_BALLOT
   uint32_t peers = FULL ? kFull : (valid ? __ballot_sync(kFull, valid) : ~__ballot_sync(kFull, valid));
 #pragma unroll
-  for (int b = 0; b < kRadixBits; ++b) {
+  for (int b = 0; b < BITS; ++b) {
     const uint32_t bit = (d >> b) & 1u;
     peers &= __ballot_sync(kFull, bit) ^ (bit - 1u);
   }
@@ -298,12 +322,13 @@ __device__ __forceinline__ uint32_t warp_rank(uint32_t* whist, uint32_t d, bool 
 }
 
 // Rank, scatter (in place, into stage buffer `buf`) and write out one sub-tile.
-template <bool FULL, typename K, int VW, int BLOCK, int ITEMS, class S, class Emitter>
+template <bool FULL, typename K, int PW, int BLOCK, int ITEMS, int BITS, class S, class Emitter>
 __device__ __forceinline__ void down_subtile(const SweepArgs& a, const Emitter& em, typename S::Misc& m,
-                                             unsigned char* buf, K (&k)[ITEMS], Vals<VW> (&v)[ITEMS],
+                                             unsigned char* buf, K (&k)[ITEMS], Vals<PW> (&v)[ITEMS],
                                              int cnt_items) {
-  constexpr int T = S::T, NW = S::NW, R = S::R, BPT = R / BLOCK;
-  constexpr int BITS = R == 256 ? 8 : R == 512 ? 9 : 10;
+  constexpr int T = S::T, NW = S::NW, R = S::R;
+  constexpr int BPT = R >= BLOCK ? R / BLOCK : 1;  // digits owned per thread
+  constexpr int OWNERS = R / BPT;                  // threads owning digits
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t lt = lanemask_lt();
   const int lbase = warp * ITEMS * 32 + lane;
@@ -311,78 +336,77 @@ __device__ __forceinline__ void down_subtile(const SweepArgs& a, const Emitter& 
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const bool valid = FULL || lbase + i * 32 < cnt_items;
-    rk[i] = warp_rank<FULL>(m.whist[warp], digit_of<BITS>(k[i], a.shift), valid, lane, lt);
+    rk[i] = warp_rank<FULL, BITS>(m.whist[warp], digit_of<BITS>(k[i], a.shift), valid, lane, lt);
   }
   __syncthreads();  // (also: every thread has finished reading `buf`)
 
-  // thread t owns digits t*BPT .. t*BPT+BPT-1 (consecutive, for the block scan)
+  // thread t < OWNERS owns digits t*BPT .. t*BPT+BPT-1 (consecutive, for the block scan)
+  const bool owner = (int)tid < OWNERS;
   uint32_t cb[BPT], csum = 0;
 #pragma unroll
   for (int q = 0; q < BPT; ++q) {
-    const uint32_t b = tid * BPT + q;
-    uint32_t c = 0;
+    cb[q] = 0;
+    if (owner) {
+      const uint32_t b = tid * BPT + q;
+      uint32_t c = 0;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      const uint32_t x = m.whist[w][b];
-      m.whist[w][b] = c;
-      c += x;
+      for (int w = 0; w < NW; ++w) {
+        const uint32_t x = m.whist[w][b];
+        m.whist[w][b] = c;
+        c += x;
+      }
+      cb[q] = c;
+      csum += c;
     }
-    cb[q] = c;
-    csum += c;
   }
   uint32_t total;
   uint32_t lstart = block_excl_sum<BLOCK>(csum, m.scan, &total);
+  if (owner) {
 #pragma unroll
-  for (int q = 0; q < BPT; ++q) {
-    const uint32_t b = tid * BPT + q;
-    m.lstart[b] = lstart;
-    m.gofs[b] = m.run[b] - lstart;
-    m.run[b] += cb[q];
-    lstart += cb[q];
+    for (int q = 0; q < BPT; ++q) {
+      const uint32_t b = tid * BPT + q;
+      m.lstart[b] = lstart;
+      m.gofs[b] = m.run[b] - lstart;
+      m.run[b] += cb[q];
+      lstart += cb[q];
+    }
   }
   __syncthreads();
 
   K* skeys = reinterpret_cast<K*>(buf);
-  uint32_t* svals = reinterpret_cast<uint32_t*>(buf + S::keys_bytes());
+  uint32_t* spay = reinterpret_cast<uint32_t*>(buf + S::keys_bytes());
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     if (FULL || lbase + i * 32 < cnt_items) {
       const uint32_t d = digit_of<BITS>(k[i], a.shift);
       const uint32_t pos = m.lstart[d] + m.whist[warp][d] + rk[i];
       skeys[pos] = k[i];
+      if constexpr (PW == 2) {
+        *reinterpret_cast<uint2*>(spay + pos * 2) = make_uint2(v[i].w[0], v[i].w[1]);
+      } else {
 #pragma unroll
-      for (int q = 0; q < VW; ++q) svals[q * T + pos] = v[i].w[q];
+        for (int q = 0; q < PW; ++q) spay[pos * PW + q] = v[i].w[q];
+      }
     }
   }
   __syncthreads();
-
-  uint32_t dst[ITEMS];
-  bool ok[ITEMS];
+  if (owner) {
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i) {
-    const int sidx = i * BLOCK + tid;
-    ok[i] = FULL || sidx < cnt_items;
-    if (ok[i]) {
-      k[i] = skeys[sidx];
+    for (int w = 0; w < NW; ++w)
 #pragma unroll
-      for (int q = 0; q < VW; ++q) v[i].w[q] = svals[q * T + sidx];
-      dst[i] = m.gofs[digit_of<BITS>(k[i], a.shift)] + sidx;
-    }
+      for (int q = 0; q < BPT; ++q) m.whist[w][tid * BPT + q] = 0;
   }
-#pragma unroll
-  for (int w = 0; w < NW; ++w)
-#pragma unroll
-    for (int q = 0; q < BPT; ++q) m.whist[w][tid * BPT + q] = 0;
-  em.template emit<ITEMS>(dst, k, v, ok);
+  TileView<K, PW, BITS> t{skeys, spay, m.gofs, FULL ? T : cnt_items, a.shift};
+  em.template emit<BLOCK>(t);
   __syncthreads();
 }
 
-template <typename K, int VW, int BLOCK, int ITEMS, int MINB, class Loader, class Emitter, int BITS = kRadixBits>
+template <typename K, int PW, int BLOCK, int ITEMS, int MINB, class Loader, class Emitter, int BITS = kRadixBits>
 __global__ void __launch_bounds__(BLOCK, MINB)
 k_downsweep(SweepArgs a, Loader ld, Emitter em) {
-  static_assert(BLOCK == 256 && (1 << BITS) % BLOCK == 0, "digit bins are owned by threads");
-  using S = DownSmem<K, VW, BLOCK, ITEMS, Loader, BITS>;
-  constexpr int T = S::T, NW = S::NW, NS = S::NS, BPT = S::R / BLOCK;
+  static_assert(BLOCK % 32 == 0 && ((1 << BITS) % BLOCK == 0 || BLOCK % (1 << BITS) == 0), "digit ownership");
+  using S = DownSmem<K, PW, BLOCK, ITEMS, Loader, BITS>;
+  constexpr int T = S::T, NW = S::NW, NS = S::NS, R = S::R;
   extern __shared__ __align__(128) unsigned char smem[];
   typename S::Misc& m = *reinterpret_cast<typename S::Misc*>(smem + S::off_misc());
 
@@ -393,9 +417,7 @@ k_downsweep(SweepArgs a, Loader ld, Emitter em) {
   const int nsub = (int)((end - begin + T - 1) / T);
   const bool tma = loader_tma_ok(ld);
 
-#pragma unroll
-  for (int q = 0; q < BPT; ++q) {
-    const uint32_t b = tid * BPT + q;
+  for (int b = tid; b < R; b += BLOCK) {
     m.run[b] = a.counts[(uint64_t)b * a.GS + blockIdx.x];
 #pragma unroll
     for (int w = 0; w < NW; ++w) m.whist[w][b] = 0;
@@ -414,14 +436,13 @@ k_downsweep(SweepArgs a, Loader ld, Emitter em) {
     fence_proxy_async();
     uint32_t bytes = 0;
 #pragma unroll
-    for (int s = 0; s < NS; ++s) bytes += (uint32_t)(T / Loader::IPE * Loader::sb(s));
+    for (int s = 0; s < NS; ++s) bytes += (uint32_t)(T * Loader::sb(s));
     uint64_t* bar = &m.bar[sub & 1];
     mbar_expect_tx(bar, bytes);
 #pragma unroll
     for (int s = 0; s < NS; ++s)
-      bulk_g2s(smem + S::off_stage(sub & 1) + S::stream_off(s),
-               (const char*)ld.ptr(s) + (i0 / Loader::IPE) * Loader::sb(s),
-               (uint32_t)(T / Loader::IPE * Loader::sb(s)), bar);
+      bulk_g2s(smem + S::off_stage(sub & 1) + S::stream_off(s), (const char*)ld.ptr(s) + i0 * Loader::sb(s),
+               (uint32_t)(T * Loader::sb(s)), bar);
   };
   if (tid == 0) issue(0);
 
@@ -432,7 +453,7 @@ k_downsweep(SweepArgs a, Loader ld, Emitter em) {
     const int cnt_items = rem_items < T ? (int)rem_items : T;
     unsigned char* buf = smem + S::off_stage(sub & 1);
     K k[ITEMS];
-    Vals<VW> v[ITEMS];
+    Vals<PW> v[ITEMS];
     const int lbase = warp * ITEMS * 32 + lane;
     if (tma && cnt_items == T) {
       mbar_wait(&m.bar[sub & 1], (uint32_t)(sub >> 1) & 1u);
@@ -444,7 +465,7 @@ k_downsweep(SweepArgs a, Loader ld, Emitter em) {
         const int li = lbase + i * 32;
         ld.get(st, li, i0 + li, k[i], v[i]);
       }
-      down_subtile<true, K, VW, BLOCK, ITEMS, S>(a, em, m, buf, k, v, T);
+      down_subtile<true, K, PW, BLOCK, ITEMS, BITS, S>(a, em, m, buf, k, v, T);
     } else {
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
@@ -452,27 +473,36 @@ k_downsweep(SweepArgs a, Loader ld, Emitter em) {
         if (li < cnt_items) ld.load(i0 + li, k[i], v[i]);
       }
       if (cnt_items == T)
-        down_subtile<true, K, VW, BLOCK, ITEMS, S>(a, em, m, buf, k, v, T);
+        down_subtile<true, K, PW, BLOCK, ITEMS, BITS, S>(a, em, m, buf, k, v, T);
       else
-        down_subtile<false, K, VW, BLOCK, ITEMS, S>(a, em, m, buf, k, v, cnt_items);
+        down_subtile<false, K, PW, BLOCK, ITEMS, BITS, S>(a, em, m, buf, k, v, cnt_items);
     }
   }
 }
 
-// Every digit was constant: the stable order is the identity.
-template <typename K, int VW, class Loader, class Emitter>
-__global__ void k_identity_pass(int64_t n, Loader ld, Emitter em) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t dst[1];
-  K k[1];
-  Vals<VW> v[1];
-  bool ok[1];
-  ok[0] = i < n;
-  if (ok[0]) {
-    ld.load(i, k[0], v[0]);
-    dst[0] = (uint32_t)i;
+// Every digit was constant: the stable order is the identity.  Items go
+// through a shared-memory tile with gofs = tile base, so emitters see the
+// same interface as in a sort pass.
+template <typename K, int PW, int BLOCK, class Loader, class Emitter>
+__global__ void __launch_bounds__(BLOCK) k_identity_pass(int64_t n, Loader ld, Emitter em) {
+  __shared__ K skeys[BLOCK];
+  __shared__ uint32_t spay[BLOCK * PW];
+  __shared__ uint32_t gofs[kRadix];
+  const int64_t i0 = (int64_t)blockIdx.x * BLOCK;
+  const int64_t i = i0 + threadIdx.x;
+  const int cnt = n - i0 < BLOCK ? (int)(n - i0) : BLOCK;
+  if (i < n) {
+    K k;
+    Vals<PW> v;
+    ld.load(i, k, v);
+    skeys[threadIdx.x] = k;
+#pragma unroll
+    for (int q = 0; q < PW; ++q) spay[threadIdx.x * PW + q] = v.w[q];
   }
-  em.template emit<1>(dst, k, v, ok);
+  for (int b = threadIdx.x; b < kRadix; b += BLOCK) gofs[b] = (uint32_t)i0;
+  __syncthreads();
+  TileView<K, PW, kRadixBits> t{skeys, spay, gofs, cnt, 0};
+  em.template emit<BLOCK>(t);
 }
 
 // Exclusive scan of per-digit global histograms: hist[p][256] -> gbase[p][256].

@@ -95,7 +95,7 @@ struct Workspace {
   int32_t* grank[2];
   int32_t* vm_all;        // vertex maps of views 0..L-1
   int32_t* smi_all;       // maxIncident (global ranks) of views 1..L
-  int2* lvl_all;          // walk table: (vertex_map, maxIncident) of views 1..L
+  int32_t* x1;            // view-1 supervertex of every edge (walk start)
   uint32_t* sel_status;   // select/leafscan look-back words
   size_t bytes;
 };
@@ -134,7 +134,7 @@ Workspace carve(int64_t n, int64_t nv, char* base) {
   }
   w.vm_all = (int32_t*)take(4 * (2 * nv + DMST_MAX_LEVELS + 2));
   w.smi_all = (int32_t*)take(4 * (nv + DMST_MAX_LEVELS + 2));
-  w.lvl_all = (int2*)take(8 * (nv + DMST_MAX_LEVELS + 2));
+  w.x1 = (int32_t*)take(4 * (n + 2));
   w.sel_status = (uint32_t*)take(4 * (cdiv(std::max(nv, n), SEL_TILE) + 2));
   w.bytes = off + 256;
   return w;
@@ -463,6 +463,7 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     es.rec_vtx = rec;
     es.rec_j1 = rec + 2 * n_next;
     es.rec_oth = rec + 4 * n_next;
+    es.x1 = level == 0 ? w.x1 : nullptr;
     es.level = (int8_t)level;
     {
       const int64_t tiles = cdiv(n_k, SEL_TILE);
@@ -504,13 +505,8 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
   uint32_t* keys = (uint32_t*)w.R;
   const uint32_t kinit[2] = {~0u, 0u};
   DMST_CUDA(cudaMemcpyAsync(key_ao, kinit, 8, cudaMemcpyHostToDevice, c.s));
-  if (soff > 0) {
-    c.begin(KK_OTHER);
-    k_pack_levels<<<grid_for(soff, EW_BLOCK), EW_BLOCK, 0, c.s>>>(soff, w.vm_all, w.smi_all, lt, w.lvl_all);
-    c.launched();
-  }
   c.begin(KK_WALK);
-  k_walk<256><<<c.persistent_grid(n, 256, 8), 256, 0, c.s>>>(n, w.ret, w.euv0, w.vm_all, w.lvl_all, lt, keys,
+  k_walk<256><<<c.persistent_grid(n, 256, 8), 256, 0, c.s>>>(n, w.ret, w.x1, w.vm_all, w.smi_all, lt, keys,
                                                               key_ao);
   c.launched();
   if (dbg_ret) DMST_CUDA(cudaMemcpyAsync(dbg_ret, w.ret, n, cudaMemcpyDeviceToDevice, c.s));

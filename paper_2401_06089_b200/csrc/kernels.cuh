@@ -378,6 +378,7 @@ struct EdgeSel {
   uint32_t* __restrict__ rec_vtx;
   uint32_t* __restrict__ rec_j1;
   uint32_t* __restrict__ rec_oth;
+  int32_t* __restrict__ x1;          // view 0 only: view-1 supervertex of every edge (walk start)
   int8_t level;
   struct Item {
     int32_t g;
@@ -392,11 +393,17 @@ struct EdgeSel {
   }
   __device__ __forceinline__ void emit(int64_t j, bool alpha, uint32_t pos, const Item& it, Shared&) const {
     if ((j & 15) == 0) cnt2[j >> 4] = 0u;
+    int2 e = make_int2(0, 0);
+    int32_t a = 0;
+    if (alpha || x1) {
+      e = __ldcs(euv + j);
+      a = vm[e.x];
+    }
+    if (x1) __stcs(x1 + j, a);
     if (!alpha) {
       ret[it.g] = level;
     } else {
-      const int2 e = __ldcs(euv + j);
-      const int32_t a = vm[e.x], b = vm[e.y];
+      const int32_t b = vm[e.y];
       __stcs(euv_next + pos, make_int2(a, b));
       __stcs(grank_next + pos, it.g);
       if (mi64_next) {
@@ -432,23 +439,14 @@ struct LevelTable {
 // 0 <= p < e wins.  The chain (terminal, anchor) is encoded as the dense key
 // 1 + soff[k] + anchor (a terminal edge is a terminal only at the one level
 // it retires at, so (level, anchor) identifies the chain); 0 = root chain.
-// Walk table of views 1..L: lvl[soff[k] + x] = (vertex_map_k[x] (-1 for the
-// final view), maxIncident_k[x]) so each level of the walk is one 8-B hop.
-__global__ void k_pack_levels(int64_t total, const int32_t* __restrict__ vm_all,
-                              const int32_t* __restrict__ smi_all, const __grid_constant__ LevelTable lt,
-                              int2* __restrict__ lvl) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= total) return;
-  int k = 1;
-  while (k < lt.L && i >= lt.soff[k + 1]) ++k;
-  const int32_t next = k < lt.L ? vm_all[lt.voff[k] + (i - lt.soff[k])] : -1;
-  __stcs(lvl + i, make_int2(next, smi_all[i]));
-}
-
+// The walk starts at the edge's view-1 supervertex x1[e] (written by the
+// view-0 select); per level it reads smi_k[x] (maxIncident of view k, global
+// ranks) and, on a miss, vm_k[x] (view k -> k + 1), so the dominant first
+// check touches a 4-B table of nv_1 entries.
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK)
-k_walk(int64_t n, const int8_t* __restrict__ ret, const int2* __restrict__ euv,
-       const int32_t* __restrict__ vm0, const int2* __restrict__ lvl,
+k_walk(int64_t n, const int8_t* __restrict__ ret, const int32_t* __restrict__ x1,
+       const int32_t* __restrict__ vm_all, const int32_t* __restrict__ smi_all,
        const __grid_constant__ LevelTable lt, uint32_t* __restrict__ keys,
        uint32_t* __restrict__ and_or) {
   uint32_t ka = ~0u, ko = 0u;
@@ -459,14 +457,17 @@ k_walk(int64_t n, const int8_t* __restrict__ ret, const int2* __restrict__ euv,
       uint32_t key = 0;
       const int r = __ldcs(ret + e);
       if (r < lt.L) {
-        int32_t x = vm0[__ldcs(euv + e).x];  // view-1 supervertex
-        for (int k = 1; k <= lt.L; ++k) {
-          const int2 t = lvl[lt.soff[k] + x];
-          if (k > r && t.y >= 0 && t.y < (int32_t)e) {
-            key = (uint32_t)(1 + lt.soff[k] + x);
-            break;
+        int32_t x = __ldcs(x1 + e);  // view-1 supervertex
+        for (int k = 1;; ++k) {
+          if (k > r) {
+            const int32_t p = smi_all[lt.soff[k] + x];
+            if (p >= 0 && p < (int32_t)e) {
+              key = (uint32_t)(1 + lt.soff[k] + x);
+              break;
+            }
           }
-          x = t.x;
+          if (k >= lt.L) break;
+          x = vm_all[lt.voff[k] + x];
         }
       }
       __stcs(keys + e, key);

@@ -22,10 +22,11 @@
  *   Device dtypes are int32 ids/ranks and float64 weights; the Python
  *   wrapper widens to the reference's int64.
  *
- * Every pointer except `level_counts`, `num_levels` and `stats` is a DEVICE
- * pointer.  The caller allocates every device buffer, including the
- * workspace (size from dmst_workspace_bytes); the library never allocates,
- * frees, or keeps state between calls.  Inputs are read-only.  Work is
+ * Every pointer except `stats` is a DEVICE pointer (dmst_build_host takes
+ * HOST buffers instead).  The caller allocates every device buffer, including
+ * the workspace (size from dmst_workspace_bytes); the library never allocates
+ * device memory and keeps no data between calls (it caches CUDA events, and
+ * for dmst_build_host one side stream, per host thread).  Inputs are read-only.  Work is
  * enqueued on `stream`; the call returns after the stream has drained
  * (the contraction level loop sizes each level from device counts).
  * Calls on different streams with different workspaces may run
@@ -36,7 +37,7 @@
  * (thread-local).  The input must already be a valid spanning tree
  * (validation is the caller's, tree_core.py:110-139, as in the reference,
  * whose `pandora` raises nothing itself — SPEC.md:265).
- * Limits: 1 <= n_edges < 2^30, n_vertices == n_edges + 1.
+ * Limits: 1 <= n_edges < 2^29, n_vertices == n_edges + 1.
  */
 #ifndef DMST_H
 #define DMST_H
@@ -79,6 +80,24 @@ int dmst_build(const int32_t* u, const int32_t* v, const double* w, int64_t n_ed
                int64_t n_vertices, int32_t* orig_of, double* heights, int32_t* edge_parent,
                int32_t* vertex_parent, dmst_stats* stats, void* workspace,
                size_t workspace_bytes, void* stream);
+
+/* Device workspace for dmst_build_host (pipeline workspace + device copies
+ * of the inputs and outputs). */
+size_t dmst_host_workspace_bytes(int64_t n_edges, int64_t n_vertices);
+
+/* dmst_build with HOST buffers: u, v, w, orig_of, heights, edge_parent and
+ * vertex_parent are host pointers (page-locked memory gives asynchronous,
+ * overlapped copies; pageable memory works but serialises).  The inputs are
+ * copied in on a per-thread side stream; each output is copied out as soon
+ * as the stage producing it completes (orig_of/heights after the edge sort,
+ * vertex_parent after maxIncident, edge_parent at the end), overlapping the
+ * copies with the remaining kernels.  Returns when every copy has landed.
+ * This is the call a host-side binding of the reference's `dendromst build`
+ * path (cli.py:82-85: rank_edges + pandora on numpy arrays) makes. */
+int dmst_build_host(const int32_t* u, const int32_t* v, const double* w, int64_t n_edges,
+                    int64_t n_vertices, int32_t* orig_of, double* heights, int32_t* edge_parent,
+                    int32_t* vertex_parent, dmst_stats* stats, void* workspace,
+                    size_t workspace_bytes, void* stream);
 
 /* rank_edges only: orig_of, heights and rank-order endpoints ru/rv. */
 int dmst_rank_edges(const int32_t* u, const int32_t* v, const double* w, int64_t n_edges,

@@ -5,9 +5,9 @@ vertex_parent) + merge heights, bit-identical to the reference
 `dendromst` package, on hand-written sm_100a CUDA kernels behind a C ABI
 (include/dmst.h).  See DESIGN.md.
 """
-from .api import (ROOT, BuildResult, Dendrogram, DendrogramBuilder, RankedTree,
+from .api import (ROOT, BuildResult, Dendrogram, DendrogramBuilder, HostBuildResult, RankedTree,
                   build_b200, pandora_b200, rank_edges_b200, register_algorithm)
 
-__all__ = ["ROOT", "BuildResult", "Dendrogram", "DendrogramBuilder", "RankedTree",
+__all__ = ["ROOT", "BuildResult", "Dendrogram", "DendrogramBuilder", "HostBuildResult", "RankedTree",
            "build_b200", "pandora_b200", "rank_edges_b200", "register_algorithm"]
 __version__ = "0.1.0"

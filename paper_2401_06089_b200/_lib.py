@@ -21,7 +21,9 @@ DMST_MAX_KERNELS = 16
 # every symbol include/dmst.h declares
 EXPORTS = (
     "dmst_workspace_bytes",
+    "dmst_host_workspace_bytes",
     "dmst_build",
+    "dmst_build_host",
     "dmst_rank_edges",
     "dmst_pandora",
     "dmst_build_debug",
@@ -82,6 +84,11 @@ def load() -> ctypes.CDLL:
     lib.dmst_build.argtypes = [vp, vp, vp, i64, i64, vp, vp, vp, vp,
                                ctypes.POINTER(DmstStats), vp, sz, vp]
     lib.dmst_build.restype = ctypes.c_int
+    lib.dmst_host_workspace_bytes.argtypes = [i64, i64]
+    lib.dmst_host_workspace_bytes.restype = sz
+    lib.dmst_build_host.argtypes = [vp, vp, vp, i64, i64, vp, vp, vp, vp,
+                                    ctypes.POINTER(DmstStats), vp, sz, vp]
+    lib.dmst_build_host.restype = ctypes.c_int
     lib.dmst_build_debug.argtypes = [vp, vp, vp, i64, i64, vp, vp, vp, vp,
                                      ctypes.POINTER(DmstStats), vp, vp, vp, vp, vp, sz, vp]
     lib.dmst_build_debug.restype = ctypes.c_int

@@ -106,6 +106,35 @@ class BuildResult:
                           self.vertex_parent.cpu().numpy().astype(np.int64))
 
 
+@dataclass
+class HostBuildResult:
+    """Host-resident outputs of :meth:`DendrogramBuilder.build_host`."""
+    orig_of: torch.Tensor        # int32[n]   (CPU)
+    heights: torch.Tensor        # float64[n]
+    edge_parent: torch.Tensor    # int32[n]
+    vertex_parent: torch.Tensor  # int32[nv]
+    stats: _lib.DmstStats = field(repr=False, default=None)
+
+    @classmethod
+    def empty(cls, n: int, nv: int, pin: bool = True) -> "HostBuildResult":
+        def mk(k, dt):
+            t = torch.empty(k, dtype=dt)
+            return t.pin_memory() if pin else t
+        return cls(mk(n, torch.int32), mk(n, torch.float64), mk(n, torch.int32), mk(nv, torch.int32))
+
+    def dendrogram(self) -> Dendrogram:
+        return Dendrogram(self.edge_parent.numpy().astype(np.int64), self.vertex_parent.numpy().astype(np.int64))
+
+
+def _as_host(x, dtype: torch.dtype) -> torch.Tensor:
+    t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
+    if t.device.type != "cpu":
+        raise ValueError("build_host takes host (CPU) arrays")
+    if t.dtype != dtype:
+        t = t.to(dtype)
+    return t.contiguous()
+
+
 def _ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
 
@@ -151,6 +180,42 @@ class DendrogramBuilder:
             self._ws = None
             self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
         return self._ws
+
+    def host_workspace(self, n: int, nv: int) -> torch.Tensor:
+        need = int(self.lib.dmst_host_workspace_bytes(n, nv))
+        if need == 0:
+            raise ValueError(f"bad sizes n={n} nv={nv}")
+        if getattr(self, "_hws", None) is None or self._hws.numel() < need:
+            self._hws = None
+            self._hws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        return self._hws
+
+    def build_host(self, num_vertices: int, u, v, w, *, out: HostBuildResult | None = None,
+                   profile: bool = False) -> HostBuildResult:
+        """rank_edges + pandora on HOST arrays (dmst_build_host): inputs are
+        copied in and every output copied back as soon as its stage is done,
+        overlapped with the remaining kernels.  Page-locked (pinned) inputs
+        and outputs make the copies asynchronous; ``out`` defaults to pinned
+        buffers.  Returns after the results have landed in host memory."""
+        dev = self.device
+        u = _as_host(u, torch.int32)
+        v = _as_host(v, torch.int32)
+        w = _as_host(w, torch.float64)
+        n, nv = int(u.shape[0]), int(num_vertices)
+        if v.shape[0] != n or w.shape[0] != n:
+            raise ValueError("edge arrays have mismatched lengths")
+        if out is None:
+            out = HostBuildResult.empty(n, nv)
+        with torch.cuda.device(dev):
+            ws = self.host_workspace(n, nv) if n >= 1 and nv >= 2 else torch.empty(1, dtype=torch.uint8, device=dev)
+            st = _lib.DmstStats()
+            st.profile = 1 if profile else 0
+            _lib.check(self.lib.dmst_build_host(
+                _ptr(u), _ptr(v), _ptr(w), n, nv, _ptr(out.orig_of), _ptr(out.heights),
+                _ptr(out.edge_parent), _ptr(out.vertex_parent), ctypes.byref(st),
+                _ptr(ws), ws.numel(), self._stream()))
+        out.stats = st
+        return out
 
     def _stream(self) -> int:
         return torch.cuda.current_stream(self.device).cuda_stream

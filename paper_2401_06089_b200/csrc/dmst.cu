@@ -155,12 +155,69 @@ int num_sms() {
   return sms > 0 ? sms : 148;
 }
 
+// Per-thread host-mapped pinned buffer for small readbacks (Ctx::to_host).
+struct MappedBuf {
+  static constexpr uint32_t kWords = 256;
+  volatile uint32_t* host = nullptr;
+  uint32_t* dev = nullptr;
+  int device = -1;
+};
+MappedBuf& mapped_buf() {
+  thread_local MappedBuf mb;
+  int dev = 0;
+  DMST_CUDA(cudaGetDevice(&dev));
+  if (mb.host == nullptr || mb.device != dev) {
+    void* h = nullptr;
+    DMST_CUDA(cudaHostAlloc(&h, 4 * MappedBuf::kWords, cudaHostAllocMapped | cudaHostAllocPortable));
+    void* d = nullptr;
+    DMST_CUDA(cudaHostGetDevicePointer(&d, h, 0));
+    mb.host = (volatile uint32_t*)h;
+    mb.dev = (uint32_t*)d;
+    mb.device = dev;
+  }
+  return mb;
+}
+
+// Thread-local pool of timing events (profiling creates two per launch).
+std::vector<cudaEvent_t>& event_pool() {
+  thread_local std::vector<cudaEvent_t> pool;
+  return pool;
+}
+cudaEvent_t pooled_event() {
+  auto& p = event_pool();
+  if (!p.empty()) {
+    cudaEvent_t e = p.back();
+    p.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  DMST_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+// Copies between caller host buffers and the device, overlapped with the
+// pipeline on a side stream (dmst_build_host).  Stages signal readiness of
+// their outputs with events; the side stream waits on them and copies out.
+struct HostIO {
+  cudaStream_t side = nullptr;
+  int32_t* h_orig = nullptr;
+  double* h_heights = nullptr;
+  int32_t* h_ep = nullptr;
+  int32_t* h_vp = nullptr;
+  const int32_t* d_orig = nullptr;
+  const double* d_heights = nullptr;
+  const int32_t* d_vp = nullptr;
+  int64_t n = 0, nv = 0;
+  cudaEvent_t ev[4] = {};
+};
+
 struct Ctx {
   cudaStream_t s;
   Workspace w;
   int launches = 0;
   int sms = 148;
   bool profile = false;
+  HostIO* io = nullptr;
   struct Ev {
     int kind;
     cudaEvent_t a, b;
@@ -168,9 +225,7 @@ struct Ctx {
   std::vector<Ev> ev;
   void begin(int kind) {
     if (!profile) return;
-    Ev e{kind, nullptr, nullptr};
-    DMST_CUDA(cudaEventCreate(&e.a));
-    DMST_CUDA(cudaEventCreate(&e.b));
+    Ev e{kind, pooled_event(), pooled_event()};
     DMST_CUDA(cudaEventRecord(e.a, s));
     ev.push_back(e);
   }
@@ -190,16 +245,46 @@ struct Ctx {
     release();
   }
   void release() {
+    auto& p = event_pool();
     for (Ev& e : ev) {
-      cudaEventDestroy(e.a);
-      cudaEventDestroy(e.b);
+      p.push_back(e.a);
+      p.push_back(e.b);
     }
     ev.clear();
   }
   ~Ctx() { release(); }
-  void sync() { DMST_CUDA(cudaStreamSynchronize(s)); }
+  // host copy-out of an output that is complete on `s` (no-op without HostIO)
+  void copy_out(int slot, void* h, const void* d, size_t bytes) {
+    if (!io || !h) return;
+    DMST_CUDA(cudaEventRecord(io->ev[slot], s));
+    DMST_CUDA(cudaStreamWaitEvent(io->side, io->ev[slot], 0));
+    DMST_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, io->side));
+  }
+  // Small device->host reads (level counts, digit masks) go through a
+  // host-mapped pinned buffer written by a tiny kernel, not the copy
+  // engines: dmst_build_host's multi-GB output copies occupy those, and a
+  // queued 8-byte cudaMemcpy would wait behind them.
+  struct Pending {
+    void* h;
+    uint32_t off, bytes;
+  };
+  std::vector<Pending> pend;
+  uint32_t mapped_used = 0;
   void to_host(void* h, const void* d, size_t bytes) {
-    DMST_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s));
+    MappedBuf& mb = mapped_buf();
+    const uint32_t words = (uint32_t)((bytes + 3) / 4);
+    if (mapped_used + words > MappedBuf::kWords) invalid("readback buffer overflow");
+    k_readback<<<1, 32, 0, s>>>(mb.dev + mapped_used, (const uint32_t*)d, words);
+    DMST_CUDA(cudaGetLastError());
+    pend.push_back({h, mapped_used, (uint32_t)bytes});
+    mapped_used += words;
+  }
+  void sync() {
+    DMST_CUDA(cudaStreamSynchronize(s));
+    MappedBuf& mb = mapped_buf();
+    for (const Pending& p : pend) memcpy(p.h, (const void*)(mb.host + p.off), p.bytes);
+    pend.clear();
+    mapped_used = 0;
   }
   void zero(void* d, size_t bytes) { DMST_CUDA(cudaMemsetAsync(d, 0, bytes, s)); }
   unsigned persistent_grid(int64_t work, int block, int per_sm) {
@@ -358,6 +443,7 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
   c.zero(w.cnt2, 4 * (n / 16 + 2));
   mi_buckets(c, EdgeRecSrc{w.euv0}, 2 * n, nv, recs_at(w.R, 2 * n), recs_at(w.R + 24 * n, 2 * n),
              MiApplyOut{w.mi64_0, vertex_parent, nullptr, w.cnt2});
+  if (c.io) c.copy_out(2, c.io->h_vp, vertex_parent, 4 * (size_t)nv);
   bool v1_done = true;
 
   LevelTable lt{};
@@ -563,6 +649,63 @@ void init_ctx(Ctx& c, int64_t n, int64_t nv, void* ws, void* stream, dmst_stats*
   }
 }
 
+static int build_impl(const int32_t* u, const int32_t* v, const double* w, int64_t n, int64_t nv,
+                      int32_t* orig_of, double* heights, int32_t* edge_parent, int32_t* vertex_parent,
+                      dmst_stats* st, int8_t* dbg_ret, int32_t* dbg_key, int32_t* dbg_term,
+                      int32_t* dbg_lvl, void* ws, size_t ws_bytes, void* stream, HostIO* io = nullptr,
+                      cudaEvent_t inputs_ready = nullptr) {
+  return guarded([&] {
+    check_args(n, nv, ws, ws_bytes);
+    if (!u || !v || !w || !orig_of || !heights || !edge_parent || !vertex_parent)
+      invalid("null input/output pointer");
+    Ctx c;
+    init_ctx(c, n, nv, ws, stream, st);
+    c.io = io;
+    if (inputs_ready) DMST_CUDA(cudaStreamWaitEvent(c.s, inputs_ready, 0));
+    Sort1FinalEmitter em{orig_of, heights, c.w.euv0, nullptr, nullptr};
+    int p1 = 0;
+    edge_sort(c, u, v, w, n, em, &p1);
+    if (io) {
+      c.copy_out(0, io->h_orig, orig_of, 4 * (size_t)n);
+      c.copy_out(1, io->h_heights, heights, 8 * (size_t)n);
+    }
+    pandora_core(c, n, nv, vertex_parent, edge_parent, st, dbg_ret, dbg_key, dbg_term, dbg_lvl);
+    if (io) c.copy_out(3, io->h_ep, edge_parent, 4 * (size_t)n);
+    c.sync();
+    if (io) DMST_CUDA(cudaStreamSynchronize(io->side));
+    c.collect(st);
+    if (st) {
+      st->sort1_passes = p1;
+      st->kernel_launches = c.launches;
+    }
+  });
+}
+
+// Device buffers of dmst_build_host behind the pipeline workspace.
+struct HostBufs {
+  int32_t *u, *v, *orig, *ep, *vp;
+  double *w, *heights;
+  size_t bytes;
+};
+HostBufs host_bufs(int64_t n, int64_t nv, char* base) {
+  HostBufs b{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> char* {
+    char* p = base ? base + off : nullptr;
+    off += align_up(bytes);
+    return p;
+  };
+  b.w = (double*)take(8 * n);
+  b.u = (int32_t*)take(4 * n);
+  b.v = (int32_t*)take(4 * n);
+  b.orig = (int32_t*)take(4 * n);
+  b.heights = (double*)take(8 * n);
+  b.ep = (int32_t*)take(4 * n);
+  b.vp = (int32_t*)take(4 * nv);
+  b.bytes = off;
+  return b;
+}
+
 }  // namespace
 }  // namespace dmst
 
@@ -575,27 +718,60 @@ size_t dmst_workspace_bytes(int64_t n_edges, int64_t n_vertices) {
   return carve(n_edges, n_vertices, nullptr).bytes;
 }
 
-static int build_impl(const int32_t* u, const int32_t* v, const double* w, int64_t n, int64_t nv,
-                      int32_t* orig_of, double* heights, int32_t* edge_parent, int32_t* vertex_parent,
-                      dmst_stats* st, int8_t* dbg_ret, int32_t* dbg_key, int32_t* dbg_term,
-                      int32_t* dbg_lvl, void* ws, size_t ws_bytes, void* stream) {
-  return guarded([&] {
-    check_args(n, nv, ws, ws_bytes);
+size_t dmst_host_workspace_bytes(int64_t n_edges, int64_t n_vertices) {
+  if (n_edges < 1 || n_vertices < 2) return 0;
+  return carve(n_edges, n_vertices, nullptr).bytes + host_bufs(n_edges, n_vertices, nullptr).bytes + 256;
+}
+
+int dmst_build_host(const int32_t* u, const int32_t* v, const double* w, int64_t n_edges,
+                    int64_t n_vertices, int32_t* orig_of, double* heights, int32_t* edge_parent,
+                    int32_t* vertex_parent, dmst_stats* stats, void* workspace, size_t workspace_bytes,
+                    void* stream) {
+  // side stream + events are per host thread and reused across calls
+  thread_local cudaStream_t side = nullptr;
+  thread_local cudaEvent_t evs[6] = {};
+  thread_local int side_dev = -1;
+  int rc = guarded([&] {
+    if (n_edges < 1 || n_vertices != n_edges + 1) invalid("n_vertices must equal n_edges + 1 (a spanning tree)");
     if (!u || !v || !w || !orig_of || !heights || !edge_parent || !vertex_parent)
       invalid("null input/output pointer");
-    Ctx c;
-    init_ctx(c, n, nv, ws, stream, st);
-    Sort1FinalEmitter em{orig_of, heights, c.w.euv0, nullptr, nullptr};
-    int p1 = 0;
-    edge_sort(c, u, v, w, n, em, &p1);
-    pandora_core(c, n, nv, vertex_parent, edge_parent, st, dbg_ret, dbg_key, dbg_term, dbg_lvl);
-    c.sync();
-    c.collect(st);
-    if (st) {
-      st->sort1_passes = p1;
-      st->kernel_launches = c.launches;
+    if (!workspace || workspace_bytes < dmst_host_workspace_bytes(n_edges, n_vertices))
+      invalid("workspace too small (dmst_host_workspace_bytes)");
+    int dev = 0;
+    DMST_CUDA(cudaGetDevice(&dev));
+    if (side == nullptr || side_dev != dev) {
+      DMST_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+      for (auto& e : evs) DMST_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      side_dev = dev;
     }
   });
+  if (rc) return rc;
+  const int64_t n = n_edges, nv = n_vertices;
+  char* base = (char*)(((uintptr_t)workspace + 255) & ~uintptr_t(255));
+  const size_t pipe = carve(n, nv, nullptr).bytes;
+  HostBufs b = host_bufs(n, nv, base + pipe);
+  rc = guarded([&] {
+    cudaStream_t s = (cudaStream_t)stream;
+    // inputs: H2D on the side stream, ordered after work already on `stream`
+    DMST_CUDA(cudaEventRecord(evs[4], s));
+    DMST_CUDA(cudaStreamWaitEvent(side, evs[4], 0));
+    DMST_CUDA(cudaMemcpyAsync(b.w, w, 8 * (size_t)n, cudaMemcpyHostToDevice, side));
+    DMST_CUDA(cudaMemcpyAsync(b.u, u, 4 * (size_t)n, cudaMemcpyHostToDevice, side));
+    DMST_CUDA(cudaMemcpyAsync(b.v, v, 4 * (size_t)n, cudaMemcpyHostToDevice, side));
+    DMST_CUDA(cudaEventRecord(evs[5], side));
+  });
+  if (rc) return rc;
+  HostIO io;
+  io.side = side;
+  io.h_orig = orig_of;
+  io.h_heights = heights;
+  io.h_ep = edge_parent;
+  io.h_vp = vertex_parent;
+  io.n = n;
+  io.nv = nv;
+  for (int i = 0; i < 4; ++i) io.ev[i] = evs[i];
+  return build_impl(b.u, b.v, b.w, n, nv, b.orig, b.heights, b.ep, b.vp, stats, nullptr, nullptr, nullptr,
+                    nullptr, base, pipe, stream, &io, evs[5]);
 }
 
 int dmst_build(const int32_t* u, const int32_t* v, const double* w, int64_t n_edges,

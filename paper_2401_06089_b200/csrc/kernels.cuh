@@ -129,6 +129,11 @@ __global__ void k_fix_negzero(const double* __restrict__ w, const int32_t* __res
   if (r < n && heights[r] == 0.0) heights[r] = w[orig_of[r]];
 }
 
+// Copy a few words into host-mapped memory (small readbacks without the copy engines).
+__global__ void k_readback(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, uint32_t words) {
+  for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+}
+
 // dmst_pandora entry: already-ranked endpoints -> packed euv.
 __global__ void k_pack_euv(const int32_t* __restrict__ ru, const int32_t* __restrict__ rv, int64_t n,
                            int2* __restrict__ euv) {

@@ -153,6 +153,23 @@ def test_split_entry_points_equal_fused(builder):
     assert st.view_kind_counts() == fused.view_kind_counts
 
 
+@pytest.mark.parametrize("shape,n", [("tied", 1), ("random", 5000), ("tied", 300_000), ("path", 70_000)])
+def test_host_buffer_entry_point(builder, shape, n):
+    # dmst_build_host: host inputs/outputs, copies overlapped with the pipeline
+    import torch
+    from paper_2401_06089_b200 import HostBuildResult
+    nv, u, v, w = synth.GENERATORS[shape](n, seed=7)
+    exp = O.build(nv, u, v, w)
+    for pinned in (True, False):
+        out = HostBuildResult.empty(n, nv, pin=pinned)
+        hu, hv, hw = (torch.from_numpy(x) for x in (u, v, w))
+        if pinned:
+            hu, hv, hw = hu.pin_memory(), hv.pin_memory(), hw.pin_memory()
+        res = builder.build_host(nv, hu, hv, hw, out=out)
+        assert_matches(res, exp.orig_of, exp.heights, exp.edge_parent, exp.vertex_parent)
+        assert res.stats.view_kind_counts() == list(exp.view_kind_counts)
+
+
 def test_drop_in_functions():
     from paper_2401_06089_b200 import pandora_b200, rank_edges_b200, Dendrogram
     from types import SimpleNamespace

@@ -11,24 +11,42 @@
 // the bucket's slice of mi64 (and V1's outputs) with coalesced stores.
 #pragma once
 #include "common.cuh"
+#include "radix.cuh"  // TMA bulk-copy / mbarrier helpers
 
 namespace dmst {
 
 constexpr int FB_BITS = 13;                  // fine bucket = 8192 vertices (64 KB of smem state)
 constexpr int FB = 1 << FB_BITS;
-constexpr int BK_BLOCK = 256, BK_ITEMS = 16;  // bucketing sub-tile = 4096 records
-constexpr int BK_T = BK_BLOCK * BK_ITEMS;
-constexpr int BK_SPAN = 4096;                 // max fine buckets one pass-B sub-tile may touch
+// multisplit geometry: pass A (coarse, <= 256 buckets) and pass B (fine)
+constexpr int BKA_BLOCK = 512, BKA_ITEMS = 8;   // 4096 records per sub-tile
+constexpr int BKB_BLOCK = 256, BKB_ITEMS = 8;   // 2048 records per sub-tile
+constexpr int BKB_SPAN = 1024;                  // max fine buckets a pass-B sub-tile may touch
 
-struct Recs {  // SoA records (vertex, j + 1, other end)
-  uint32_t* x;
-  uint32_t* j1;
-  uint32_t* o;
+// Records are AoS triples (vertex, j + 1, other end): a bucket run of m
+// records is one contiguous run of 12 m bytes.
+struct Recs {
+  uint32_t* r;  // [3 m]
 };
 
-// Record i of edge i >> 1 of a view (endpoints euv).
+// Record i of edge i >> 1 of a view (endpoints euv).  Sources also describe
+// their staged form (SB bytes per record, contiguous from base()) so
+// sub-tiles can be fetched with TMA bulk copies.
 struct EdgeRecSrc {
+  static constexpr int SB = 4;  // 8 B per edge = 2 records
   const int2* __restrict__ euv;
+  __device__ __forceinline__ const void* base() const { return euv; }
+  __device__ __forceinline__ void get(const unsigned char* stage, int li, int64_t i, uint32_t& x, uint32_t& j1,
+                                      uint32_t& o) const {
+    const int2 e = reinterpret_cast<const int2*>(stage)[li >> 1];
+    const bool second = i & 1;
+    x = (uint32_t)(second ? e.y : e.x);
+    o = (uint32_t)(second ? e.x : e.y);
+    j1 = (uint32_t)(i >> 1) + 1u;
+  }
+  __device__ __forceinline__ uint32_t staged_vertex(const unsigned char* stage, int li, int64_t i) const {
+    const int2 e = reinterpret_cast<const int2*>(stage)[li >> 1];
+    return (uint32_t)((i & 1) ? e.y : e.x);
+  }
   __device__ __forceinline__ void load(int64_t i, uint32_t& x, uint32_t& j1, uint32_t& o) const {
     const int2 e = __ldg(euv + (i >> 1));
     const bool second = i & 1;
@@ -42,16 +60,26 @@ struct EdgeRecSrc {
   }
 };
 
-struct SoaRecSrc {
-  const uint32_t* __restrict__ x;
-  const uint32_t* __restrict__ j1;
-  const uint32_t* __restrict__ o;
-  __device__ __forceinline__ void load(int64_t i, uint32_t& xx, uint32_t& jj, uint32_t& oo) const {
-    xx = ld_stream(x + i);
-    jj = ld_stream(j1 + i);
-    oo = ld_stream(o + i);
+struct AosRecSrc {
+  static constexpr int SB = 12;
+  const uint32_t* __restrict__ r;
+  __device__ __forceinline__ const void* base() const { return r; }
+  __device__ __forceinline__ void get(const unsigned char* stage, int li, int64_t, uint32_t& x, uint32_t& j1,
+                                      uint32_t& o) const {
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(stage) + 3 * li;
+    x = p[0];
+    j1 = p[1];
+    o = p[2];
   }
-  __device__ __forceinline__ uint32_t vertex(int64_t i) const { return ld_stream(x + i); }
+  __device__ __forceinline__ uint32_t staged_vertex(const unsigned char* stage, int li, int64_t) const {
+    return reinterpret_cast<const uint32_t*>(stage)[3 * li];
+  }
+  __device__ __forceinline__ void load(int64_t i, uint32_t& xx, uint32_t& jj, uint32_t& oo) const {
+    xx = ld_stream(r + 3 * i);
+    jj = ld_stream(r + 3 * i + 1);
+    oo = ld_stream(r + 3 * i + 2);
+  }
+  __device__ __forceinline__ uint32_t vertex(int64_t i) const { return __ldg(r + 3 * i); }
 };
 
 // counts[f] += number of records whose vertex is in fine bucket f, for
@@ -107,129 +135,149 @@ __global__ void __launch_bounds__(1024) k_fine_scan(const uint32_t* __restrict__
 }
 
 // One order-free multisplit pass.  Pass A (FINE = false): bucket = fine >> gshift
-// (< 256 buckets).  Pass B (FINE = true): bucket = fine bucket, input already
+// (<= 256 buckets).  Pass B (FINE = true): bucket = fine bucket, input already
 // grouped by coarse bucket so a sub-tile touches a narrow fine range.
-// Persistent CTAs, grid-stride over sub-tiles of BK_T records.
-template <bool FINE>
-constexpr size_t bucket_smem_bytes() { return 4 * (2 * (FINE ? BK_SPAN : 256) + 3 * BK_T); }
+// Persistent CTAs take sub-tiles round-robin; sub-tile k + 2 is fetched by a
+// TMA bulk copy (mbarrier completion) while sub-tile k is grouped, so DRAM
+// latency stays off the critical path.  Per sub-tile: a shared-memory atomic
+// per record gives its slot within its bucket, one global atomic per
+// non-empty bucket reserves the output range, the records are regrouped in
+// shared memory and written out as one word stream (consecutive threads ->
+// consecutive words of a bucket run).  Only the slots live in registers.
+template <class Src, int BLOCK, int ITEMS, int NC>
+struct SplitSmem {
+  static constexpr int T = BLOCK * ITEMS;
+  __host__ __device__ static constexpr size_t in_bytes() { return ((size_t)T * Src::SB + 127) & ~size_t(127); }
+  __host__ __device__ static constexpr size_t off_st() { return 2 * in_bytes(); }
+  __host__ __device__ static constexpr size_t off_cnt() { return off_st() + 12 * (size_t)T; }
+  __host__ __device__ static constexpr size_t bytes() { return off_cnt() + 8 * (size_t)NC; }
+};
 
-template <bool FINE, class Src>
-__global__ void __launch_bounds__(BK_BLOCK) k_bucket(Src src, int64_t m, uint32_t gshift,
-                                                     uint32_t* __restrict__ cursor, Recs out) {
-  constexpr int NC = FINE ? BK_SPAN : 256;
-  extern __shared__ uint32_t bsm[];
-  uint32_t* cnt = bsm;            // [NC]
-  uint32_t* gofs = bsm + NC;      // [NC]
-  uint32_t* stx = bsm + 2 * NC;   // [BK_T]
-  uint32_t* stj = stx + BK_T;
-  uint32_t* sto = stj + BK_T;
-  __shared__ uint32_t scratch[BK_BLOCK / 32 + 1];
+template <bool FINE, class Src, int BLOCK, int ITEMS, int NC>
+__global__ void __launch_bounds__(BLOCK) k_split(Src src, int64_t m, uint32_t gshift,
+                                                 uint32_t* __restrict__ cursor, Recs out) {
+  using S = SplitSmem<Src, BLOCK, ITEMS, NC>;
+  constexpr int T = S::T;
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint32_t* st = reinterpret_cast<uint32_t*>(sm + S::off_st());    // [3 T] grouped records
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(sm + S::off_cnt());  // [NC]
+  uint32_t* gofs = cnt + NC;                                       // [NC]
+  __shared__ uint32_t scratch[BLOCK / 32 + 1];
   __shared__ uint32_t s_lo, s_span;
+  __shared__ __align__(8) uint64_t bar[2];
   const uint32_t tid = threadIdx.x;
-  for (int64_t t0 = (int64_t)blockIdx.x * BK_T; t0 < m; t0 += (int64_t)gridDim.x * BK_T) {
-    const int64_t rem = m - t0;
-    const int count = rem < BK_T ? (int)rem : BK_T;
+  const int64_t ntiles = (m + T - 1) / T;
+  const bool tma = aligned16(src.base());
+
+  auto issue = [&](int64_t tile, int buf) {
+    const int64_t t0 = tile * T;
+    if (!tma || tile >= ntiles || t0 + T > m) return;
+    fence_proxy_async();
+    mbar_expect_tx(&bar[buf], (uint32_t)(T * Src::SB));
+    bulk_g2s(sm + buf * S::in_bytes(), (const char*)src.base() + t0 * Src::SB, (uint32_t)(T * Src::SB), &bar[buf]);
+  };
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    issue(blockIdx.x, 0);
+    issue(blockIdx.x + gridDim.x, 1);
+  }
+
+  int k = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+    const int buf = k & 1;
+    const unsigned char* stage = sm + buf * S::in_bytes();
+    const int64_t t0 = tile * T;
+    const int count = m - t0 < T ? (int)(m - t0) : T;
+    const bool staged = tma && count == T;
+    if (staged) mbar_wait(&bar[buf], (uint32_t)(k >> 1) & 1u);
+    auto rec = [&](int li, uint32_t& x, uint32_t& j1, uint32_t& o) {
+      if (staged)
+        src.get(stage, li, t0 + li, x, j1, o);
+      else
+        src.load(t0 + li, x, j1, o);
+    };
+    auto vtx = [&](int li) { return staged ? src.staged_vertex(stage, li, t0 + li) : src.vertex(t0 + li); };
     if (tid == 0) {
       uint32_t lo = 0, span = NC;
       if (FINE) {
-        const uint32_t c0 = src.vertex(t0) >> (FB_BITS + gshift);
-        const uint32_t c1 = src.vertex(t0 + count - 1) >> (FB_BITS + gshift);
+        const uint32_t c0 = vtx(0) >> (FB_BITS + gshift);
+        const uint32_t c1 = vtx(count - 1) >> (FB_BITS + gshift);
         lo = c0 << gshift;
         span = (c1 + 1 - c0) << gshift;
       }
       s_lo = lo;
       s_span = span;
     }
-    for (int i = tid; i < NC; i += BK_BLOCK) cnt[i] = 0;
+    for (int i = tid; i < NC; i += BLOCK) cnt[i] = 0;
     __syncthreads();
     const uint32_t lo = s_lo;
-    const bool smem_path = s_span <= (uint32_t)NC;
-    uint32_t x[BK_ITEMS], j1[BK_ITEMS], o[BK_ITEMS], bk[BK_ITEMS], slot[BK_ITEMS];
-#pragma unroll
-    for (int i = 0; i < BK_ITEMS; ++i) {
-      const int li = i * BK_BLOCK + tid;
-      if (li < count) src.load(t0 + li, x[i], j1[i], o[i]);
-    }
-    if (!smem_path) {
+    if (s_span > (uint32_t)NC) {
       // rare: a sub-tile spanning more fine buckets than the shared counters
       // hold (heavily skewed vertex ids) -> one global atomic per record
-#pragma unroll
-      for (int i = 0; i < BK_ITEMS; ++i) {
-        const int li = i * BK_BLOCK + tid;
-        if (li < count) {
-          const uint32_t f = x[i] >> FB_BITS;
-          const uint32_t d = atomicAdd(cursor + f, 1u);
-          out.x[d] = x[i];
-          out.j1[d] = j1[i];
-          out.o[d] = o[i];
-        }
+      for (int li = tid; li < count; li += BLOCK) {
+        uint32_t x, j1, o;
+        rec(li, x, j1, o);
+        const uint64_t d = atomicAdd(cursor + (x >> FB_BITS), 1u);
+        out.r[3 * d] = x;
+        out.r[3 * d + 1] = j1;
+        out.r[3 * d + 2] = o;
       }
       __syncthreads();
+      if (tid == 0) issue(tile + 2 * (int64_t)gridDim.x, buf);
       continue;
     }
+    auto bucket = [&](uint32_t x) { return FINE ? (x >> FB_BITS) - lo : (x >> FB_BITS) >> gshift; };
+    uint32_t slot[ITEMS];
 #pragma unroll
-    for (int i = 0; i < BK_ITEMS; ++i) {
-      const int li = i * BK_BLOCK + tid;
-      if (li < count) {
-        const uint32_t f = x[i] >> FB_BITS;
-        bk[i] = FINE ? f - lo : f >> gshift;
-        slot[i] = atomicAdd(&cnt[bk[i]], 1u);
-      }
+    for (int i = 0; i < ITEMS; ++i) {
+      const int li = i * BLOCK + tid;
+      if (li < count) slot[i] = atomicAdd(&cnt[bucket(vtx(li))], 1u);
     }
     __syncthreads();
-    // local exclusive scan of the counters + global reservation; thread t owns
-    // counters [t * per, (t + 1) * per) of the active span (per = 1 unless a
-    // sub-tile straddles many buckets), so reservations go out in parallel
-    const uint32_t span = FINE ? s_span : (uint32_t)NC;
-    const uint32_t per = (span + BK_BLOCK - 1) / BK_BLOCK;
-    constexpr int PMAX = NC / BK_BLOCK;
-    uint32_t c[PMAX], s = 0;
+    // exclusive scan of the counters + global reservation; thread t owns
+    // counters [t * PER, (t + 1) * PER)
+    constexpr int PER = (NC + BLOCK - 1) / BLOCK;
+    uint32_t c[PER], sum = 0;
 #pragma unroll
-    for (int q = 0; q < PMAX; ++q) {
-      c[q] = (uint32_t)q < per ? cnt[tid * per + q] : 0u;
-      s += c[q];
+    for (int q = 0; q < PER; ++q) {
+      const uint32_t b = tid * PER + q;
+      c[q] = b < (uint32_t)NC ? cnt[b] : 0u;
+      sum += c[q];
     }
     uint32_t tot;
-    uint32_t run = block_excl_sum<BK_BLOCK>(s, scratch, &tot);
-    uint32_t g[PMAX];
+    uint32_t run = block_excl_sum<BLOCK>(sum, scratch, &tot);
 #pragma unroll
-    for (int q = 0; q < PMAX; ++q) {
-      const uint32_t b = tid * per + q;
-      g[q] = ((uint32_t)q < per && c[q]) ? atomicAdd(cursor + (FINE ? lo + b : b), c[q]) : 0u;
-    }
-#pragma unroll
-    for (int q = 0; q < PMAX; ++q) {
-      if ((uint32_t)q < per) {
-        const uint32_t b = tid * per + q;
-        if (c[q]) gofs[b] = g[q] - run;
-        cnt[b] = run;  // becomes the local start of bucket b
+    for (int q = 0; q < PER; ++q) {
+      const uint32_t b = tid * PER + q;
+      if (b < (uint32_t)NC) {
+        if (c[q]) gofs[b] = atomicAdd(cursor + (FINE ? lo + b : b), c[q]) - run;
+        cnt[b] = run;  // local start of bucket b
         run += c[q];
       }
     }
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < BK_ITEMS; ++i) {
-      const int li = i * BK_BLOCK + tid;
+    for (int i = 0; i < ITEMS; ++i) {
+      const int li = i * BLOCK + tid;
       if (li < count) {
-        const uint32_t p = cnt[bk[i]] + slot[i];
-        stx[p] = x[i];
-        stj[p] = j1[i];
-        sto[p] = o[i];
+        uint32_t x, j1, o;
+        rec(li, x, j1, o);
+        const uint32_t p = cnt[bucket(x)] + slot[i];
+        st[3 * p] = x;
+        st[3 * p + 1] = j1;
+        st[3 * p + 2] = o;
       }
     }
     __syncthreads();
-#pragma unroll
-    for (int i = 0; i < BK_ITEMS; ++i) {
-      const int sidx = i * BK_BLOCK + tid;
-      if (sidx < count) {
-        const uint32_t xx = stx[sidx];
-        const uint32_t f = xx >> FB_BITS;
-        const uint32_t b = FINE ? f - lo : f >> gshift;
-        const uint32_t d = gofs[b] + sidx;
-        out.x[d] = xx;
-        out.j1[d] = stj[sidx];
-        out.o[d] = sto[sidx];
-      }
+    if (tid == 0) issue(tile + 2 * (int64_t)gridDim.x, buf);  // stage buffer consumed
+    for (int s_ = tid; s_ < 3 * count; s_ += BLOCK) {
+      const int it = s_ / 3;
+      out.r[3 * (uint64_t)gofs[bucket(st[3 * it])] + s_] = st[s_];
     }
     __syncthreads();
   }
@@ -263,8 +311,10 @@ __global__ void __launch_bounds__(512) k_mi_apply_smem(Recs rec, const uint32_t*
 #pragma unroll
     for (int q = 0; q < U; ++q) {
       const uint32_t i = b + q * blockDim.x;
-      xl[q] = i < re ? ld_stream(rec.x + i) - (uint32_t)v0 : 0u;
-      pk[q] = i < re ? ((unsigned long long)ld_stream(rec.j1 + i) << 32) | ld_stream(rec.o + i) : 0ull;
+      xl[q] = i < re ? ld_stream(rec.r + 3 * (uint64_t)i) - (uint32_t)v0 : 0u;
+      pk[q] = i < re ? ((unsigned long long)ld_stream(rec.r + 3 * (uint64_t)i + 1) << 32) |
+                           ld_stream(rec.r + 3 * (uint64_t)i + 2)
+                     : 0ull;
     }
 #pragma unroll
     for (int q = 0; q < U; ++q)

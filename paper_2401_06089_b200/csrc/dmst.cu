@@ -396,8 +396,10 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
 template <class Src>
 void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiApplyOut out) {
   const uint32_t nf = (uint32_t)cdiv(nv, FB);
-  uint32_t gshift = 0;  // coarse bucket = 2^gshift fine buckets, <= 256 coarse buckets
-  while ((int64_t(nf) >> gshift) > 255) ++gshift;
+  // coarse bucket = 2^gshift fine buckets, about sqrt(nf) coarse buckets so
+  // both passes write runs of similar length
+  uint32_t gshift = 0;
+  while ((int64_t(nf) >> gshift) > 255 || (int64_t(nf) >> gshift) > (1ll << (gshift + 1))) ++gshift;
   uint32_t* counts = c.w.fine;
   uint32_t* fine_base = counts + (nf + 2);
   uint32_t* fine_cur = fine_base + (nf + 2);
@@ -412,15 +414,17 @@ void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiAp
   c.begin(KK_MI_SPLIT);
   k_fine_scan<<<1, 1024, 0, c.s>>>(counts, nf, gshift, fine_base, fine_cur, coarse_cur);
   c.launched();
-  constexpr size_t smA = bucket_smem_bytes<false>(), smB = bucket_smem_bytes<true>();
-  DMST_CUDA(cudaFuncSetAttribute(k_bucket<false, Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA));
-  DMST_CUDA(cudaFuncSetAttribute(k_bucket<true, SoaRecSrc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smB));
+  using SA = SplitSmem<Src, BKA_BLOCK, BKA_ITEMS, 256>;
+  using SB = SplitSmem<AosRecSrc, BKB_BLOCK, BKB_ITEMS, BKB_SPAN>;
+  auto kA = k_split<false, Src, BKA_BLOCK, BKA_ITEMS, 256>;
+  auto kB = k_split<true, AosRecSrc, BKB_BLOCK, BKB_ITEMS, BKB_SPAN>;
+  DMST_CUDA(cudaFuncSetAttribute(kA, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SA::bytes()));
+  DMST_CUDA(cudaFuncSetAttribute(kB, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SB::bytes()));
   c.begin(KK_MI_SPLIT);
-  k_bucket<false, Src><<<c.persistent_grid(m, BK_T, 3), BK_BLOCK, smA, c.s>>>(src, m, gshift, coarse_cur, mid);
+  kA<<<c.persistent_grid(m, SA::T, 2), BKA_BLOCK, SA::bytes(), c.s>>>(src, m, gshift, coarse_cur, mid);
   c.launched();
   c.begin(KK_MI_SPLIT);
-  k_bucket<true, SoaRecSrc><<<c.persistent_grid(m, BK_T, 2), BK_BLOCK, smB, c.s>>>(SoaRecSrc{mid.x, mid.j1, mid.o}, m,
-                                                                                   gshift, fine_cur, fin);
+  kB<<<c.persistent_grid(m, SB::T, 2), BKB_BLOCK, SB::bytes(), c.s>>>(AosRecSrc{mid.r}, m, gshift, fine_cur, fin);
   c.launched();
   DMST_CUDA(cudaFuncSetAttribute(k_mi_apply_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * FB));  // 64 KB
   c.begin(KK_MI_APPLY);
@@ -428,9 +432,8 @@ void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiAp
   c.launched();
 }
 
-Recs recs_at(char* base, int64_t m) {
-  uint32_t* p = (uint32_t*)base;
-  return Recs{p, p + m, p + 2 * m};
+Recs recs_at(char* base, int64_t) {
+  return Recs{(uint32_t*)base};
 }
 
 // Full pipeline after the edge sort: euv0 (rank-order endpoints) ready.
@@ -546,9 +549,6 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     es.euv_next = w.euv[cur ^ 1];
     es.grank_next = w.grank[cur ^ 1];
     es.mi64_next = direct ? mi_next : nullptr;
-    es.rec_vtx = rec;
-    es.rec_j1 = rec + 2 * n_next;
-    es.rec_oth = rec + 4 * n_next;
     es.x1 = level == 0 ? w.x1 : nullptr;
     es.level = (int8_t)level;
     {
@@ -564,8 +564,7 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     v1_done = false;
     if (!direct && n_next > 0) {
       const int64_t m = 2 * n_next;
-      mi_buckets(c, SoaRecSrc{es.rec_vtx, es.rec_j1, es.rec_oth}, m, nv_next, recs_at(w.R, m),
-                 Recs{es.rec_vtx, es.rec_j1, es.rec_oth},
+      mi_buckets(c, EdgeRecSrc{es.euv_next}, m, nv_next, recs_at(w.R, m), Recs{rec},
                  MiApplyOut{mi_next, w.smi_all + lt.soff[level + 1], w.grank[cur ^ 1], w.cnt2});
       v1_done = true;
     }

@@ -369,8 +369,8 @@ k_select(int64_t n, uint32_t* __restrict__ status, uint32_t* __restrict__ tile_c
 // Retire non-alpha edges of view k at level k (contraction.py:207) and
 // compact alpha edges, in rank order, into view k+1 with endpoints remapped
 // to supervertices (:170-172).  The next view's maxIncident is either
-// scatter-maxed directly (small views) or emitted as records for the
-// multisplit + apply path.
+// scatter-maxed directly (small views) or bucketed afterwards from euv_next
+// (multisplit + apply path, bucket.cuh).
 struct EdgeSel {
   uint32_t* __restrict__ cnt2;       // read, then zeroed for the next view
   const int2* __restrict__ euv;
@@ -379,10 +379,7 @@ struct EdgeSel {
   int8_t* __restrict__ ret;
   int2* __restrict__ euv_next;
   int32_t* __restrict__ grank_next;
-  unsigned long long* __restrict__ mi64_next;  // direct mode (null => records)
-  uint32_t* __restrict__ rec_vtx;
-  uint32_t* __restrict__ rec_j1;
-  uint32_t* __restrict__ rec_oth;
+  unsigned long long* __restrict__ mi64_next;  // direct mode (null => bucketed from euv_next)
   int32_t* __restrict__ x1;          // view 0 only: view-1 supervertex of every edge (walk start)
   int8_t level;
   struct Item {
@@ -414,13 +411,6 @@ struct EdgeSel {
       if (mi64_next) {
         atomicMax(mi64_next + a, pack_mi(pos + 1u, (uint32_t)b));
         atomicMax(mi64_next + b, pack_mi(pos + 1u, (uint32_t)a));
-      } else {
-        rec_vtx[2 * pos] = (uint32_t)a;
-        rec_j1[2 * pos] = pos + 1u;
-        rec_oth[2 * pos] = (uint32_t)b;
-        rec_vtx[2 * pos + 1] = (uint32_t)b;
-        rec_j1[2 * pos + 1] = pos + 1u;
-        rec_oth[2 * pos + 1] = (uint32_t)a;
       }
     }
   }

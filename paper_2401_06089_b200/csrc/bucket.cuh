@@ -19,7 +19,7 @@ constexpr int FB_BITS = 13;                  // fine bucket = 8192 vertices (64 
 constexpr int FB = 1 << FB_BITS;
 // multisplit geometry: pass A (coarse, <= 256 buckets) and pass B (fine)
 constexpr int BKA_BLOCK = 512, BKA_ITEMS = 8;   // 4096 records per sub-tile
-constexpr int BKB_BLOCK = 256, BKB_ITEMS = 8;   // 2048 records per sub-tile
+constexpr int BKB_BLOCK = 512, BKB_ITEMS = 4;   // 2048 records per sub-tile
 constexpr int BKB_SPAN = 1024;                  // max fine buckets a pass-B sub-tile may touch
 
 // Records are AoS triples (vertex, j + 1, other end): a bucket run of m

@@ -225,24 +225,39 @@ __global__ void __launch_bounds__(256) k_upsweep(SweepArgs a, Loader ld) {
 }
 
 // Exclusive scan of counts[R][GS] in place, digit-major => the global
-// output offset of every (digit, chunk).  Thread t owns rows t*BPT.. (vector loads).
+// output offset of every (digit, chunk).  Thread t owns rows t*BPT.. (vector
+// loads).  Also picks the pass's warp-ranking method: with digit
+// frequencies p_d, a warp of 32 items holds E = sum_d 1 - (1 - p_d)^32
+// distinct digits on average; __match_any_sync is cheaper below ~kBallotE,
+// ballots above (counts[R * GS] = 1 => ballots).
+constexpr float kBallotE = 12.0f;
 template <int BITS>
 __global__ void __launch_bounds__(256) k_chunk_scan(uint32_t* counts, uint32_t GS) {
-  constexpr int BPT = (1 << BITS) / 256;
+  constexpr int R = 1 << BITS, BPT = R / 256;
   __shared__ uint32_t scratch[256 / 32 + 1];
+  __shared__ float fscr[256 / 32];
   const uint32_t nq = GS / 4;
-  uint32_t s = 0;
+  uint32_t s = 0, rs[BPT];
 #pragma unroll
   for (int r = 0; r < BPT; ++r) {
     const uint4* row = reinterpret_cast<const uint4*>(counts + (uint64_t)(threadIdx.x * BPT + r) * GS);
+    uint32_t t = 0;
 #pragma unroll 8
     for (uint32_t q = 0; q < nq; ++q) {
       const uint4 v = row[q];
-      s += v.x + v.y + v.z + v.w;
+      t += v.x + v.y + v.z + v.w;
     }
+    rs[r] = t;
+    s += t;
   }
   uint32_t tot;
   uint32_t run = block_excl_sum<256>(s, scratch, &tot);
+  float e = 0.f;
+#pragma unroll
+  for (int r = 0; r < BPT; ++r) e += 1.f - __powf(1.f - (float)rs[r] / (float)max(tot, 1u), 32.f);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(kFull, e, o);
+  if ((threadIdx.x & 31) == 0) fscr[threadIdx.x >> 5] = e;
 #pragma unroll
   for (int r = 0; r < BPT; ++r) {
     uint4* row = reinterpret_cast<uint4*>(counts + (uint64_t)(threadIdx.x * BPT + r) * GS);
@@ -257,6 +272,12 @@ __global__ void __launch_bounds__(256) k_chunk_scan(uint32_t* counts, uint32_t G
       run = o.w + v.w;
       row[q] = o;
     }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float E = 0.f;
+    for (int w = 0; w < 256 / 32; ++w) E += fscr[w];
+    counts[(uint64_t)R * GS] = E > kBallotE ? 1u : 0u;
   }
 }
 
@@ -291,27 +312,31 @@ struct DownSmem {
     uint32_t lstart[R];
     uint32_t gofs[R];
     uint32_t scan[NW + 1];
+    uint32_t ballot;     // ranking method of this pass
     uint64_t bar[2];
   };
   __host__ __device__ static constexpr size_t bytes() { return off_misc() + sizeof(Misc); }
 };
 
-// Stable rank of item i within its warp's items of equal digit.  Peers by
-// __match_any_sync (DMST_RANK_BALLOT selects 8 ballots instead); all peers
-// read the warp counter (broadcast), the lowest peer advances it.
+// Stable rank of item i within its warp's items of equal digit.  Peers come
+// from __match_any_sync (cost grows with the number of distinct digits in
+// the warp) or from BITS ballots (constant cost); `ballot` is chosen per
+// pass from the digit distribution (k_chunk_scan).  All peers read the warp
+// counter (broadcast), the lowest peer advances it.
 template <bool FULL, int BITS>
 __device__ __forceinline__ uint32_t warp_rank(uint32_t* whist, uint32_t d, bool valid, uint32_t lane,
-                                              uint32_t lt) {
-#ifdef DMST_RANK_BALLOT
-  uint32_t peers = FULL ? kFull : (valid ? __ballot_sync(kFull, valid) : ~__ballot_sync(kFull, valid));
+                                              uint32_t lt, bool ballot) {
+  uint32_t peers;
+  if (ballot) {
+    peers = FULL ? kFull : (valid ? __ballot_sync(kFull, valid) : ~__ballot_sync(kFull, valid));
 #pragma unroll
-  for (int b = 0; b < BITS; ++b) {
-    const uint32_t bit = (d >> b) & 1u;
-    peers &= __ballot_sync(kFull, bit) ^ (bit - 1u);
+    for (int b = 0; b < BITS; ++b) {
+      const uint32_t bit = (d >> b) & 1u;
+      peers &= __ballot_sync(kFull, bit) ^ (bit - 1u);
+    }
+  } else {
+    peers = __match_any_sync(kFull, FULL ? d : (valid ? d : 0xffffu));
   }
-#else
-  const uint32_t peers = __match_any_sync(kFull, FULL ? d : (valid ? d : 0xffffu));
-#endif
   uint32_t old = 0;
   if (FULL || valid) old = whist[d];
   const uint32_t below = __popc(peers & lt);
@@ -336,7 +361,7 @@ __device__ __forceinline__ void down_subtile(const SweepArgs& a, const Emitter& 
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const bool valid = FULL || lbase + i * 32 < cnt_items;
-    rk[i] = warp_rank<FULL, BITS>(m.whist[warp], digit_of<BITS>(k[i], a.shift), valid, lane, lt);
+    rk[i] = warp_rank<FULL, BITS>(m.whist[warp], digit_of<BITS>(k[i], a.shift), valid, lane, lt, m.ballot);
   }
   __syncthreads();  // (also: every thread has finished reading `buf`)
 
@@ -426,6 +451,7 @@ k_downsweep(SweepArgs a, Loader ld, Emitter em) {
     mbar_init(&m.bar[0], 1);
     mbar_init(&m.bar[1], 1);
     mbar_fence_init();
+    m.ballot = a.counts[(uint64_t)R * a.GS];
   }
   __syncthreads();
 

@@ -16,7 +16,7 @@
 //  3. contraction      build_hierarchy       contraction.py:186-219
 //     per view k: k_v1 (maxIncident + 2-bit child counts), k_leafscan
 //     (leaf-edge numbering = supervertex ids), k_v2 (chase to the leaf
-//     edge; k_jump rounds for deep in-trees), k_select<EdgeSel>
+//     edge; k_jump rounds for deep in-trees), k_select_edges
 //     (retirement, alpha-edge compaction into view k+1).
 //  4. expansion        assign_chains         expansion.py:97-128
 //     k_walk: per edge, the level walk -> dense chain key (+ digit histogram)
@@ -96,7 +96,8 @@ struct Workspace {
   int32_t* vm_all;        // vertex maps of views 0..L-1
   int32_t* smi_all;       // maxIncident (global ranks) of views 1..L
   int32_t* x1;            // view-1 supervertex of every edge (walk start)
-  uint32_t* sel_status;   // select/leafscan look-back words
+  uint32_t* sel_status;   // leafscan look-back words (leaf, alpha)
+  uint32_t* apre;         // alpha prefix per 16 edges
   size_t bytes;
 };
 
@@ -107,7 +108,7 @@ constexpr int SM_HIST1 = 0, SM_GBASE1 = SM_HIST1 + 8 * kRadix, SM_HIST2 = SM_GBA
               SM_GBASE2 = SM_HIST2 + 4 * kRadix, SM_VHIST = SM_GBASE2 + 4 * kRadix,
               SM_VBASE = SM_VHIST + kRadix, SM_TILECTR = SM_VBASE + kRadix, SM_MISC = SM_TILECTR + 64;
 constexpr int MISC_NEGZERO = 0, MISC_ACTIVE0 = 1, MISC_ACTIVE1 = 2, MISC_ACTIVE2 = 3, MISC_COUNTS = 4 /*2*/,
-              MISC_NONRUL = 6, MISC_SELTOT = 8 /*1*/, MISC_SELCTR = 12, MISC_LSCTR = 13;
+              MISC_NONRUL = 6, MISC_LSCTR = 13;
 
 Workspace carve(int64_t n, int64_t nv, char* base) {
   Workspace w{};
@@ -135,7 +136,8 @@ Workspace carve(int64_t n, int64_t nv, char* base) {
   w.vm_all = (int32_t*)take(4 * (2 * nv + DMST_MAX_LEVELS + 2));
   w.smi_all = (int32_t*)take(4 * (nv + DMST_MAX_LEVELS + 2));
   w.x1 = (int32_t*)take(4 * (n + 2));
-  w.sel_status = (uint32_t*)take(4 * (cdiv(std::max(nv, n), SEL_TILE) + 2));
+  w.sel_status = (uint32_t*)take(8 * (cdiv(n / 16 + 1, LS_TILE) + 2));
+  w.apre = (uint32_t*)take(4 * (n / 16 + 2));
   w.bytes = off + 256;
   return w;
 }
@@ -471,12 +473,13 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     }
     // leaf numbering + kind counts
     const int64_t words = n_k / 16 + 1;
-    c.zero(w.sel_status, 4 * (cdiv(words, 2048) + 1));
+    const unsigned ls_tiles = grid_for(words, LS_TILE);
+    c.zero(w.sel_status, 8 * (size_t)ls_tiles);
     c.zero(misc + MISC_COUNTS, 8);
     c.zero(misc + MISC_LSCTR, 4);
     c.begin(KK_LEAFSCAN);
-    k_leafscan<<<grid_for(words, 2048), 256, 0, c.s>>>(words, w.cnt2, w.kw, w.sel_status, misc + MISC_LSCTR,
-                                                       misc + MISC_COUNTS);
+    k_leafscan<<<ls_tiles, 256, 0, c.s>>>(words, n_k, w.cnt2, w.kw, w.apre, w.sel_status, misc + MISC_LSCTR,
+                                         misc + MISC_COUNTS);
     c.launched();
     // V2: supervertex labels (vertex_map).  Runs before the host reads the
     // counts (one sync per level); on the final view its result is unused.
@@ -542,6 +545,8 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     if (direct) c.zero(mi_next, 8 * nv_next);
     EdgeSel es;
     es.cnt2 = w.cnt2;
+    es.kw = w.kw;
+    es.apre = w.apre;
     es.euv = euv_k;
     es.grank = grank_k;
     es.vm = vm;
@@ -551,16 +556,9 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     es.mi64_next = direct ? mi_next : nullptr;
     es.x1 = level == 0 ? w.x1 : nullptr;
     es.level = (int8_t)level;
-    {
-      const int64_t tiles = cdiv(n_k, SEL_TILE);
-      c.zero(w.sel_status, 4 * (tiles + 1));
-      c.zero(misc + MISC_SELCTR, 4);
-      c.zero(misc + MISC_SELTOT, 4);
-      c.begin(KK_SELECT_EDGES);
-      k_select<EdgeSel><<<(unsigned)tiles, SEL_BLOCK, 0, c.s>>>(n_k, w.sel_status, misc + MISC_SELCTR,
-                                                                misc + MISC_SELTOT, es);
-      c.launched();
-    }
+    c.begin(KK_SELECT_EDGES);
+    k_select_edges<<<c.persistent_grid(n_k, SEL_BLOCK * SEL_U, 8), SEL_BLOCK, 0, c.s>>>(n_k, es);
+    c.launched();
     v1_done = false;
     if (!direct && n_next > 0) {
       const int64_t m = 2 * n_next;

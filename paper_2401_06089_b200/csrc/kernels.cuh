@@ -10,8 +10,8 @@
 namespace dmst {
 
 constexpr int EW_BLOCK = 256;                  // elementwise kernels
-constexpr int SEL_BLOCK = 256, SEL_ITEMS = 8;  // select-scan tiles
-constexpr int SEL_TILE = SEL_BLOCK * SEL_ITEMS;
+constexpr int SEL_BLOCK = 256;                 // k_select_edges
+constexpr int LS_TILE = 2048;                  // k_leafscan words per tile
 constexpr int CHASE_FREE = 8;    // V2 chase steps before rulers may end a chase
 constexpr int CHASE_CAP = 512;   // hard bound on one V2 chase
 
@@ -177,56 +177,74 @@ __global__ void k_v1(int64_t nv, const unsigned long long* __restrict__ mi64,
   parent_out[x] = out;
 }
 
+// Exclusive prefixes of leaf-edge and alpha-edge counts per 16-edge word
+// (single pass, decoupled look-back: warp 0 resolves the leaf prefix, warp 1
+// the alpha prefix) + view totals (n_leaf, n_chain).  A supervertex is
+// numbered by the rank order of its component's leaf edge, so
+// label(leaf j) = kw[j >> 4].y + leaves below j in its word; an alpha edge's
+// slot in the next view is apre[j >> 4] + alphas below j in its word.  Both
+// are lookups into L2-resident arrays instead of scans.
+// kw[w] = (cnt2[w], exclusive count of leaf edges before edge 16w).
 __device__ __forceinline__ uint32_t leaf_bits(uint32_t w) { return (w >> 1) & 0x55555555u; }
 __device__ __forceinline__ uint32_t chain_bits(uint32_t w) { return w & 0x55555555u; }
+// one bit (at even positions) per edge whose 2-bit count is 0 and which exists (< ne)
+__device__ __forceinline__ uint32_t alpha_bits(uint32_t w, int64_t word, int64_t ne) {
+  uint32_t a = ~(w | (w >> 1)) & 0x55555555u;
+  const int64_t valid = ne - word * 16;
+  if (valid < 16) a &= valid <= 0 ? 0u : (1u << (2 * valid)) - 1u;
+  return a;
+}
 
-// Exclusive prefix of leaf-edge counts per 16-edge word (single pass,
-// decoupled look-back) + view totals (n_leaf, n_chain).  A supervertex is
-// numbered by the rank order of its component's leaf edge, so
-// label(leaf j) = kw[j >> 4].y + leaves below j in its word: a lookup
-// into two L2-resident arrays (n/4 bytes each) instead of a scan over
-// vertices and a gather.
-// kw[w] = (cnt2[w], exclusive count of leaf edges before edge 16w): one
-// 8-B lookup gives an edge's kind and its leaf ordinal (V2).
-__global__ void __launch_bounds__(256) k_leafscan(int64_t words, const uint32_t* __restrict__ cnt2,
-                                                  uint2* __restrict__ kw, uint32_t* __restrict__ status,
-                                                  uint32_t* __restrict__ tile_ctr, uint32_t* __restrict__ counts) {
+__global__ void __launch_bounds__(256) k_leafscan(int64_t words, int64_t ne, const uint32_t* __restrict__ cnt2,
+                                                  uint2* __restrict__ kw, uint32_t* __restrict__ apre,
+                                                  uint32_t* __restrict__ status, uint32_t* __restrict__ tile_ctr,
+                                                  uint32_t* __restrict__ counts) {
   constexpr int ITEMS = 8, TILE = 256 * ITEMS;
-  __shared__ uint32_t s_tile, s_excl;
+  __shared__ uint32_t s_tile, s_excl[2];
   __shared__ uint32_t scratch[256 / 32 + 1];
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
+  const uint32_t ntiles = gridDim.x;
   const int64_t base = (int64_t)tile * TILE + (int64_t)threadIdx.x * ITEMS;
-  uint32_t lc[ITEMS], cw[ITEMS], sum = 0, chains = 0;
+  uint32_t cw[ITEMS], lsum = 0, asum = 0, chains = 0;
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const uint32_t w = base + i < words ? cnt2[base + i] : 0u;
     cw[i] = w;
-    lc[i] = __popc(leaf_bits(w));
+    lsum += __popc(leaf_bits(w));
+    asum += __popc(alpha_bits(w, base + i, ne));
     chains += __popc(chain_bits(w));
-    sum += lc[i];
   }
-  uint32_t total;
-  uint32_t excl = block_excl_sum<256>(sum, scratch, &total);
-  if (threadIdx.x < 32) {
-    if (threadIdx.x == 0) st_relaxed(status + tile, (tile == 0 ? kFlagPrefix : kFlagAgg) | total);
-    const uint32_t prev = tile == 0 ? 0u : warp_lookback(status, tile);
-    if (threadIdx.x == 0) {
-      if (tile) st_relaxed(status + tile, kFlagPrefix | (prev + total));
-      s_excl = prev;
-      atomicAdd(counts + 0, total);
+  uint32_t ltot, atot, ctot;
+  const uint32_t lex = block_excl_sum<256>(lsum, scratch, &ltot);
+  const uint32_t aex = block_excl_sum<256>(asum, scratch, &atot);
+  block_excl_sum<256>(chains, scratch, &ctot);
+  const uint32_t warp = threadIdx.x >> 5;
+  if (warp < 2) {
+    uint32_t* st = status + warp * ntiles;
+    const uint32_t tot = warp == 0 ? ltot : atot;
+    if (lane_id() == 0) st_relaxed(st + tile, (tile == 0 ? kFlagPrefix : kFlagAgg) | tot);
+    const uint32_t prev = tile == 0 ? 0u : warp_lookback(st, tile);
+    if (lane_id() == 0) {
+      if (tile) st_relaxed(st + tile, kFlagPrefix | (prev + tot));
+      s_excl[warp] = prev;
     }
   }
-  uint32_t ctot;
-  block_excl_sum<256>(chains, scratch, &ctot);
-  if (threadIdx.x == 0) atomicAdd(counts + 1, ctot);
+  if (threadIdx.x == 0) {
+    atomicAdd(counts + 0, ltot);
+    atomicAdd(counts + 1, ctot);
+  }
   __syncthreads();
-  uint32_t run = s_excl + excl;
+  uint32_t lrun = s_excl[0] + lex, arun = s_excl[1] + aex;
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
-    if (base + i < words) kw[base + i] = make_uint2(cw[i], run);
-    run += lc[i];
+    if (base + i < words) {
+      kw[base + i] = make_uint2(cw[i], lrun);
+      apre[base + i] = arun;
+    }
+    lrun += __popc(leaf_bits(cw[i]));
+    arun += __popc(alpha_bits(cw[i], base + i, ne));
   }
 }
 
@@ -309,70 +327,18 @@ __global__ void k_jump(const int32_t* __restrict__ in, const uint32_t* __restric
   }
 }
 
-// Order-preserving select: single pass, decoupled look-back over tiles.
-// Items are warp-striped (coalesced); rank order = index order.
-template <class Sel>
-__global__ void __launch_bounds__(SEL_BLOCK)
-k_select(int64_t n, uint32_t* __restrict__ status, uint32_t* __restrict__ tile_ctr,
-         uint32_t* __restrict__ totals, Sel sel) {
-  constexpr int NW = SEL_BLOCK / 32;
-  __shared__ uint32_t s_tile;
-  __shared__ uint32_t s_warp[NW + 1];
-  __shared__ uint32_t s_excl;
-  __shared__ typename Sel::Shared s_sel;
-  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
-  sel.init_shared(s_sel);
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  const int64_t wbase = (int64_t)tile * SEL_TILE + (int64_t)warp * SEL_ITEMS * 32 + lane;
-  const uint32_t lt = lanemask_lt();
-
-  typename Sel::Item it[SEL_ITEMS];
-  uint32_t wpos[SEL_ITEMS];
-  bool flag[SEL_ITEMS];
-  uint32_t run = 0;
-#pragma unroll
-  for (int i = 0; i < SEL_ITEMS; ++i) {
-    int64_t idx = wbase + (int64_t)i * 32;
-    flag[i] = idx < n ? sel.flag(idx, it[i]) : false;
-    uint32_t b = __ballot_sync(kFull, flag[i]);
-    wpos[i] = run + __popc(b & lt);
-    run += __popc(b);
-  }
-  if (lane == 0) s_warp[warp] = run;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t c = lane < NW ? s_warp[lane] : 0;
-    uint32_t incl = warp_incl_sum(c);
-    if (lane < NW) s_warp[lane] = incl - c;
-    uint32_t total = __shfl_sync(kFull, incl, NW - 1);
-    if (lane == 0) st_relaxed(status + tile, (tile == 0 ? kFlagPrefix : kFlagAgg) | total);
-    const uint32_t excl = tile == 0 ? 0u : warp_lookback(status, tile);
-    if (lane == 0) {
-      if (tile) st_relaxed(status + tile, kFlagPrefix | (excl + total));
-      s_excl = excl;
-      if (tile == gridDim.x - 1) totals[0] = excl + total;
-    }
-  }
-  __syncthreads();
-  const uint32_t base = s_excl + s_warp[warp];
-#pragma unroll
-  for (int i = 0; i < SEL_ITEMS; ++i) {
-    int64_t idx = wbase + (int64_t)i * 32;
-    if (idx < n) sel.emit(idx, flag[i], base + wpos[i], it[i], s_sel);
-  }
-  __syncthreads();
-  sel.flush_shared(s_sel);
-}
-
 // Retire non-alpha edges of view k at level k (contraction.py:207) and
 // compact alpha edges, in rank order, into view k+1 with endpoints remapped
-// to supervertices (:170-172).  The next view's maxIncident is either
-// scatter-maxed directly (small views) or bucketed afterwards from euv_next
-// (multisplit + apply path, bucket.cuh).
+// to supervertices (:170-172).  An alpha edge's slot comes from the alpha
+// prefix of its 16-edge word (k_leafscan), so this is a plain elementwise
+// pass with no inter-CTA scan.  The next view's maxIncident is scatter-maxed
+// here for small views (L2-resident), else bucketed afterwards from
+// euv_next (bucket.cuh).  View 0 also writes x1[j] = view-1 supervertex of
+// every edge (the chain walk's starting point).
 struct EdgeSel {
-  uint32_t* __restrict__ cnt2;       // read, then zeroed for the next view
+  uint32_t* __restrict__ cnt2;       // zeroed for the next view
+  const uint2* __restrict__ kw;      // (child counts, leaf prefix) per 16 edges
+  const uint32_t* __restrict__ apre; // alpha prefix per 16 edges
   const int2* __restrict__ euv;
   const int32_t* __restrict__ grank; // null => identity (view 0)
   const int32_t* __restrict__ vm;
@@ -380,41 +346,59 @@ struct EdgeSel {
   int2* __restrict__ euv_next;
   int32_t* __restrict__ grank_next;
   unsigned long long* __restrict__ mi64_next;  // direct mode (null => bucketed from euv_next)
-  int32_t* __restrict__ x1;          // view 0 only: view-1 supervertex of every edge (walk start)
+  int32_t* __restrict__ x1;          // view 0 only
   int8_t level;
-  struct Item {
-    int32_t g;
-  };
-  struct Shared {};
-  __device__ __forceinline__ void init_shared(Shared&) const {}
-  __device__ __forceinline__ void flush_shared(Shared&) const {}
-  __device__ __forceinline__ bool flag(int64_t j, Item& it) const {
-    const uint32_t c = (cnt2[j >> 4] >> ((j & 15) * 2)) & 3u;
-    it.g = grank ? __ldcs(grank + j) : (int32_t)j;
-    return c == 0;
-  }
-  __device__ __forceinline__ void emit(int64_t j, bool alpha, uint32_t pos, const Item& it, Shared&) const {
-    if ((j & 15) == 0) cnt2[j >> 4] = 0u;
-    int2 e = make_int2(0, 0);
-    int32_t a = 0;
-    if (alpha || x1) {
-      e = __ldcs(euv + j);
-      a = vm[e.x];
+};
+
+constexpr int SEL_U = 4;  // edges per thread per iteration (gathers in flight together)
+__global__ void __launch_bounds__(SEL_BLOCK) k_select_edges(int64_t n, EdgeSel es) {
+  const int64_t stride = (int64_t)gridDim.x * SEL_BLOCK * SEL_U;
+  for (int64_t b0 = (int64_t)blockIdx.x * SEL_BLOCK * SEL_U + threadIdx.x; b0 < n; b0 += stride) {
+    bool alpha[SEL_U], in[SEL_U], need[SEL_U];
+    int32_t lab[SEL_U], g[SEL_U];
+    uint32_t pos[SEL_U];
+    int2 e[SEL_U];
+#pragma unroll
+    for (int q = 0; q < SEL_U; ++q) {
+      const int64_t j = b0 + (int64_t)q * SEL_BLOCK;
+      in[q] = j < n;
+      const uint2 w = in[q] ? es.kw[j >> 4] : make_uint2(0, 0);
+      const uint32_t sh = (uint32_t)(j & 15) * 2;
+      const uint32_t c = (w.x >> sh) & 3u;
+      alpha[q] = in[q] && c == 0u;
+      lab[q] = c == 2u ? (int32_t)leaf_label(w, (uint32_t)j) : -1;
+      pos[q] = alpha[q] ? es.apre[j >> 4] + __popc(alpha_bits(w.x, 0, 16) & ((1u << sh) - 1u)) : 0u;
+      g[q] = in[q] ? (es.grank ? __ldcs(es.grank + j) : (int32_t)j) : 0;
+      need[q] = alpha[q] || (in[q] && es.x1 != nullptr && lab[q] < 0);
+      e[q] = need[q] ? __ldcs(es.euv + j) : make_int2(0, 0);
+      if (in[q] && (j & 15) == 0) es.cnt2[j >> 4] = 0u;
     }
-    if (x1) __stcs(x1 + j, a);
-    if (!alpha) {
-      ret[it.g] = level;
-    } else {
-      const int32_t b = vm[e.y];
-      __stcs(euv_next + pos, make_int2(a, b));
-      __stcs(grank_next + pos, it.g);
-      if (mi64_next) {
-        atomicMax(mi64_next + a, pack_mi(pos + 1u, (uint32_t)b));
-        atomicMax(mi64_next + b, pack_mi(pos + 1u, (uint32_t)a));
+    int32_t a[SEL_U], bb[SEL_U];
+#pragma unroll
+    for (int q = 0; q < SEL_U; ++q) {
+      a[q] = need[q] ? es.vm[e[q].x] : lab[q];
+      bb[q] = alpha[q] ? es.vm[e[q].y] : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < SEL_U; ++q) {
+      if (!in[q]) continue;
+      const int64_t j = b0 + (int64_t)q * SEL_BLOCK;
+      // a leaf edge's component is labelled by the edge itself; a chain or
+      // alpha edge's by its first endpoint
+      if (es.x1) __stcs(es.x1 + j, a[q]);
+      if (!alpha[q]) {
+        es.ret[g[q]] = es.level;
+      } else {
+        __stcs(es.euv_next + pos[q], make_int2(a[q], bb[q]));
+        __stcs(es.grank_next + pos[q], g[q]);
+        if (es.mi64_next) {
+          atomicMax(es.mi64_next + a[q], pack_mi(pos[q] + 1u, (uint32_t)bb[q]));
+          atomicMax(es.mi64_next + bb[q], pack_mi(pos[q] + 1u, (uint32_t)a[q]));
+        }
       }
     }
   }
-};
+}
 
 // Final view (no alpha edges, contraction.py:203-205): every edge retires at L.
 __global__ void k_retire_all(int64_t n, const int32_t* __restrict__ grank, int8_t* __restrict__ ret, int8_t L) {

@@ -37,7 +37,7 @@ namespace dmst {
 // Edge sort: u64 key + 3-word payload.
 constexpr int S1_BLOCK = 512, S1_ITEMS = 8, S1_MINB = 1;
 // Chain sort: u32 key + 1-word payload.
-constexpr int S2_BLOCK = 512, S2_ITEMS = 16, S2_MINB = 1, S2_BITS = 8;  // 9-bit digits measured slower (shorter runs)
+constexpr int S2_BLOCK = 512, S2_ITEMS = 16, S2_MINB = 1, S2_BITS = 9;
 constexpr int64_t kDirectMiBytes = 24ll << 20;  // direct scatter-max below this mi64 size
 
 enum KernelKind {

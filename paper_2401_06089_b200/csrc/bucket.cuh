@@ -22,37 +22,42 @@ constexpr int BKA_BLOCK = 512, BKA_ITEMS = 8;   // 4096 records per sub-tile
 constexpr int BKB_BLOCK = 512, BKB_ITEMS = 4;   // 2048 records per sub-tile
 constexpr int BKB_SPAN = 1024;                  // max fine buckets a pass-B sub-tile may touch
 
-// Records are AoS triples (vertex, j + 1, other end): a bucket run of m
-// records is one contiguous run of 12 m bytes.
+// Records are AoS tuples of RW words whose first word is the bucketing key
+// (maxIncident: (vertex, j + 1, other end), RW = 3; chain links: (rank,
+// parent), RW = 2): a bucket run of m records is one contiguous run of
+// 4 RW m bytes.
 struct Recs {
-  uint32_t* r;  // [3 m]
+  uint32_t* r;  // [RW m]
 };
 
-// Record i of edge i >> 1 of a view (endpoints euv).  Sources also describe
-// their staged form (SB bytes per record, contiguous from base()) so
-// sub-tiles can be fetched with TMA bulk copies.
+// Record sources.  Besides global loads (load / vertex) a source describes
+// its staged form: NS streams of sb(s) bytes per record, contiguous from
+// ptr(s), fetched per sub-tile with TMA bulk copies; get() / staged_vertex()
+// then read the stage (st[s] = stream s of the sub-tile).
+//
+// Record i of edge i >> 1 of a view (endpoints euv).
 struct EdgeRecSrc {
-  static constexpr int SB = 4;  // 8 B per edge = 2 records
+  static constexpr int RW = 3, NS = 1;
+  __host__ __device__ static constexpr int sb(int) { return 4; }  // 8 B per edge = 2 records
   const int2* __restrict__ euv;
-  __device__ __forceinline__ const void* base() const { return euv; }
-  __device__ __forceinline__ void get(const unsigned char* stage, int li, int64_t i, uint32_t& x, uint32_t& j1,
-                                      uint32_t& o) const {
-    const int2 e = reinterpret_cast<const int2*>(stage)[li >> 1];
+  __device__ __forceinline__ const void* ptr(int) const { return euv; }
+  __device__ __forceinline__ void get(const unsigned char* const* st, int li, int64_t i, uint32_t (&r)[3]) const {
+    const int2 e = reinterpret_cast<const int2*>(st[0])[li >> 1];
     const bool second = i & 1;
-    x = (uint32_t)(second ? e.y : e.x);
-    o = (uint32_t)(second ? e.x : e.y);
-    j1 = (uint32_t)(i >> 1) + 1u;
+    r[0] = (uint32_t)(second ? e.y : e.x);
+    r[2] = (uint32_t)(second ? e.x : e.y);
+    r[1] = (uint32_t)(i >> 1) + 1u;
   }
-  __device__ __forceinline__ uint32_t staged_vertex(const unsigned char* stage, int li, int64_t i) const {
-    const int2 e = reinterpret_cast<const int2*>(stage)[li >> 1];
+  __device__ __forceinline__ uint32_t staged_vertex(const unsigned char* const* st, int li, int64_t i) const {
+    const int2 e = reinterpret_cast<const int2*>(st[0])[li >> 1];
     return (uint32_t)((i & 1) ? e.y : e.x);
   }
-  __device__ __forceinline__ void load(int64_t i, uint32_t& x, uint32_t& j1, uint32_t& o) const {
+  __device__ __forceinline__ void load(int64_t i, uint32_t (&r)[3]) const {
     const int2 e = __ldg(euv + (i >> 1));
     const bool second = i & 1;
-    x = (uint32_t)(second ? e.y : e.x);
-    o = (uint32_t)(second ? e.x : e.y);
-    j1 = (uint32_t)(i >> 1) + 1u;
+    r[0] = (uint32_t)(second ? e.y : e.x);
+    r[2] = (uint32_t)(second ? e.x : e.y);
+    r[1] = (uint32_t)(i >> 1) + 1u;
   }
   __device__ __forceinline__ uint32_t vertex(int64_t i) const {
     const int2 e = __ldg(euv + (i >> 1));
@@ -60,26 +65,26 @@ struct EdgeRecSrc {
   }
 };
 
+// Materialised records (RW words each).
+template <int RW_>
 struct AosRecSrc {
-  static constexpr int SB = 12;
+  static constexpr int RW = RW_, NS = 1;
+  __host__ __device__ static constexpr int sb(int) { return 4 * RW; }
   const uint32_t* __restrict__ r;
-  __device__ __forceinline__ const void* base() const { return r; }
-  __device__ __forceinline__ void get(const unsigned char* stage, int li, int64_t, uint32_t& x, uint32_t& j1,
-                                      uint32_t& o) const {
-    const uint32_t* p = reinterpret_cast<const uint32_t*>(stage) + 3 * li;
-    x = p[0];
-    j1 = p[1];
-    o = p[2];
+  __device__ __forceinline__ const void* ptr(int) const { return r; }
+  __device__ __forceinline__ void get(const unsigned char* const* st, int li, int64_t, uint32_t (&o)[RW]) const {
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(st[0]) + RW * li;
+#pragma unroll
+    for (int q = 0; q < RW; ++q) o[q] = p[q];
   }
-  __device__ __forceinline__ uint32_t staged_vertex(const unsigned char* stage, int li, int64_t) const {
-    return reinterpret_cast<const uint32_t*>(stage)[3 * li];
+  __device__ __forceinline__ uint32_t staged_vertex(const unsigned char* const* st, int li, int64_t) const {
+    return reinterpret_cast<const uint32_t*>(st[0])[RW * li];
   }
-  __device__ __forceinline__ void load(int64_t i, uint32_t& xx, uint32_t& jj, uint32_t& oo) const {
-    xx = ld_stream(r + 3 * i);
-    jj = ld_stream(r + 3 * i + 1);
-    oo = ld_stream(r + 3 * i + 2);
+  __device__ __forceinline__ void load(int64_t i, uint32_t (&o)[RW]) const {
+#pragma unroll
+    for (int q = 0; q < RW; ++q) o[q] = ld_stream(r + RW * i + q);
   }
-  __device__ __forceinline__ uint32_t vertex(int64_t i) const { return __ldg(r + 3 * i); }
+  __device__ __forceinline__ uint32_t vertex(int64_t i) const { return __ldg(r + RW * i); }
 };
 
 // counts[f] += number of records whose vertex is in fine bucket f, for
@@ -147,9 +152,15 @@ __global__ void __launch_bounds__(1024) k_fine_scan(const uint32_t* __restrict__
 template <class Src, int BLOCK, int ITEMS, int NC>
 struct SplitSmem {
   static constexpr int T = BLOCK * ITEMS;
-  __host__ __device__ static constexpr size_t in_bytes() { return ((size_t)T * Src::SB + 127) & ~size_t(127); }
+  __host__ __device__ static constexpr size_t stream_bytes(int s) { return ((size_t)T * Src::sb(s) + 127) & ~size_t(127); }
+  __host__ __device__ static constexpr size_t stream_off(int s) {
+    size_t b = 0;
+    for (int q = 0; q < s; ++q) b += stream_bytes(q);
+    return b;
+  }
+  __host__ __device__ static constexpr size_t in_bytes() { return stream_off(Src::NS); }
   __host__ __device__ static constexpr size_t off_st() { return 2 * in_bytes(); }
-  __host__ __device__ static constexpr size_t off_cnt() { return off_st() + 12 * (size_t)T; }
+  __host__ __device__ static constexpr size_t off_cnt() { return off_st() + 4 * Src::RW * (size_t)T; }
   __host__ __device__ static constexpr size_t bytes() { return off_cnt() + 8 * (size_t)NC; }
 };
 
@@ -157,9 +168,9 @@ template <bool FINE, class Src, int BLOCK, int ITEMS, int NC>
 __global__ void __launch_bounds__(BLOCK) k_split(Src src, int64_t m, uint32_t gshift,
                                                  uint32_t* __restrict__ cursor, Recs out) {
   using S = SplitSmem<Src, BLOCK, ITEMS, NC>;
-  constexpr int T = S::T;
+  constexpr int T = S::T, RW = Src::RW, NS = Src::NS;
   extern __shared__ __align__(128) unsigned char sm[];
-  uint32_t* st = reinterpret_cast<uint32_t*>(sm + S::off_st());    // [3 T] grouped records
+  uint32_t* st = reinterpret_cast<uint32_t*>(sm + S::off_st());    // [RW T] grouped records
   uint32_t* cnt = reinterpret_cast<uint32_t*>(sm + S::off_cnt());  // [NC]
   uint32_t* gofs = cnt + NC;                                       // [NC]
   __shared__ uint32_t scratch[BLOCK / 32 + 1];
@@ -167,14 +178,22 @@ __global__ void __launch_bounds__(BLOCK) k_split(Src src, int64_t m, uint32_t gs
   __shared__ __align__(8) uint64_t bar[2];
   const uint32_t tid = threadIdx.x;
   const int64_t ntiles = (m + T - 1) / T;
-  const bool tma = aligned16(src.base());
+  bool tma = true;
+#pragma unroll
+  for (int q = 0; q < NS; ++q) tma &= aligned16(src.ptr(q));
 
   auto issue = [&](int64_t tile, int buf) {
     const int64_t t0 = tile * T;
     if (!tma || tile >= ntiles || t0 + T > m) return;
     fence_proxy_async();
-    mbar_expect_tx(&bar[buf], (uint32_t)(T * Src::SB));
-    bulk_g2s(sm + buf * S::in_bytes(), (const char*)src.base() + t0 * Src::SB, (uint32_t)(T * Src::SB), &bar[buf]);
+    uint32_t bytes = 0;
+#pragma unroll
+    for (int q = 0; q < NS; ++q) bytes += (uint32_t)(T * Src::sb(q));
+    mbar_expect_tx(&bar[buf], bytes);
+#pragma unroll
+    for (int q = 0; q < NS; ++q)
+      bulk_g2s(sm + buf * S::in_bytes() + S::stream_off(q), (const char*)src.ptr(q) + t0 * Src::sb(q),
+               (uint32_t)(T * Src::sb(q)), &bar[buf]);
   };
   if (tid == 0) {
     mbar_init(&bar[0], 1);
@@ -190,16 +209,18 @@ __global__ void __launch_bounds__(BLOCK) k_split(Src src, int64_t m, uint32_t gs
   int k = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
     const int buf = k & 1;
-    const unsigned char* stage = sm + buf * S::in_bytes();
+    const unsigned char* stage[NS];
+#pragma unroll
+    for (int q = 0; q < NS; ++q) stage[q] = sm + buf * S::in_bytes() + S::stream_off(q);
     const int64_t t0 = tile * T;
     const int count = m - t0 < T ? (int)(m - t0) : T;
     const bool staged = tma && count == T;
     if (staged) mbar_wait(&bar[buf], (uint32_t)(k >> 1) & 1u);
-    auto rec = [&](int li, uint32_t& x, uint32_t& j1, uint32_t& o) {
+    auto rec = [&](int li, uint32_t (&r)[RW]) {
       if (staged)
-        src.get(stage, li, t0 + li, x, j1, o);
+        src.get(stage, li, t0 + li, r);
       else
-        src.load(t0 + li, x, j1, o);
+        src.load(t0 + li, r);
     };
     auto vtx = [&](int li) { return staged ? src.staged_vertex(stage, li, t0 + li) : src.vertex(t0 + li); };
     if (tid == 0) {
@@ -220,12 +241,11 @@ __global__ void __launch_bounds__(BLOCK) k_split(Src src, int64_t m, uint32_t gs
       // rare: a sub-tile spanning more fine buckets than the shared counters
       // hold (heavily skewed vertex ids) -> one global atomic per record
       for (int li = tid; li < count; li += BLOCK) {
-        uint32_t x, j1, o;
-        rec(li, x, j1, o);
-        const uint64_t d = atomicAdd(cursor + (x >> FB_BITS), 1u);
-        out.r[3 * d] = x;
-        out.r[3 * d + 1] = j1;
-        out.r[3 * d + 2] = o;
+        uint32_t r[RW];
+        rec(li, r);
+        const uint64_t d = atomicAdd(cursor + (r[0] >> FB_BITS), 1u);
+#pragma unroll
+        for (int q = 0; q < RW; ++q) out.r[RW * d + q] = r[q];
       }
       __syncthreads();
       if (tid == 0) issue(tile + 2 * (int64_t)gridDim.x, buf);
@@ -265,19 +285,18 @@ __global__ void __launch_bounds__(BLOCK) k_split(Src src, int64_t m, uint32_t gs
     for (int i = 0; i < ITEMS; ++i) {
       const int li = i * BLOCK + tid;
       if (li < count) {
-        uint32_t x, j1, o;
-        rec(li, x, j1, o);
-        const uint32_t p = cnt[bucket(x)] + slot[i];
-        st[3 * p] = x;
-        st[3 * p + 1] = j1;
-        st[3 * p + 2] = o;
+        uint32_t r[RW];
+        rec(li, r);
+        const uint32_t p = cnt[bucket(r[0])] + slot[i];
+#pragma unroll
+        for (int q = 0; q < RW; ++q) st[RW * p + q] = r[q];
       }
     }
     __syncthreads();
     if (tid == 0) issue(tile + 2 * (int64_t)gridDim.x, buf);  // stage buffer consumed
-    for (int s_ = tid; s_ < 3 * count; s_ += BLOCK) {
-      const int it = s_ / 3;
-      out.r[3 * (uint64_t)gofs[bucket(st[3 * it])] + s_] = st[s_];
+    for (int s_ = tid; s_ < RW * count; s_ += BLOCK) {
+      const int it = s_ / RW;
+      out.r[RW * (uint64_t)gofs[bucket(st[RW * it])] + s_] = st[s_];
     }
     __syncthreads();
   }

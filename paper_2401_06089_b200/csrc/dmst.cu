@@ -103,7 +103,7 @@ struct Workspace {
 
 constexpr int kSmallWords = 8 * kRadix /*hist1*/ + 8 * kRadix /*gbase1*/ + 4 * kRadix /*hist2*/ +
                             4 * kRadix /*gbase2*/ + kRadix /*vhist*/ + kRadix /*vbase*/ + 64 /*tile ctrs*/ +
-                            64 /*misc*/;
+                            256 /*misc*/;
 constexpr int SM_HIST1 = 0, SM_GBASE1 = SM_HIST1 + 8 * kRadix, SM_HIST2 = SM_GBASE1 + 8 * kRadix,  // NOLINT
               SM_GBASE2 = SM_HIST2 + 4 * kRadix, SM_VHIST = SM_GBASE2 + 4 * kRadix,
               SM_VBASE = SM_VHIST + kRadix, SM_TILECTR = SM_VBASE + kRadix, SM_MISC = SM_TILECTR + 64;
@@ -296,8 +296,8 @@ struct Ctx {
 
 // One radix pass: upsweep (per-chunk digit counts), chunk scan, downsweep.
 template <typename K, int PW, int BLOCK, int ITEMS, int MINB, int BITS, class Loader, class Emitter>
-void radix_pass(Ctx& c, int kind, int64_t n, int shift, Loader ld, Emitter em) {
-  using S = DownSmem<K, PW, BLOCK, ITEMS, Loader, BITS>;
+int64_t radix_pass(Ctx& c, int kind, int64_t n, int shift, Loader ld, Emitter em) {
+  using S = DownSmem<K, PW, BLOCK, ITEMS, Loader, Emitter, BITS>;
   constexpr int T = S::T;
   auto kern = k_downsweep<K, PW, BLOCK, ITEMS, MINB, Loader, Emitter, BITS>;
   DMST_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes()));
@@ -320,34 +320,37 @@ void radix_pass(Ctx& c, int kind, int64_t n, int shift, Loader ld, Emitter em) {
   c.begin(kind);
   kern<<<(unsigned)G, BLOCK, S::bytes(), c.s>>>(a, ld, em);
   c.launched();
+  return G;
 }
 
 // Multi-pass driver over the non-constant digits (bit offsets `shifts`).
 // Ping-pong buffers: keys bufK[2], AoS payload bufP[2] (PW words per item);
 // first/last passes use the given loader/emitter.
 template <typename K, int PW, int BLOCK, int ITEMS, int MINB, int BITS, class FirstLoader, class FinalEmitter>
-void run_sort(Ctx& c, const int (&kinds)[3], int64_t n, const std::vector<int>& shifts,
+int64_t run_sort(Ctx& c, const int (&kinds)[3], int64_t n, const std::vector<int>& shifts,
               K* const (&bufK)[2], uint32_t* const (&bufP)[2], FirstLoader first, FinalEmitter final_em) {
   const int P = (int)shifts.size();
   if (P == 0) {
     c.begin(KK_OTHER);
     k_identity_pass<K, PW, EW_BLOCK><<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(n, first, final_em);
     c.launched();
-    return;
+    return grid_for(n, EW_BLOCK);
   }
+  int64_t G = 0;
   for (int p = 0; p < P; ++p) {
     const int o = p % 2, in = o ^ 1;
     ArrayEmitter<K, PW> mid{bufK[o], bufP[o]};
     ArrayLoader<K, PW> ldr{bufK[in], bufP[in]};
     if (P == 1)
-      radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[2], n, shifts[p], first, final_em);
+      G = radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[2], n, shifts[p], first, final_em);
     else if (p == 0)
-      radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[0], n, shifts[p], first, mid);
+      G = radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[0], n, shifts[p], first, mid);
     else if (p == P - 1)
-      radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[2], n, shifts[p], ldr, final_em);
+      G = radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[2], n, shifts[p], ldr, final_em);
     else
-      radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[1], n, shifts[p], ldr, mid);
+      G = radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[1], n, shifts[p], ldr, mid);
   }
+  return G;
 }
 
 // Radix digits (BITS wide, at bit offsets 0, BITS, ...) that are not
@@ -395,13 +398,18 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
 // order-free multisplit passes (coarse, fine) and the per-bucket shared-memory
 // reduction, which also performs V1 for the view.  `in`/`mid`/`fin` are
 // record buffers (mid and fin must not overlap the source).
+// coarse bucket = 2^gshift fine buckets: about sqrt(nf) coarse buckets (at
+// most 256) so both multisplit passes write runs of similar length
+uint32_t coarse_shift(uint32_t nf) {
+  uint32_t gshift = 0;
+  while ((int64_t(nf) >> gshift) > 255 || (int64_t(nf) >> gshift) > (1ll << (gshift + 1))) ++gshift;
+  return gshift;
+}
+
 template <class Src>
 void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiApplyOut out) {
   const uint32_t nf = (uint32_t)cdiv(nv, FB);
-  // coarse bucket = 2^gshift fine buckets, about sqrt(nf) coarse buckets so
-  // both passes write runs of similar length
-  uint32_t gshift = 0;
-  while ((int64_t(nf) >> gshift) > 255 || (int64_t(nf) >> gshift) > (1ll << (gshift + 1))) ++gshift;
+  const uint32_t gshift = coarse_shift(nf);
   uint32_t* counts = c.w.fine;
   uint32_t* fine_base = counts + (nf + 2);
   uint32_t* fine_cur = fine_base + (nf + 2);
@@ -417,16 +425,16 @@ void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiAp
   k_fine_scan<<<1, 1024, 0, c.s>>>(counts, nf, gshift, fine_base, fine_cur, coarse_cur);
   c.launched();
   using SA = SplitSmem<Src, BKA_BLOCK, BKA_ITEMS, 256>;
-  using SB = SplitSmem<AosRecSrc, BKB_BLOCK, BKB_ITEMS, BKB_SPAN>;
+  using SB = SplitSmem<AosRecSrc<3>, BKB_BLOCK, BKB_ITEMS, BKB_SPAN>;
   auto kA = k_split<false, Src, BKA_BLOCK, BKA_ITEMS, 256>;
-  auto kB = k_split<true, AosRecSrc, BKB_BLOCK, BKB_ITEMS, BKB_SPAN>;
+  auto kB = k_split<true, AosRecSrc<3>, BKB_BLOCK, BKB_ITEMS, BKB_SPAN>;
   DMST_CUDA(cudaFuncSetAttribute(kA, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SA::bytes()));
   DMST_CUDA(cudaFuncSetAttribute(kB, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SB::bytes()));
   c.begin(KK_MI_SPLIT);
   kA<<<c.persistent_grid(m, SA::T, 2), BKA_BLOCK, SA::bytes(), c.s>>>(src, m, gshift, coarse_cur, mid);
   c.launched();
   c.begin(KK_MI_SPLIT);
-  kB<<<c.persistent_grid(m, SB::T, 2), BKB_BLOCK, SB::bytes(), c.s>>>(AosRecSrc{mid.r}, m, gshift, fine_cur, fin);
+  kB<<<c.persistent_grid(m, SB::T, 2), BKB_BLOCK, SB::bytes(), c.s>>>(AosRecSrc<3>{mid.r}, m, gshift, fine_cur, fin);
   c.launched();
   DMST_CUDA(cudaFuncSetAttribute(k_mi_apply_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * FB));  // 64 KB
   c.begin(KK_MI_APPLY);
@@ -603,23 +611,47 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
   c.sync();
   const std::vector<int> shifts = active_digits(kao[0], kao[1], S2_BITS, 32);
   if (st) st->sort2_passes = (int)shifts.size();
-  // chain sort: keys at R[0, 4n); ping-pong A = R[4n, 12n), B = R[12n, 20n)
-  const uint32_t* skeys = keys;
-  const uint32_t* svals = nullptr;
-  if (!shifts.empty()) {
+  // chain sort: keys at R[0, 4n); ping-pong A = R[4n, 12n), B = R[12n, 20n);
+  if (shifts.empty()) {  // one chain (all keys equal): rank order is chain order
+    c.begin(KK_LINK);
+    k_link<<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(n, keys, nullptr, w.smi_all, edge_parent);
+    c.launched();
+  } else {
     uint32_t* base = (uint32_t*)w.R;
     uint32_t* const bufK[2] = {base + n, base + 3 * n};
     uint32_t* const bufP[2] = {base + 2 * n, base + 4 * n};
     const int lastb = ((int)shifts.size() - 1) % 2;
     ArrayEmitter<uint32_t, 1> fin{bufK[lastb], bufP[lastb]};
     run_sort<uint32_t, 1, S2_BLOCK, S2_ITEMS, S2_MINB, S2_BITS>(c, {KK_SORT2_PASS, KK_SORT2_PASS, KK_SORT2_PASS}, n,
-                                                       shifts, bufK, bufP, Sort2FirstLoader{keys}, fin);
-    skeys = fin.keys;
-    svals = fin.pay;
+                                                             shifts, bufK, bufP, Sort2FirstLoader{keys}, fin);
+    // (rank, parent) records grouped by 8192-rank window: R[20n, 28n) -> R[28n, 36n)
+    uint32_t* recA = (uint32_t*)(w.R + align_up(20 * n));
+    uint32_t* recB = (uint32_t*)(w.R + align_up(28 * n));
+    const uint32_t nf = (uint32_t)cdiv(n, FB), gshift = coarse_shift(nf);
+    const uint32_t nc = (uint32_t)cdiv(nf, 1u << gshift);
+    uint32_t* fine_cur = w.fine;
+    uint32_t* coarse_cur = w.fine + (nf + 2);
+    c.begin(KK_LINK);
+    k_link_cursors<<<grid_for(nf, EW_BLOCK), EW_BLOCK, 0, c.s>>>(coarse_cur, nc, fine_cur, nf, gshift);
+    c.launched();
+    using LA = SplitSmem<LinkSortedSrc, BKA_BLOCK, BKA_ITEMS, 256>;
+    using LB = SplitSmem<AosRecSrc<2>, BKB_BLOCK, BKB_ITEMS, BKB_SPAN>;
+    auto kA = k_split<false, LinkSortedSrc, BKA_BLOCK, BKA_ITEMS, 256>;
+    auto kB = k_split<true, AosRecSrc<2>, BKB_BLOCK, BKB_ITEMS, BKB_SPAN>;
+    DMST_CUDA(cudaFuncSetAttribute(kA, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LA::bytes()));
+    DMST_CUDA(cudaFuncSetAttribute(kB, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LB::bytes()));
+    c.begin(KK_LINK);
+    kA<<<c.persistent_grid(n, LA::T, 2), BKA_BLOCK, LA::bytes(), c.s>>>(
+        LinkSortedSrc{fin.keys, fin.pay, w.smi_all}, n, gshift, coarse_cur, Recs{recA});
+    c.launched();
+    c.begin(KK_LINK);
+    kB<<<c.persistent_grid(n, LB::T, 2), BKB_BLOCK, LB::bytes(), c.s>>>(AosRecSrc<2>{recA}, n, gshift, fine_cur,
+                                                                        Recs{recB});
+    c.launched();
+    c.begin(KK_LINK);
+    k_link_apply<<<nf, 512, 0, c.s>>>((const uint2*)recB, n, edge_parent);
+    c.launched();
   }
-  c.begin(KK_LINK);
-  k_link<<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(n, skeys, svals, w.smi_all, edge_parent);
-  c.launched();
 }
 
 template <class F>

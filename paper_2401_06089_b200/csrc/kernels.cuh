@@ -100,13 +100,18 @@ struct Sort1FirstLoader {
 // Final pass: RankedTree outputs (orig_of, w by rank) + rank-order endpoints,
 // written from the sorted sub-tile (payload = (original id, u, v)).
 struct Sort1FinalEmitter {
+  using State = NoEmitState;
+  template <int BLOCK, int R>
+  __device__ __forceinline__ void init(State&) const {}
+  template <int BLOCK, int R>
+  __device__ __forceinline__ void finish(State&) const {}
   int32_t* __restrict__ orig_of;
   double* __restrict__ heights;
   int2* __restrict__ euv;        // rank-order endpoints (pipeline)
   int32_t* __restrict__ ru;      // optional split copies (dmst_rank_edges)
   int32_t* __restrict__ rv;
   template <int BLOCK, class Tile>
-  __device__ __forceinline__ void emit(const Tile& t) const {
+  __device__ __forceinline__ void emit(const Tile& t, State&) const {
     for (int s = threadIdx.x; s < t.cnt; s += BLOCK) {
       const uint64_t k = t.skeys[s];
       const uint32_t r = t.gofs[digit_of<kRadixBits>(k, t.shift)] + (uint32_t)s;
@@ -479,7 +484,73 @@ struct Sort2FirstLoader {
 };
 
 // stitch_chains (expansion.py:131-145): in (key, rank) order the parent of
-// an edge is its predecessor in the same chain, or the chain's terminal.
+// an edge is its predecessor in the same chain, or the chain's terminal
+// (-1 = ROOT for the root chain, key 0).  Writing edge_parent[e] straight
+// from chain order is a random 4-B store per edge (~1.3 ms per 128M even
+// into an L2-resident window, 3 ms into DRAM; tools/winscatter), so the
+// (rank, parent) records are grouped by 8192-rank window with the two
+// multisplit passes of bucket.cuh (this source feeds the first one, reading
+// the sorted chain keys / ranks) and k_link_apply writes every window from
+// shared memory with coalesced stores.  Window f holds exactly the ranks
+// [8192 f, 8192 (f + 1)), so all bucket offsets are static.
+struct LinkSortedSrc {
+  static constexpr int RW = 2, NS = 2;
+  __host__ __device__ static constexpr int sb(int) { return 4; }
+  const uint32_t* __restrict__ keys;  // sorted chain keys
+  const uint32_t* __restrict__ vals;  // ranks in (key, rank) order
+  const int32_t* __restrict__ smi_all;
+  __device__ __forceinline__ const void* ptr(int s) const { return s == 0 ? (const void*)keys : (const void*)vals; }
+  __device__ __forceinline__ uint32_t parent(uint32_t key, uint32_t pkey, uint32_t pval, bool first) const {
+    if (!first && pkey == key) return pval;
+    return key == 0 ? 0xffffffffu : (uint32_t)smi_all[key - 1];
+  }
+  __device__ __forceinline__ void get(const unsigned char* const* st, int li, int64_t i, uint32_t (&r)[2]) const {
+    const uint32_t* k = reinterpret_cast<const uint32_t*>(st[0]);
+    const uint32_t* v = reinterpret_cast<const uint32_t*>(st[1]);
+    const uint32_t key = k[li];
+    r[0] = v[li];
+    const uint32_t pk = li > 0 ? k[li - 1] : (i > 0 ? __ldg(keys + i - 1) : 0u);
+    const uint32_t pv = li > 0 ? v[li - 1] : (i > 0 ? __ldg(vals + i - 1) : 0u);
+    r[1] = parent(key, pk, pv, i == 0);
+  }
+  __device__ __forceinline__ uint32_t staged_vertex(const unsigned char* const* st, int li, int64_t) const {
+    return reinterpret_cast<const uint32_t*>(st[1])[li];
+  }
+  __device__ __forceinline__ void load(int64_t i, uint32_t (&r)[2]) const {
+    const uint32_t key = __ldg(keys + i);
+    r[0] = __ldg(vals + i);
+    const uint32_t pk = i > 0 ? __ldg(keys + i - 1) : 0u, pv = i > 0 ? __ldg(vals + i - 1) : 0u;
+    r[1] = parent(key, pk, pv, i == 0);
+  }
+  __device__ __forceinline__ uint32_t vertex(int64_t i) const { return __ldg(vals + i); }
+};
+
+// Static bucket starts: coarse bucket c = [c << (FB_BITS + gshift)), fine f = [f << FB_BITS).
+__global__ void k_link_cursors(uint32_t* __restrict__ coarse, uint32_t nc, uint32_t* __restrict__ fine, uint32_t nf,
+                               uint32_t gshift) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
+    fine[i] = i << FB_BITS;
+    if (i < nc) coarse[i] = i << (FB_BITS + gshift);
+  }
+}
+
+// One CTA per 8192-rank window: place its (rank, parent) records in shared
+// memory, then store the window's edge_parent slice coalesced.
+__global__ void __launch_bounds__(512) k_link_apply(const uint2* __restrict__ recs, int64_t n,
+                                                    int32_t* __restrict__ edge_parent) {
+  __shared__ int32_t sp[FB];
+  const int64_t base = (int64_t)blockIdx.x << FB_BITS;
+  const int cnt = n - base < FB ? (int)(n - base) : FB;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const uint2 r = __ldcs(recs + base + i);
+    sp[r.x - (uint32_t)base] = (int32_t)r.y;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) __stcs(edge_parent + base + i, sp[i]);
+}
+
+// Single-chain trees (every chain key equal, chain sort skipped): rank order
+// is chain order.
 __global__ void k_link(int64_t n, const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ svals,
                        const int32_t* __restrict__ smi_all, int32_t* __restrict__ edge_parent) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -493,7 +564,6 @@ __global__ void k_link(int64_t n, const uint32_t* __restrict__ skeys, const uint
     parent = key == 0 ? -1 : smi_all[key - 1];
   edge_parent[e] = parent;
 }
-
 // Debug: ChainAssignment.terminal / .level from the dense key.
 __global__ void k_debug_chain(int64_t n, const uint32_t* __restrict__ keys,
                               const int32_t* __restrict__ smi_all, const __grid_constant__ LevelTable lt,

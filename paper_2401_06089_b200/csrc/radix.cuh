@@ -122,24 +122,35 @@ struct ArrayLoader {
 
 // A sorted sub-tile in shared memory: item s (0 <= s < cnt) has key
 // skeys[s], payload words spay[s * PW ..], and goes to global index
-// gofs[digit] + s.  Emitters write it out with coalesced per-digit runs.
+// gofs[digit] + s; digit d's run is [lstart[d], lstart[d + 1]).  Emitters
+// write it out with coalesced per-digit runs.
 template <typename K, int PW, int BITS>
 struct TileView {
   const K* skeys;
   const uint32_t* spay;
   const uint32_t* gofs;
+  const uint32_t* lstart;  // [R + 1]
   int cnt;
   int shift;
   __device__ __forceinline__ uint32_t digit(int s) const { return digit_of<BITS>(skeys[s], shift); }
   __device__ __forceinline__ uint32_t dst(int s) const { return gofs[digit(s)] + (uint32_t)s; }
 };
 
+// Emitters may keep per-CTA state across the sub-tiles of a pass (State,
+// in shared memory): init() before the first sub-tile, finish() after the last.
+struct NoEmitState {};
+
 template <typename K, int PW>
 struct ArrayEmitter {
+  using State = NoEmitState;
   K* __restrict__ keys;
   uint32_t* __restrict__ pay;
+  template <int BLOCK, int R>
+  __device__ __forceinline__ void init(State&) const {}
+  template <int BLOCK, int R>
+  __device__ __forceinline__ void finish(State&) const {}
   template <int BLOCK, class Tile>
-  __device__ __forceinline__ void emit(const Tile& t) const {
+  __device__ __forceinline__ void emit(const Tile& t, State&) const {
     for (int s = threadIdx.x; s < t.cnt; s += BLOCK) {
       const uint32_t d = t.dst(s);
       keys[d] = t.skeys[s];
@@ -282,7 +293,7 @@ __global__ void __launch_bounds__(256) k_chunk_scan(uint32_t* counts, uint32_t G
 }
 
 // ------------------------------------------------------------- downsweep
-template <typename K, int PW, int BLOCK, int ITEMS, class Loader, int BITS = kRadixBits>
+template <typename K, int PW, int BLOCK, int ITEMS, class Loader, class Emitter, int BITS = kRadixBits>
 struct DownSmem {
   static constexpr int R = 1 << BITS;
   static constexpr int T = BLOCK * ITEMS;
@@ -309,8 +320,9 @@ struct DownSmem {
   struct Misc {
     uint32_t whist[NW][R];
     uint32_t run[R];     // running global offset per digit
-    uint32_t lstart[R];
+    uint32_t lstart[R + 1];
     uint32_t gofs[R];
+    typename Emitter::State est;
     uint32_t scan[NW + 1];
     uint32_t ballot;     // ranking method of this pass
     uint64_t bar[2];
@@ -396,6 +408,7 @@ __device__ __forceinline__ void down_subtile(const SweepArgs& a, const Emitter& 
       lstart += cb[q];
     }
   }
+  if (tid == 0) m.lstart[R] = FULL ? T : cnt_items;
   __syncthreads();
 
   K* skeys = reinterpret_cast<K*>(buf);
@@ -421,8 +434,8 @@ __device__ __forceinline__ void down_subtile(const SweepArgs& a, const Emitter& 
 #pragma unroll
       for (int q = 0; q < BPT; ++q) m.whist[w][tid * BPT + q] = 0;
   }
-  TileView<K, PW, BITS> t{skeys, spay, m.gofs, FULL ? T : cnt_items, a.shift};
-  em.template emit<BLOCK>(t);
+  TileView<K, PW, BITS> t{skeys, spay, m.gofs, m.lstart, FULL ? T : cnt_items, a.shift};
+  em.template emit<BLOCK>(t, m.est);
   __syncthreads();
 }
 
@@ -430,7 +443,7 @@ template <typename K, int PW, int BLOCK, int ITEMS, int MINB, class Loader, clas
 __global__ void __launch_bounds__(BLOCK, MINB)
 k_downsweep(SweepArgs a, Loader ld, Emitter em) {
   static_assert(BLOCK % 32 == 0 && ((1 << BITS) % BLOCK == 0 || BLOCK % (1 << BITS) == 0), "digit ownership");
-  using S = DownSmem<K, PW, BLOCK, ITEMS, Loader, BITS>;
+  using S = DownSmem<K, PW, BLOCK, ITEMS, Loader, Emitter, BITS>;
   constexpr int T = S::T, NW = S::NW, NS = S::NS, R = S::R;
   extern __shared__ __align__(128) unsigned char smem[];
   typename S::Misc& m = *reinterpret_cast<typename S::Misc*>(smem + S::off_misc());
@@ -453,6 +466,7 @@ k_downsweep(SweepArgs a, Loader ld, Emitter em) {
     mbar_fence_init();
     m.ballot = a.counts[(uint64_t)R * a.GS];
   }
+  em.template init<BLOCK, R>(m.est);
   __syncthreads();
 
   // issue the bulk copies of sub-tile `sub` into stage buffer sub & 1
@@ -504,7 +518,10 @@ k_downsweep(SweepArgs a, Loader ld, Emitter em) {
         down_subtile<false, K, PW, BLOCK, ITEMS, BITS, S>(a, em, m, buf, k, v, cnt_items);
     }
   }
+  __syncthreads();
+  em.template finish<BLOCK, R>(m.est);
 }
+
 
 // Every digit was constant: the stable order is the identity.  Items go
 // through a shared-memory tile with gofs = tile base, so emitters see the
@@ -514,6 +531,8 @@ __global__ void __launch_bounds__(BLOCK) k_identity_pass(int64_t n, Loader ld, E
   __shared__ K skeys[BLOCK];
   __shared__ uint32_t spay[BLOCK * PW];
   __shared__ uint32_t gofs[kRadix];
+  __shared__ uint32_t lstart[kRadix + 1];
+  __shared__ typename Emitter::State est;
   const int64_t i0 = (int64_t)blockIdx.x * BLOCK;
   const int64_t i = i0 + threadIdx.x;
   const int cnt = n - i0 < BLOCK ? (int)(n - i0) : BLOCK;
@@ -525,10 +544,18 @@ __global__ void __launch_bounds__(BLOCK) k_identity_pass(int64_t n, Loader ld, E
 #pragma unroll
     for (int q = 0; q < PW; ++q) spay[threadIdx.x * PW + q] = v.w[q];
   }
-  for (int b = threadIdx.x; b < kRadix; b += BLOCK) gofs[b] = (uint32_t)i0;
   __syncthreads();
-  TileView<K, PW, kRadixBits> t{skeys, spay, gofs, cnt, 0};
-  em.template emit<BLOCK>(t);
+  const uint32_t d0 = digit_of<kRadixBits>(skeys[0], 0);  // every key is the same
+  for (int b = threadIdx.x; b <= kRadix; b += BLOCK) {
+    if (b < kRadix) gofs[b] = (uint32_t)i0;
+    lstart[b] = (uint32_t)b <= d0 ? 0u : (uint32_t)cnt;  // one run, of digit d0
+  }
+  em.template init<BLOCK, kRadix>(est);
+  __syncthreads();
+  TileView<K, PW, kRadixBits> t{skeys, spay, gofs, lstart, cnt, 0};
+  em.template emit<BLOCK>(t, est);
+  __syncthreads();
+  em.template finish<BLOCK, kRadix>(est);
 }
 
 // Exclusive scan of per-digit global histograms: hist[p][256] -> gbase[p][256].

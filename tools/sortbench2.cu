@@ -32,7 +32,7 @@ template <typename K, int PW, int BLOCK, int ITEMS, int MINB>
 void run(int64_t n, K* k, uint32_t* v, K* k2, uint32_t* v2, uint32_t* counts, int sms, const char* tag) {
   using L = ArrayLoader<K, PW>;
   using E = ArrayEmitter<K, PW>;
-  using S = DownSmem<K, PW, BLOCK, ITEMS, L>;
+  using S = DownSmem<K, PW, BLOCK, ITEMS, L, E>;
   auto kern = k_downsweep<K, PW, BLOCK, ITEMS, MINB, L, E>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes());
   SweepArgs a{};

@@ -271,11 +271,16 @@ __global__ void __launch_bounds__(BLOCK) k_split(Src src, int64_t m, uint32_t gs
     }
     uint32_t tot;
     uint32_t run = block_excl_sum<BLOCK>(sum, scratch, &tot);
+    // the reservations' round trip overlaps the regrouping below: their
+    // results are only needed for the write-out
+    uint32_t g[PER], lst[PER];
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
       const uint32_t b = tid * PER + q;
+      g[q] = 0;
+      lst[q] = run;
       if (b < (uint32_t)NC) {
-        if (c[q]) gofs[b] = atomicAdd(cursor + (FINE ? lo + b : b), c[q]) - run;
+        if (c[q]) g[q] = atomicAdd(cursor + (FINE ? lo + b : b), c[q]);
         cnt[b] = run;  // local start of bucket b
         run += c[q];
       }
@@ -291,6 +296,11 @@ __global__ void __launch_bounds__(BLOCK) k_split(Src src, int64_t m, uint32_t gs
 #pragma unroll
         for (int q = 0; q < RW; ++q) st[RW * p + q] = r[q];
       }
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const uint32_t b = tid * PER + q;
+      if (b < (uint32_t)NC && c[q]) gofs[b] = g[q] - lst[q];
     }
     __syncthreads();
     if (tid == 0) issue(tile + 2 * (int64_t)gridDim.x, buf);  // stage buffer consumed

@@ -47,21 +47,50 @@ WORKLOADS = {
                 "config5: batch of 64 independent random spanning trees n=8M (uniform weights, seeds 0..63), "
                 "tree i on GPU i mod N"),
     "config1": ("random", 100_000, "config1: random spanning tree n=100k, uniform weights, seed 0"),
+    "config2": ("blobs1m", 999_999, "config2: EMST of 1M 3-D Gaussian-blob points (mutual reachability, "
+                "min_samples=2) computed by the reference, tests/golden/config2_blobs1m.npz"),
 }
 
-# Algorithmic HBM bytes per launch of each kernel kind.  n = edges of
-# the launch's view; int32 ids/ranks = 4 B, float64 = 8 B.
-BYTES_PER_EDGE = {
-    "sort1_hist": 8,          # read w
-    "sort1_pass_first": 36,   # read w 8, u 4, v 4; write key 8 + (id, u, v) 12
-    "sort1_pass_mid": 40,     # read key + payload 20; write 20
-    "sort1_pass_final": 40,   # read 20; write orig_of 4, heights 8, euv 8
-    "mi_split": 32,           # read euv 8; write 2 records x (vertex, rank, other) 12
-    "mi_apply": 40,           # read 2 records 24; mi64 read-modify-write 16
-    "sort2_pass": 16,         # read key + rank 8; write 8
-    "walk": 17,               # ret 1 + eu 4 + map 4 + smi 4 + key 4
-    "link": 12,               # read key + rank 8; scatter 4
-}
+# Algorithmic HBM bytes of each kernel kind per build: what the
+# kernel must read and write given its design, counting a random 4-B access
+# as 4 B (the 64-B DRAM sector it really costs is NOT credited; `traffic`
+# shows it).  ids / ranks 4 B, weights and keys 8 B, records 12 B (maxIncident)
+# or 8 B (chain links).
+DIRECT_MI_BYTES = 24 << 20  # dmst.cu kDirectMiBytes: views whose mi64 fits are scatter-maxed directly
+
+
+def kernel_bytes(stats, n: int, nv: int) -> dict[str, float]:
+    counts = stats.view_kind_counts()            # (n_alpha, n_leaf, n_chain, n_k) per view
+    L = stats.num_levels
+    views_n = [c[3] for c in counts]
+    views_v = [int(stats.view_vertices[k]) for k in range(L + 1)]
+    # views whose maxIncident is bucketed: view 0 and later views with a large mi64
+    buck = [0] + [k for k in range(1, L + 1) if views_v[k] * 8 > DIRECT_MI_BYTES]
+    mb = sum(2 * views_n[k] for k in buck)        # records (2 per edge) of bucketed views
+    vb = sum(views_v[k] for k in buck)
+    p1, p2 = stats.sort1_passes, stats.sort2_passes
+    alpha = sum(c[0] for c in counts[:L])         # edges copied into the next view
+    return {
+        "sort1_hist": 8.0 * n,                                  # read w
+        "sort1_pass_first": 36.0 * n,                           # read w, u, v 16; write key + (id, u, v) 20
+        "sort1_pass_mid": 40.0 * n * max(p1 - 2, 0),            # read 20, write 20 per pass
+        "sort1_pass_final": 40.0 * n,                           # read 20; write orig_of 4, heights 8, euv 8
+        "upsweep_scan": 8.0 * n * p1 + 4.0 * n * p2,            # key reads
+        "mi_hist": 4.0 * mb,                                    # read endpoints
+        "mi_split_a": 16.0 * mb,                                # read 4 + write 12 per record
+        "mi_split_b": 24.0 * mb,                                # read 12 + write 12 per record
+        "mi_apply": 12.0 * mb + 12.0 * vb,                      # read records; write mi64 8 + parent 4
+        "v1": 12.0 * sum(views_v[k] for k in range(1, L + 1) if k not in buck),
+        "leafscan": 1.0 * sum(views_n),                         # 2-bit counts in, prefixes out (per 16 edges)
+        "v2": 12.0 * sum(views_v[:L]),                          # mi64 8 + vertex map 4 (chase hops not credited)
+        "jump": 0.0,
+        "select_edges": 9.0 * sum(views_n[:L]) + 4.0 * n + 20.0 * alpha,  # euv + ret; x1; alpha: 2 gathers + next view
+        "walk": 17.0 * n,                                       # ret 1 + x1 4 + smi 4 + map 4 + key 4
+        "sort2_pass": 16.0 * n * p2,                            # read 8, write 8 per pass
+        "link_split": 32.0 * n if p2 else 0.0,                  # two 8-B record passes (read + write)
+        "link_apply": 12.0 * n,                                 # read records 8, write edge_parent 4
+        "other": 0.0,
+    }
 
 
 def pipeline_bytes(n: int, S: int) -> int:
@@ -92,7 +121,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -401,25 +430,32 @@ def run_b200(args) -> None:
 
     if rank == 0:
         peak, peak_src = load_peaks()
-        # dominant kernel (largest total device time in the timed region)
+        # every kernel kind: algorithmic bytes / device time over the timed
+        # region (CUDA events on the launching stream); the dominant kind
+        # (largest device time) is the headline `roofline`
+        per_build = kernel_bytes(stats, n_last, n_last + 1)
+        builds = args.steps * len(trees)
+        traffic_tab = {}
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath):
+            try:
+                traffic_tab = json.load(open(tpath)).get(args.workload, {})
+            except Exception:
+                traffic_tab = {}
+        kroof = {}
+        for k, (kms, kcalls) in prof.items():
+            bts = per_build.get(k, 0.0) * builds
+            kroof[k] = {"ms_per_build": kms / builds, "launches_per_build": kcalls / builds,
+                        "algorithmic_bytes_per_build": bts / builds,
+                        "achieved_GBs": bts / (kms * 1e-3) / 1e9 if kms > 0 else 0.0}
         kname, (kms, kcalls) = max(prof.items(), key=lambda kv: kv[1][0])
-        per_launch_ms = kms / kcalls
-        bpe = BYTES_PER_EDGE.get(kname)
-        roof = None
-        if bpe is not None:
-            n_launch = n_last if kname not in ("mi_split", "mi_apply") else n_last
-            achieved = bpe * n_launch / (per_launch_ms * 1e-3) / 1e9
-            traffic = None
-            tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-            if os.path.exists(tpath):
-                try:
-                    traffic = json.load(open(tpath)).get(args.workload, {}).get(kname)
-                except Exception:
-                    traffic = None
-            roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak, "traffic": traffic,
-                    "algorithmic_bytes_per_launch": bpe * n_launch, "avg_launch_ms": per_launch_ms,
-                    "peak_source": peak_src}
+        kr = kroof[kname]
+        roof = {"bound": "hbm", "kernel": kname, "achieved": kr["achieved_GBs"], "peak": peak, "unit": "GB/s",
+                "frac": kr["achieved_GBs"] / peak, "traffic": traffic_tab.get(kname),
+                "algorithmic_bytes_per_launch": kr["algorithmic_bytes_per_build"] / max(kr["launches_per_build"], 1e-9),
+                "avg_launch_ms": kms / kcalls, "launches_per_build": kr["launches_per_build"],
+                "peak_source": peak_src,
+                "note": "traffic = ncu dram__bytes_read+write per launch (profiles/ncu_traffic.json)"}
         B = sum(pipeline_bytes(int(t[1].shape[0]), S) for t in trees) * ws
         pipe_ach = B / (ms_step * 1e-3) / 1e9
         cpu = None
@@ -457,6 +493,9 @@ def run_b200(args) -> None:
                                   "model": "403 n + 98 S (SURVEY.md 8d)", "peak_source": peak_src,
                                   "frac_vs_nominal_8TBs": pipe_ach / 8000.0},
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])},
+            "kernel_roofline": {k: {"ms": round(v["ms_per_build"], 4), "GBs": round(v["achieved_GBs"], 1),
+                                    "frac": round(v["achieved_GBs"] / peak, 4)}
+                                for k, v in sorted(kroof.items(), key=lambda kv: -kv[1]["ms_per_build"])},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": launches,

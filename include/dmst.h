@@ -53,7 +53,7 @@ extern "C" {
 #define DMST_ECUDA (-1)
 #define DMST_MAX_LEVELS 64
 
-#define DMST_MAX_KERNELS 16
+#define DMST_MAX_KERNELS 24
 
 /* Per-call diagnostics (host memory, optional).  Set `profile` = 1 before
  * the call to have every kernel bracketed by CUDA events on `stream`;

@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libdmst.so")
 DMST_EINVAL = 22
 DMST_ECUDA = -1
 DMST_MAX_LEVELS = 64
-DMST_MAX_KERNELS = 16
+DMST_MAX_KERNELS = 24
 
 # every symbol include/dmst.h declares
 EXPORTS = (

@@ -41,14 +41,15 @@ constexpr int S2_BLOCK = 512, S2_ITEMS = 16, S2_MINB = 1, S2_BITS = 9;
 constexpr int64_t kDirectMiBytes = 24ll << 20;  // direct scatter-max below this mi64 size
 
 enum KernelKind {
-  KK_SORT1_HIST, KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL, KK_MI_SPLIT, KK_MI_APPLY, KK_V1,
-  KK_LEAFSCAN, KK_V2, KK_JUMP, KK_SELECT_EDGES, KK_WALK, KK_SORT2_PASS, KK_LINK, KK_UPSWEEP, KK_OTHER,
-  KK_COUNT
+  KK_SORT1_HIST, KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL, KK_MI_HIST, KK_MI_SPLIT_A, KK_MI_SPLIT_B,
+  KK_MI_APPLY, KK_V1, KK_LEAFSCAN, KK_V2, KK_JUMP, KK_SELECT_EDGES, KK_WALK, KK_SORT2_PASS, KK_LINK_SPLIT,
+  KK_LINK_APPLY, KK_UPSWEEP, KK_OTHER, KK_COUNT
 };
 static_assert(KK_COUNT <= DMST_MAX_KERNELS, "kernel kinds");
 const char* const kKernelNames[KK_COUNT] = {
-    "sort1_hist", "sort1_pass_first", "sort1_pass_mid", "sort1_pass_final", "mi_split", "mi_apply",
-    "v1", "leafscan", "v2", "jump", "select_edges", "walk", "sort2_pass", "link", "upsweep_scan", "other"};
+    "sort1_hist", "sort1_pass_first", "sort1_pass_mid", "sort1_pass_final", "mi_hist", "mi_split_a",
+    "mi_split_b", "mi_apply", "v1", "leafscan", "v2", "jump", "select_edges", "walk", "sort2_pass",
+    "link_split", "link_apply", "upsweep_scan", "other"};
 
 namespace {
 
@@ -417,11 +418,11 @@ void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiAp
   c.zero(counts, 4 * (nf + 1));
   DMST_CUDA(cudaFuncSetAttribute(k_fine_hist<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * FH_WINDOW));
   for (uint32_t flo = 0; flo < nf; flo += FH_WINDOW) {
-    c.begin(KK_MI_SPLIT);
+    c.begin(KK_MI_HIST);
     k_fine_hist<Src><<<c.persistent_grid(m, 256, 3), 256, 4 * FH_WINDOW, c.s>>>(src, m, flo, nf, counts);
     c.launched();
   }
-  c.begin(KK_MI_SPLIT);
+  c.begin(KK_MI_HIST);
   k_fine_scan<<<1, 1024, 0, c.s>>>(counts, nf, gshift, fine_base, fine_cur, coarse_cur);
   c.launched();
   using SA = SplitSmem<Src, BKA_BLOCK, BKA_ITEMS, 256>;
@@ -430,10 +431,10 @@ void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiAp
   auto kB = k_split<true, AosRecSrc<3>, BKB_BLOCK, BKB_ITEMS, BKB_SPAN>;
   DMST_CUDA(cudaFuncSetAttribute(kA, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SA::bytes()));
   DMST_CUDA(cudaFuncSetAttribute(kB, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SB::bytes()));
-  c.begin(KK_MI_SPLIT);
+  c.begin(KK_MI_SPLIT_A);
   kA<<<c.persistent_grid(m, SA::T, 2), BKA_BLOCK, SA::bytes(), c.s>>>(src, m, gshift, coarse_cur, mid);
   c.launched();
-  c.begin(KK_MI_SPLIT);
+  c.begin(KK_MI_SPLIT_B);
   kB<<<c.persistent_grid(m, SB::T, 2), BKB_BLOCK, SB::bytes(), c.s>>>(AosRecSrc<3>{mid.r}, m, gshift, fine_cur, fin);
   c.launched();
   DMST_CUDA(cudaFuncSetAttribute(k_mi_apply_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * FB));  // 64 KB
@@ -613,7 +614,7 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
   if (st) st->sort2_passes = (int)shifts.size();
   // chain sort: keys at R[0, 4n); ping-pong A = R[4n, 12n), B = R[12n, 20n);
   if (shifts.empty()) {  // one chain (all keys equal): rank order is chain order
-    c.begin(KK_LINK);
+    c.begin(KK_LINK_APPLY);
     k_link<<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(n, keys, nullptr, w.smi_all, edge_parent);
     c.launched();
   } else {
@@ -631,7 +632,7 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     const uint32_t nc = (uint32_t)cdiv(nf, 1u << gshift);
     uint32_t* fine_cur = w.fine;
     uint32_t* coarse_cur = w.fine + (nf + 2);
-    c.begin(KK_LINK);
+    c.begin(KK_LINK_SPLIT);
     k_link_cursors<<<grid_for(nf, EW_BLOCK), EW_BLOCK, 0, c.s>>>(coarse_cur, nc, fine_cur, nf, gshift);
     c.launched();
     using LA = SplitSmem<LinkSortedSrc, BKA_BLOCK, BKA_ITEMS, 256>;
@@ -640,15 +641,15 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     auto kB = k_split<true, AosRecSrc<2>, BKB_BLOCK, BKB_ITEMS, BKB_SPAN>;
     DMST_CUDA(cudaFuncSetAttribute(kA, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LA::bytes()));
     DMST_CUDA(cudaFuncSetAttribute(kB, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LB::bytes()));
-    c.begin(KK_LINK);
+    c.begin(KK_LINK_SPLIT);
     kA<<<c.persistent_grid(n, LA::T, 2), BKA_BLOCK, LA::bytes(), c.s>>>(
         LinkSortedSrc{fin.keys, fin.pay, w.smi_all}, n, gshift, coarse_cur, Recs{recA});
     c.launched();
-    c.begin(KK_LINK);
+    c.begin(KK_LINK_SPLIT);
     kB<<<c.persistent_grid(n, LB::T, 2), BKB_BLOCK, LB::bytes(), c.s>>>(AosRecSrc<2>{recA}, n, gshift, fine_cur,
                                                                         Recs{recB});
     c.launched();
-    c.begin(KK_LINK);
+    c.begin(KK_LINK_APPLY);
     k_link_apply<<<nf, 512, 0, c.s>>>((const uint2*)recB, n, edge_parent);
     c.launched();
   }

@@ -54,10 +54,24 @@ def caterpillar(n: int, seed: int = 0):
     return (nv, *_shuffle(rng, u, v, np.arange(n, dtype=np.float64)))
 
 
+def blobs1m(n: int = 999_999, seed: int = 0):
+    """Config 2: the reference's mutual-reachability MST (min_samples=2) of 1M
+    3-D Gaussian-blob points, computed once by the unmodified reference
+    (tests/golden/make_config2.py) and committed as a fixture; n and seed are
+    fixed by the fixture."""
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
+                        "config2_blobs1m.npz")
+    g = np.load(path)
+    return (int(g["num_vertices"]), np.ascontiguousarray(g["u"], np.int32), np.ascontiguousarray(g["v"], np.int32),
+            np.ascontiguousarray(g["w"], np.float64))
+
+
 GENERATORS = {
     "random": lambda n, seed=0: random_attach(n, seed, tied=False),
     "tied": lambda n, seed=0: random_attach(n, seed, tied=True),
     "path": path,
+    "blobs1m": blobs1m,
     "caterpillar": caterpillar,
 }
 

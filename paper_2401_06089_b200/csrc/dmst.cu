@@ -94,7 +94,8 @@ struct Workspace {
   int8_t* ret;            // retirement level per edge
   int2* euv[2];           // view edges (ping-pong)
   int32_t* grank[2];
-  int32_t* vm_all;        // vertex maps of views 0..L-1
+  int32_t* vm_all;        // vertex map of view 0
+  int2* lvl_all;          // walk table of views 1..L: (vertex map, maxIncident) at soff[k] + x
   int32_t* smi_all;       // maxIncident (global ranks) of views 1..L
   int32_t* x1;            // view-1 supervertex of every edge (walk start)
   uint32_t* sel_status;   // leafscan look-back words (leaf, alpha)
@@ -134,7 +135,8 @@ Workspace carve(int64_t n, int64_t nv, char* base) {
     w.euv[i] = (int2*)take(8 * half);
     w.grank[i] = (int32_t*)take(4 * half);
   }
-  w.vm_all = (int32_t*)take(4 * (2 * nv + DMST_MAX_LEVELS + 2));
+  w.vm_all = (int32_t*)take(4 * (nv + 2));
+  w.lvl_all = (int2*)take(8 * (nv + DMST_MAX_LEVELS + 2));
   w.smi_all = (int32_t*)take(4 * (nv + DMST_MAX_LEVELS + 2));
   w.x1 = (int32_t*)take(4 * (n + 2));
   w.sel_status = (uint32_t*)take(8 * (cdiv(n / 16 + 1, LS_TILE) + 2));
@@ -466,7 +468,7 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
   const int32_t* grank_k = nullptr;
   const unsigned long long* mi_k = w.mi64_0;
   int cur = 0, level = 0, jump_rounds = 0;
-  int64_t voff = 0, soff = 0;
+  int64_t soff = 0;
   // jump lists in R: rulers (+ 2 ping-pong) and non-rulers
   int32_t* lists[4] = {(int32_t*)w.R, (int32_t*)w.R + nv, (int32_t*)w.R + 2 * nv, (int32_t*)w.R + 3 * nv};
   uint32_t* lcnt[4] = {misc + MISC_ACTIVE0, misc + MISC_ACTIVE1, misc + MISC_ACTIVE2, misc + MISC_NONRUL};
@@ -492,12 +494,15 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     c.launched();
     // V2: supervertex labels (vertex_map).  Runs before the host reads the
     // counts (one sync per level); on the final view its result is unused.
-    int32_t* vm = w.vm_all + voff;
+    // view 0: plain vertex map; views >= 1: packed walk table (stride 2)
+    int32_t* vm = level == 0 ? w.vm_all : (int32_t*)(w.lvl_all + lt.soff[level]);
+    const int vs = level == 0 ? 1 : 2;
     c.zero(misc + MISC_ACTIVE0, 12);
     c.zero(misc + MISC_NONRUL, 4);
     c.begin(KK_V2);
-    k_v2<<<grid_for(nv_k, EW_BLOCK), EW_BLOCK, 0, c.s>>>(nv_k, mi_k, w.kw, vm, lists[0], lcnt[0], lists[3],
-                                                         lcnt[3]);
+    k_v2<<<grid_for(nv_k, EW_BLOCK), EW_BLOCK, 0, c.s>>>(nv_k, mi_k, w.kw, vm,
+                                                         level == 0 ? nullptr : w.smi_all + lt.soff[level],
+                                                         lists[0], lcnt[0], lists[3], lcnt[3]);
     c.launched();
     uint32_t counts[4];
     c.to_host(counts, misc + MISC_COUNTS, 8);
@@ -521,8 +526,6 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
       }
       break;
     }
-    lt.voff[level] = voff;
-    voff += nv_k;
     // pointer jumping: rulers first (a chain of rulers ~1/32 as long as the
     // in-tree), then the non-rulers, whose targets are then resolved rulers
     for (int phase = 0; phase < 2; ++phase) {
@@ -533,7 +536,8 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
       while (pending) {
         c.zero(lcnt[a], 4);
         c.begin(KK_JUMP);
-        k_jump<<<c.persistent_grid(pending, EW_BLOCK, 16), EW_BLOCK, 0, c.s>>>(in, in_cnt, lists[a], lcnt[a], vm);
+        k_jump<<<c.persistent_grid(pending, EW_BLOCK, 16), EW_BLOCK, 0, c.s>>>(in, in_cnt, lists[a], lcnt[a], vm,
+                                                                               vs);
         c.launched();
         ++jump_rounds;
         c.to_host(&pending, lcnt[a], 4);
@@ -559,6 +563,7 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     es.euv = euv_k;
     es.grank = grank_k;
     es.vm = vm;
+    es.vs = vs;
     es.ret = w.ret;
     es.euv_next = w.euv[cur ^ 1];
     es.grank_next = w.grank[cur ^ 1];
@@ -598,7 +603,7 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
   const uint32_t kinit[2] = {~0u, 0u};
   DMST_CUDA(cudaMemcpyAsync(key_ao, kinit, 8, cudaMemcpyHostToDevice, c.s));
   c.begin(KK_WALK);
-  k_walk<256><<<c.persistent_grid(n, 256, 8), 256, 0, c.s>>>(n, w.ret, w.x1, w.vm_all, w.smi_all, lt, keys,
+  k_walk<256><<<c.persistent_grid(n, 256, 8), 256, 0, c.s>>>(n, w.ret, w.x1, w.lvl_all, lt, keys,
                                                               key_ao);
   c.launched();
   if (dbg_ret) DMST_CUDA(cudaMemcpyAsync(dbg_ret, w.ret, n, cudaMemcpyDeviceToDevice, c.s));

@@ -265,9 +265,12 @@ __device__ __forceinline__ uint32_t leaf_label(uint2 w, uint32_t j) {
 // A chase longer than CHASE_FREE steps stops at the first ruler vertex (or
 // after CHASE_CAP steps) and stores ~y (y = where it stopped); rulers and
 // non-rulers go to separate lists for pointer jumping.
+// Views >= 1 (smi != null) store the vertex map interleaved with the view's
+// maxIncident as (vm[x], smi[x]) pairs: the chain walk then gets both from
+// one random 8-B probe (one DRAM sector) per level; vm has stride 2 there.
 __global__ void k_v2(int64_t nv, const unsigned long long* __restrict__ mi64, const uint2* __restrict__ kw,
-                     int32_t* __restrict__ vm, int32_t* __restrict__ rul, uint32_t* __restrict__ rul_cnt,
-                     int32_t* __restrict__ non, uint32_t* __restrict__ non_cnt) {
+                     int32_t* __restrict__ vm, const int32_t* __restrict__ smi, int32_t* __restrict__ rul,
+                     uint32_t* __restrict__ rul_cnt, int32_t* __restrict__ non, uint32_t* __restrict__ non_cnt) {
   const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t pol = l2_keep_policy();
   bool unresolved = false;
@@ -289,7 +292,11 @@ __global__ void k_v2(int64_t nv, const unsigned long long* __restrict__ mi64, co
       j = (uint32_t)(m >> 32) - 1u;
       y = (uint32_t)m;
     }
-    __stcs(vm + x, unresolved ? ~(int32_t)y : (m ? (int32_t)leaf_label(kwj, j) : 0));
+    const int32_t lab = unresolved ? ~(int32_t)y : (m ? (int32_t)leaf_label(kwj, j) : 0);
+    if (smi)
+      __stcs(reinterpret_cast<int2*>(vm) + x, make_int2(lab, __ldcs(smi + x)));
+    else
+      __stcs(vm + x, lab);
   }
   const bool ruler = unresolved && is_ruler((uint32_t)x);
   const bool plain = unresolved && !ruler;
@@ -310,7 +317,7 @@ __global__ void k_v2(int64_t nv, const unsigned long long* __restrict__ mi64, co
 // vm[x] < 0 is ~(a vertex further along the chase).  Pointers only ever
 // move forward along the chase, so in-place updates are safe.
 __global__ void k_jump(const int32_t* __restrict__ in, const uint32_t* __restrict__ in_cnt,
-                       int32_t* __restrict__ out, uint32_t* __restrict__ out_cnt, int32_t* vm) {
+                       int32_t* __restrict__ out, uint32_t* __restrict__ out_cnt, int32_t* vm, int vs) {
   const uint32_t cnt = *in_cnt;
   for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x; t0 < cnt; t0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = t0 + threadIdx.x;
@@ -318,8 +325,8 @@ __global__ void k_jump(const int32_t* __restrict__ in, const uint32_t* __restric
     int32_t x = 0;
     if (t < cnt) {
       x = in[t];
-      const int32_t q = vm[~vm[x]];
-      vm[x] = q;
+      const int32_t q = vm[(int64_t)~vm[(int64_t)x * vs] * vs];
+      vm[(int64_t)x * vs] = q;
       again = q < 0;
     }
     const uint32_t m = __ballot_sync(kFull, again);
@@ -346,7 +353,8 @@ struct EdgeSel {
   const uint32_t* __restrict__ apre; // alpha prefix per 16 edges
   const int2* __restrict__ euv;
   const int32_t* __restrict__ grank; // null => identity (view 0)
-  const int32_t* __restrict__ vm;
+  const int32_t* __restrict__ vm;    // vertex map, stride vs (2 = packed walk table)
+  int vs;
   int8_t* __restrict__ ret;
   int2* __restrict__ euv_next;
   int32_t* __restrict__ grank_next;
@@ -381,8 +389,8 @@ __global__ void __launch_bounds__(SEL_BLOCK) k_select_edges(int64_t n, EdgeSel e
     int32_t a[SEL_U], bb[SEL_U];
 #pragma unroll
     for (int q = 0; q < SEL_U; ++q) {
-      a[q] = need[q] ? es.vm[e[q].x] : lab[q];
-      bb[q] = alpha[q] ? es.vm[e[q].y] : 0;
+      a[q] = need[q] ? es.vm[(int64_t)e[q].x * es.vs] : lab[q];
+      bb[q] = alpha[q] ? es.vm[(int64_t)e[q].y * es.vs] : 0;
     }
 #pragma unroll
     for (int q = 0; q < SEL_U; ++q) {
@@ -413,7 +421,6 @@ __global__ void k_retire_all(int64_t n, const int32_t* __restrict__ grank, int8_
 
 // ------------------------------------------------------ 4. expansion walk
 struct LevelTable {
-  int64_t voff[DMST_MAX_LEVELS + 1];  // offset of vertex_map of view k in vm_all
   int64_t soff[DMST_MAX_LEVELS + 2];  // offset of maxIncident (global ranks) of view k in smi_all
   int32_t L;
 };
@@ -424,15 +431,13 @@ struct LevelTable {
 // 1 + soff[k] + anchor (a terminal edge is a terminal only at the one level
 // it retires at, so (level, anchor) identifies the chain); 0 = root chain.
 // The walk starts at the edge's view-1 supervertex x1[e] (written by the
-// view-0 select); per level it reads smi_k[x] (maxIncident of view k, global
-// ranks) and, on a miss, vm_k[x] (view k -> k + 1), so the dominant first
-// check touches a 4-B table of nv_1 entries.
+// view-0 select); per level one 8-B probe of the packed walk table
+// lvl[soff[k] + x] = (vm_k[x], smi_k[x]) (maxIncident of view k in global
+// ranks, and the supervertex of x in view k + 1).
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK)
-k_walk(int64_t n, const int8_t* __restrict__ ret, const int32_t* __restrict__ x1,
-       const int32_t* __restrict__ vm_all, const int32_t* __restrict__ smi_all,
-       const __grid_constant__ LevelTable lt, uint32_t* __restrict__ keys,
-       uint32_t* __restrict__ and_or) {
+k_walk(int64_t n, const int8_t* __restrict__ ret, const int32_t* __restrict__ x1, const int2* __restrict__ lvl,
+       const __grid_constant__ LevelTable lt, uint32_t* __restrict__ keys, uint32_t* __restrict__ and_or) {
   uint32_t ka = ~0u, ko = 0u;
   const int64_t stride = (int64_t)gridDim.x * BLOCK;
   for (int64_t e0 = (int64_t)blockIdx.x * BLOCK; e0 < n; e0 += stride) {
@@ -443,15 +448,13 @@ k_walk(int64_t n, const int8_t* __restrict__ ret, const int32_t* __restrict__ x1
       if (r < lt.L) {
         int32_t x = __ldcs(x1 + e);  // view-1 supervertex
         for (int k = 1;; ++k) {
-          if (k > r) {
-            const int32_t p = smi_all[lt.soff[k] + x];
-            if (p >= 0 && p < (int32_t)e) {
-              key = (uint32_t)(1 + lt.soff[k] + x);
-              break;
-            }
+          const int2 t = lvl[lt.soff[k] + x];
+          if (k > r && t.y >= 0 && t.y < (int32_t)e) {
+            key = (uint32_t)(1 + lt.soff[k] + x);
+            break;
           }
           if (k >= lt.L) break;
-          x = vm_all[lt.voff[k] + x];
+          x = t.x;
         }
       }
       __stcs(keys + e, key);

@@ -21,6 +21,7 @@ constexpr int FB = 1 << FB_BITS;
 constexpr int BKA_BLOCK = 512, BKA_ITEMS = 8;   // 4096 records per sub-tile
 constexpr int BKB_BLOCK = 512, BKB_ITEMS = 4;   // 2048 records per sub-tile
 constexpr int BKB_SPAN = 1024;                  // max fine buckets a pass-B sub-tile may touch
+constexpr int BKB_PER_SM = 4;                   // pass-B CTAs per SM (in-place regrouping: ~56 KB smem)
 
 // Records are AoS tuples of RW words whose first word is the bucketing key
 // (maxIncident: (vertex, j + 1, other end), RW = 3; chain links: (rank,
@@ -149,9 +150,13 @@ __global__ void __launch_bounds__(1024) k_fine_scan(const uint32_t* __restrict__
 // non-empty bucket reserves the output range, the records are regrouped in
 // shared memory and written out as one word stream (consecutive threads ->
 // consecutive words of a bucket run).  Only the slots live in registers.
+// INPLACE (AoS sources whose staged record is the output record): the
+// regrouped sub-tile is written into the consumed stage buffer, so no
+// separate staging area and ~2x the CTAs per SM.
 template <class Src, int BLOCK, int ITEMS, int NC>
 struct SplitSmem {
   static constexpr int T = BLOCK * ITEMS;
+  static constexpr bool INPLACE = Src::NS == 1 && Src::sb(0) == 4 * Src::RW;
   __host__ __device__ static constexpr size_t stream_bytes(int s) { return ((size_t)T * Src::sb(s) + 127) & ~size_t(127); }
   __host__ __device__ static constexpr size_t stream_off(int s) {
     size_t b = 0;
@@ -160,7 +165,7 @@ struct SplitSmem {
   }
   __host__ __device__ static constexpr size_t in_bytes() { return stream_off(Src::NS); }
   __host__ __device__ static constexpr size_t off_st() { return 2 * in_bytes(); }
-  __host__ __device__ static constexpr size_t off_cnt() { return off_st() + 4 * Src::RW * (size_t)T; }
+  __host__ __device__ static constexpr size_t off_cnt() { return off_st() + (INPLACE ? 0 : 4 * Src::RW * (size_t)T); }
   __host__ __device__ static constexpr size_t bytes() { return off_cnt() + 8 * (size_t)NC; }
 };
 
@@ -253,10 +258,18 @@ __global__ void __launch_bounds__(BLOCK) k_split(Src src, int64_t m, uint32_t gs
     }
     auto bucket = [&](uint32_t x) { return FINE ? (x >> FB_BITS) - lo : (x >> FB_BITS) >> gshift; };
     uint32_t slot[ITEMS];
+    uint32_t keep[S::INPLACE ? ITEMS : 1][RW];  // in-place: records held across the regrouping
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const int li = i * BLOCK + tid;
-      if (li < count) slot[i] = atomicAdd(&cnt[bucket(vtx(li))], 1u);
+      if (li < count) {
+        if constexpr (S::INPLACE) {
+          rec(li, keep[i]);
+          slot[i] = atomicAdd(&cnt[bucket(keep[i][0])], 1u);
+        } else {
+          slot[i] = atomicAdd(&cnt[bucket(vtx(li))], 1u);
+        }
+      }
     }
     __syncthreads();
     // exclusive scan of the counters + global reservation; thread t owns
@@ -286,15 +299,21 @@ __global__ void __launch_bounds__(BLOCK) k_split(Src src, int64_t m, uint32_t gs
       }
     }
     __syncthreads();
+    uint32_t* stg = S::INPLACE ? reinterpret_cast<uint32_t*>(const_cast<unsigned char*>(stage[0])) : st;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
       const int li = i * BLOCK + tid;
       if (li < count) {
         uint32_t r[RW];
-        rec(li, r);
+        if constexpr (S::INPLACE) {
+#pragma unroll
+          for (int q = 0; q < RW; ++q) r[q] = keep[i][q];
+        } else {
+          rec(li, r);
+        }
         const uint32_t p = cnt[bucket(r[0])] + slot[i];
 #pragma unroll
-        for (int q = 0; q < RW; ++q) st[RW * p + q] = r[q];
+        for (int q = 0; q < RW; ++q) stg[RW * p + q] = r[q];
       }
     }
 #pragma unroll
@@ -303,12 +322,13 @@ __global__ void __launch_bounds__(BLOCK) k_split(Src src, int64_t m, uint32_t gs
       if (b < (uint32_t)NC && c[q]) gofs[b] = g[q] - lst[q];
     }
     __syncthreads();
-    if (tid == 0) issue(tile + 2 * (int64_t)gridDim.x, buf);  // stage buffer consumed
+    if (!S::INPLACE && tid == 0) issue(tile + 2 * (int64_t)gridDim.x, buf);  // stage buffer consumed
     for (int s_ = tid; s_ < RW * count; s_ += BLOCK) {
       const int it = s_ / RW;
-      out.r[RW * (uint64_t)gofs[bucket(st[RW * it])] + s_] = st[s_];
+      out.r[RW * (uint64_t)gofs[bucket(stg[RW * it])] + s_] = stg[s_];
     }
     __syncthreads();
+    if (S::INPLACE && tid == 0) issue(tile + 2 * (int64_t)gridDim.x, buf);  // regrouped tile written out
   }
 }
 

@@ -437,7 +437,8 @@ void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiAp
   kA<<<c.persistent_grid(m, SA::T, 2), BKA_BLOCK, SA::bytes(), c.s>>>(src, m, gshift, coarse_cur, mid);
   c.launched();
   c.begin(KK_MI_SPLIT_B);
-  kB<<<c.persistent_grid(m, SB::T, 2), BKB_BLOCK, SB::bytes(), c.s>>>(AosRecSrc<3>{mid.r}, m, gshift, fine_cur, fin);
+  kB<<<c.persistent_grid(m, SB::T, BKB_PER_SM), BKB_BLOCK, SB::bytes(), c.s>>>(AosRecSrc<3>{mid.r}, m, gshift,
+                                                                                 fine_cur, fin);
   c.launched();
   DMST_CUDA(cudaFuncSetAttribute(k_mi_apply_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * FB));  // 64 KB
   c.begin(KK_MI_APPLY);
@@ -651,8 +652,8 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
         LinkSortedSrc{fin.keys, fin.pay, w.smi_all}, n, gshift, coarse_cur, Recs{recA});
     c.launched();
     c.begin(KK_LINK_SPLIT);
-    kB<<<c.persistent_grid(n, LB::T, 2), BKB_BLOCK, LB::bytes(), c.s>>>(AosRecSrc<2>{recA}, n, gshift, fine_cur,
-                                                                        Recs{recB});
+    kB<<<c.persistent_grid(n, LB::T, BKB_PER_SM), BKB_BLOCK, LB::bytes(), c.s>>>(AosRecSrc<2>{recA}, n, gshift,
+                                                                                 fine_cur, Recs{recB});
     c.launched();
     c.begin(KK_LINK_APPLY);
     k_link_apply<<<nf, 512, 0, c.s>>>((const uint2*)recB, n, edge_parent);

@@ -24,6 +24,8 @@
 //     stable radix sort on the chain key (payload = rank), k_link.
 #include <algorithm>
 #include <cstdio>
+#include <mutex>
+#include <unordered_map>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -240,6 +242,17 @@ struct Ctx {
     if (profile) DMST_CUDA(cudaEventRecord(ev.back().b, s));
   }
   void collect(dmst_stats* st) {
+    if (getenv("DMST_TIMELINE") && !ev.empty()) {  // debugging aid: kernel start/end vs the first event
+      float prev_end = 0.f;
+      for (Ev& e : ev) {
+        float a = 0.f, b = 0.f;
+        cudaEventElapsedTime(&a, ev[0].a, e.a);
+        cudaEventElapsedTime(&b, ev[0].a, e.b);
+        fprintf(stderr, "TL %-18s start %9.3f end %9.3f dur %8.3f gap %8.3f\n", kKernelNames[e.kind], a, b, b - a,
+                a - prev_end);
+        prev_end = b;
+      }
+    }
     for (Ev& e : ev) {
       float ms = 0.f;
       if (st && cudaEventElapsedTime(&ms, e.a, e.b) == cudaSuccess) {
@@ -297,13 +310,29 @@ struct Ctx {
   }
 };
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and device
+// (a host API call per launch would add latency inside the level loop).
+template <typename K>
+void smem_attr(K* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> done[64];
+  int dev = 0;
+  DMST_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = done[dev & 63][(const void*)kernel];
+  if (cur < bytes) {
+    DMST_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    cur = bytes;
+  }
+}
+
 // One radix pass: upsweep (per-chunk digit counts), chunk scan, downsweep.
 template <typename K, int PW, int BLOCK, int ITEMS, int MINB, int BITS, class Loader, class Emitter>
 int64_t radix_pass(Ctx& c, int kind, int64_t n, int shift, Loader ld, Emitter em) {
   using S = DownSmem<K, PW, BLOCK, ITEMS, Loader, Emitter, BITS>;
   constexpr int T = S::T;
   auto kern = k_downsweep<K, PW, BLOCK, ITEMS, MINB, Loader, Emitter, BITS>;
-  DMST_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes()));
+  smem_attr(kern, (int)S::bytes());
   SweepArgs a;
   a.n = n;
   a.shift = shift;
@@ -418,7 +447,7 @@ void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiAp
   uint32_t* fine_cur = fine_base + (nf + 2);
   uint32_t* coarse_cur = fine_cur + (nf + 2);
   c.zero(counts, 4 * (nf + 1));
-  DMST_CUDA(cudaFuncSetAttribute(k_fine_hist<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * FH_WINDOW));
+  smem_attr(k_fine_hist<Src>, 4 * FH_WINDOW);
   for (uint32_t flo = 0; flo < nf; flo += FH_WINDOW) {
     c.begin(KK_MI_HIST);
     k_fine_hist<Src><<<c.persistent_grid(m, 256, 3), 256, 4 * FH_WINDOW, c.s>>>(src, m, flo, nf, counts);
@@ -431,8 +460,8 @@ void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiAp
   using SB = SplitSmem<AosRecSrc<3>, BKB_BLOCK, BKB_ITEMS, BKB_SPAN>;
   auto kA = k_split<false, Src, BKA_BLOCK, BKA_ITEMS, 256>;
   auto kB = k_split<true, AosRecSrc<3>, BKB_BLOCK, BKB_ITEMS, BKB_SPAN>;
-  DMST_CUDA(cudaFuncSetAttribute(kA, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SA::bytes()));
-  DMST_CUDA(cudaFuncSetAttribute(kB, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SB::bytes()));
+  smem_attr(kA, (int)SA::bytes());
+  smem_attr(kB, (int)SB::bytes());
   c.begin(KK_MI_SPLIT_A);
   kA<<<c.persistent_grid(m, SA::T, 2), BKA_BLOCK, SA::bytes(), c.s>>>(src, m, gshift, coarse_cur, mid);
   c.launched();
@@ -440,7 +469,7 @@ void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiAp
   kB<<<c.persistent_grid(m, SB::T, BKB_PER_SM), BKB_BLOCK, SB::bytes(), c.s>>>(AosRecSrc<3>{mid.r}, m, gshift,
                                                                                  fine_cur, fin);
   c.launched();
-  DMST_CUDA(cudaFuncSetAttribute(k_mi_apply_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * FB));  // 64 KB
+  smem_attr(k_mi_apply_smem, 8 * FB);  // 64 KB
   c.begin(KK_MI_APPLY);
   k_mi_apply_smem<<<nf, 512, 8 * FB, c.s>>>(fin, fine_base, nv, out);
   c.launched();
@@ -456,6 +485,10 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
   Workspace& w = c.w;
   uint32_t* misc = w.small + SM_MISC;
 
+  // level-loop counters and look-back words start at zero (later views: reset
+  // by k_select_edges once the host has read them)
+  c.zero(misc + 1, 4 * 15);
+  c.zero(w.sel_status, 8 * (cdiv(n / 16 + 1, LS_TILE) + 2));
   // maxIncident + V1 of the input view: 2n records generated from euv0
   c.zero(w.cnt2, 4 * (n / 16 + 2));
   mi_buckets(c, EdgeRecSrc{w.euv0}, 2 * n, nv, recs_at(w.R, 2 * n), recs_at(w.R + 24 * n, 2 * n),
@@ -486,9 +519,8 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     // leaf numbering + kind counts
     const int64_t words = n_k / 16 + 1;
     const unsigned ls_tiles = grid_for(words, LS_TILE);
-    c.zero(w.sel_status, 8 * (size_t)ls_tiles);
-    c.zero(misc + MISC_COUNTS, 8);
-    c.zero(misc + MISC_LSCTR, 4);
+    // look-back words and level counters were zeroed before the loop (view 0)
+    // or by the previous view's k_select_edges
     c.begin(KK_LEAFSCAN);
     k_leafscan<<<ls_tiles, 256, 0, c.s>>>(words, n_k, w.cnt2, w.kw, w.apre, w.sel_status, misc + MISC_LSCTR,
                                          misc + MISC_COUNTS);
@@ -498,18 +530,16 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     // view 0: plain vertex map; views >= 1: packed walk table (stride 2)
     int32_t* vm = level == 0 ? w.vm_all : (int32_t*)(w.lvl_all + lt.soff[level]);
     const int vs = level == 0 ? 1 : 2;
-    c.zero(misc + MISC_ACTIVE0, 12);
-    c.zero(misc + MISC_NONRUL, 4);
     c.begin(KK_V2);
     k_v2<<<grid_for(nv_k, EW_BLOCK), EW_BLOCK, 0, c.s>>>(nv_k, mi_k, w.kw, vm,
                                                          level == 0 ? nullptr : w.smi_all + lt.soff[level],
                                                          lists[0], lcnt[0], lists[3], lcnt[3]);
     c.launched();
-    uint32_t counts[4];
-    c.to_host(counts, misc + MISC_COUNTS, 8);
-    c.to_host(counts + 2, lcnt[0], 4);
-    c.to_host(counts + 3, lcnt[3], 4);
+    uint32_t mw[6];  // misc words 1..6: ACTIVE0, ACTIVE1, ACTIVE2, COUNTS[2], NONRUL
+    static_assert(MISC_ACTIVE0 == 1 && MISC_COUNTS == 4 && MISC_NONRUL == 6, "readback layout");
+    c.to_host(mw, misc + 1, sizeof(mw));
     c.sync();
+    const uint32_t counts[4] = {mw[3], mw[4], mw[0], mw[5]};
     const int64_t n_leaf = counts[0], n_chain = counts[1];
     const int64_t n_alpha = n_k - n_leaf - n_chain;
     if (st) {
@@ -571,6 +601,9 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     es.mi64_next = direct ? mi_next : nullptr;
     es.x1 = level == 0 ? w.x1 : nullptr;
     es.level = (int8_t)level;
+    es.reset_misc = misc + 1;
+    es.reset_status = w.sel_status;
+    es.n_status = 2 * (int64_t)ls_tiles;
     c.begin(KK_SELECT_EDGES);
     k_select_edges<<<c.persistent_grid(n_k, SEL_BLOCK * SEL_U, 8), SEL_BLOCK, 0, c.s>>>(n_k, es);
     c.launched();
@@ -645,8 +678,8 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     using LB = SplitSmem<AosRecSrc<2>, BKB_BLOCK, BKB_ITEMS, BKB_SPAN>;
     auto kA = k_split<false, LinkSortedSrc, BKA_BLOCK, BKA_ITEMS, 256>;
     auto kB = k_split<true, AosRecSrc<2>, BKB_BLOCK, BKB_ITEMS, BKB_SPAN>;
-    DMST_CUDA(cudaFuncSetAttribute(kA, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LA::bytes()));
-    DMST_CUDA(cudaFuncSetAttribute(kB, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LB::bytes()));
+    smem_attr(kA, (int)LA::bytes());
+    smem_attr(kB, (int)LB::bytes());
     c.begin(KK_LINK_SPLIT);
     kA<<<c.persistent_grid(n, LA::T, 2), BKA_BLOCK, LA::bytes(), c.s>>>(
         LinkSortedSrc{fin.keys, fin.pay, w.smi_all}, n, gshift, coarse_cur, Recs{recA});

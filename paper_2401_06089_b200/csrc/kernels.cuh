@@ -361,10 +361,18 @@ struct EdgeSel {
   unsigned long long* __restrict__ mi64_next;  // direct mode (null => bucketed from euv_next)
   int32_t* __restrict__ x1;          // view 0 only
   int8_t level;
+  uint32_t* __restrict__ reset_misc;   // level counters (15 words) zeroed for the next view
+  uint32_t* __restrict__ reset_status; // leafscan look-back words zeroed for the next view
+  int64_t n_status;
 };
 
 constexpr int SEL_U = 4;  // edges per thread per iteration (gathers in flight together)
 __global__ void __launch_bounds__(SEL_BLOCK) k_select_edges(int64_t n, EdgeSel es) {
+  {  // the host has read this view's counters: clear them for the next view
+    const int64_t g = (int64_t)blockIdx.x * SEL_BLOCK + threadIdx.x;
+    for (int64_t i = g; i < es.n_status; i += (int64_t)gridDim.x * SEL_BLOCK) es.reset_status[i] = 0u;
+    if (g < 15) es.reset_misc[g] = 0u;
+  }
   const int64_t stride = (int64_t)gridDim.x * SEL_BLOCK * SEL_U;
   for (int64_t b0 = (int64_t)blockIdx.x * SEL_BLOCK * SEL_U + threadIdx.x; b0 < n; b0 += stride) {
     bool alpha[SEL_U], in[SEL_U], need[SEL_U];

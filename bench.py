@@ -514,7 +514,7 @@ def main() -> None:
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="config4")
     ap.add_argument("--n", type=int, default=None, help="override the workload's edge count")
     ap.add_argument("--cpu-sample", type=int, default=8_000_000)
-    ap.add_argument("--streams", type=int, default=4, help="concurrent trees per GPU (multi-tree workloads)")
+    ap.add_argument("--streams", type=int, default=8, help="concurrent trees per GPU (multi-tree workloads)")
     ap.add_argument("--ref-sample", type=int, default=2_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-depth", type=int, default=2, help="builds in flight in the e2e leg")

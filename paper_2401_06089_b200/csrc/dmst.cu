@@ -40,7 +40,7 @@ namespace dmst {
 constexpr int S1_BLOCK = 512, S1_ITEMS = 8, S1_MINB = 1;
 // Chain sort: u32 key + 1-word payload.
 constexpr int S2_BLOCK = 512, S2_ITEMS = 16, S2_MINB = 1, S2_BITS = 9;
-constexpr int64_t kDirectMiBytes = 24ll << 20;  // direct scatter-max below this mi64 size
+constexpr int64_t kDirectMiBytes = 64ll << 20;  // direct scatter-max below this mi64 size
 
 enum KernelKind {
   KK_SORT1_HIST, KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL, KK_MI_HIST, KK_MI_SPLIT_A, KK_MI_SPLIT_B,

@@ -170,6 +170,43 @@ def test_host_buffer_entry_point(builder, shape, n):
         assert res.stats.view_kind_counts() == list(exp.view_kind_counts)
 
 
+def _stress_tree(kind: str, n: int, seed: int):
+    """Shapes that stress the bucketed / chased / sorted stages at scale."""
+    rng = np.random.default_rng(seed)
+    nv = n + 1
+    ids = rng.permutation(nv).astype(np.int64)          # scatter vertex ids
+    child = np.arange(1, nv, dtype=np.int64)
+    if kind == "star":                                  # one hub: every record in one vertex bucket
+        par = np.zeros(n, np.int64)
+    elif kind == "hubs":                                # 16 hubs
+        par = rng.integers(0, np.minimum(child, 16))
+    elif kind == "binary":                              # balanced binary tree
+        par = (child - 1) // 2
+    elif kind == "broom":                               # long handle + bristles
+        h = nv // 2
+        par = np.where(child < h, child - 1, rng.integers(h - 64, h, n))
+    else:                                               # random attachment
+        par = rng.integers(0, child)
+    u, v = ids[par], ids[child]
+    if kind in ("binary", "star"):
+        w = rng.integers(0, 7, n).astype(np.float64)      # heavy ties
+    elif kind == "equal":
+        w = np.full(n, 2.5)
+    else:
+        w = rng.random(n)
+    perm = rng.permutation(n)
+    return nv, u[perm].astype(np.int32), v[perm].astype(np.int32), w[perm]
+
+
+@pytest.mark.parametrize("kind", ["star", "hubs", "binary", "broom", "equal"])
+def test_stress_shapes_vs_oracle(builder, kind):
+    nv, u, v, w = _stress_tree(kind, 1_500_000, seed=11)
+    exp = O.build(nv, u, v, w)
+    res = builder.build(nv, u, v, w)
+    assert_matches(res, exp.orig_of, exp.heights, exp.edge_parent, exp.vertex_parent,
+                   exp.view_kind_counts)
+
+
 def test_drop_in_functions():
     from paper_2401_06089_b200 import pandora_b200, rank_edges_b200, Dendrogram
     from types import SimpleNamespace

@@ -657,13 +657,15 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     k_link<<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(n, keys, nullptr, w.smi_all, edge_parent);
     c.launched();
   } else {
-    uint32_t* base = (uint32_t*)w.R;
-    uint32_t* const bufK[2] = {base + n, base + 3 * n};
-    uint32_t* const bufP[2] = {base + 2 * n, base + 4 * n};
+    // packed (chain key << 32 | rank) items: ping-pong R[4n, 12n) / R[12n, 20n)
+    uint64_t* const bufK[2] = {(uint64_t*)(w.R + align_up(4 * n)), (uint64_t*)(w.R + align_up(12 * n))};
+    uint32_t* const bufP[2] = {nullptr, nullptr};
     const int lastb = ((int)shifts.size() - 1) % 2;
-    ArrayEmitter<uint32_t, 1> fin{bufK[lastb], bufP[lastb]};
-    run_sort<uint32_t, 1, S2_BLOCK, S2_ITEMS, S2_MINB, S2_BITS>(c, {KK_SORT2_PASS, KK_SORT2_PASS, KK_SORT2_PASS}, n,
-                                                             shifts, bufK, bufP, Sort2FirstLoader{keys}, fin);
+    ArrayEmitter<uint64_t, 0> fin{bufK[lastb], nullptr};
+    std::vector<int> shifts64(shifts);
+    for (int& x : shifts64) x += 32;
+    run_sort<uint64_t, 0, S2_BLOCK, S2_ITEMS, S2_MINB, S2_BITS>(c, {KK_SORT2_PASS, KK_SORT2_PASS, KK_SORT2_PASS}, n,
+                                                             shifts64, bufK, bufP, Sort2FirstLoader{keys}, fin);
     // (rank, parent) records grouped by 8192-rank window: R[20n, 28n) -> R[28n, 36n)
     uint32_t* recA = (uint32_t*)(w.R + align_up(20 * n));
     uint32_t* recB = (uint32_t*)(w.R + align_up(28 * n));
@@ -682,7 +684,7 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     smem_attr(kB, (int)LB::bytes());
     c.begin(KK_LINK_SPLIT);
     kA<<<c.persistent_grid(n, LA::T, 2), BKA_BLOCK, LA::bytes(), c.s>>>(
-        LinkSortedSrc{fin.keys, fin.pay, w.smi_all}, n, gshift, coarse_cur, Recs{recA});
+        LinkSortedSrc{(const unsigned long long*)fin.keys, w.smi_all}, n, gshift, coarse_cur, Recs{recA});
     c.launched();
     c.begin(KK_LINK_SPLIT);
     kB<<<c.persistent_grid(n, LB::T, BKB_PER_SM), BKB_BLOCK, LB::bytes(), c.s>>>(AosRecSrc<2>{recA}, n, gshift,

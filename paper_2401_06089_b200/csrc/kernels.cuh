@@ -478,19 +478,20 @@ k_walk(int64_t n, const int8_t* __restrict__ ret, const int32_t* __restrict__ x1
   }
 }
 
+// Chain sort items are packed 64-bit (chain key << 32 | rank): one array, so
+// a digit run of m items is one contiguous 8 m-byte run; the radix digits
+// sit at bit 32 + (chain-key digit offset).
 struct Sort2FirstLoader {
   static constexpr int NS = 1;
   __host__ __device__ static constexpr int sb(int) { return 4; }
   const uint32_t* __restrict__ keys;
   __device__ __forceinline__ const void* ptr(int) const { return keys; }
-  __device__ __forceinline__ uint32_t key(int64_t i) const { return ld_stream(keys + i); }
-  __device__ __forceinline__ void load(int64_t i, uint32_t& k, Vals<1>& v) const {
-    k = ld_stream(keys + i);
-    v.w[0] = (uint32_t)i;
+  __device__ __forceinline__ uint64_t key(int64_t i) const {
+    return ((uint64_t)ld_stream(keys + i) << 32) | (uint32_t)i;
   }
-  __device__ __forceinline__ void get(char* const* st, int li, int64_t i, uint32_t& k, Vals<1>& v) const {
-    k = reinterpret_cast<const uint32_t*>(st[0])[li];
-    v.w[0] = (uint32_t)i;
+  __device__ __forceinline__ void load(int64_t i, uint64_t& k, Vals<0>&) const { k = key(i); }
+  __device__ __forceinline__ void get(char* const* st, int li, int64_t i, uint64_t& k, Vals<0>&) const {
+    k = ((uint64_t)reinterpret_cast<const uint32_t*>(st[0])[li] << 32) | (uint32_t)i;
   }
 };
 
@@ -505,35 +506,32 @@ struct Sort2FirstLoader {
 // shared memory with coalesced stores.  Window f holds exactly the ranks
 // [8192 f, 8192 (f + 1)), so all bucket offsets are static.
 struct LinkSortedSrc {
-  static constexpr int RW = 2, NS = 2;
-  __host__ __device__ static constexpr int sb(int) { return 4; }
-  const uint32_t* __restrict__ keys;  // sorted chain keys
-  const uint32_t* __restrict__ vals;  // ranks in (key, rank) order
+  static constexpr int RW = 2, NS = 1;
+  __host__ __device__ static constexpr int sb(int) { return 8; }  // one sorted 8-B item per record
+  const unsigned long long* __restrict__ items;  // sorted (chain key << 32 | rank)
   const int32_t* __restrict__ smi_all;
-  __device__ __forceinline__ const void* ptr(int s) const { return s == 0 ? (const void*)keys : (const void*)vals; }
+  __device__ __forceinline__ const void* ptr(int) const { return items; }
   __device__ __forceinline__ uint32_t parent(uint32_t key, uint32_t pkey, uint32_t pval, bool first) const {
     if (!first && pkey == key) return pval;
     return key == 0 ? 0xffffffffu : (uint32_t)smi_all[key - 1];
   }
   __device__ __forceinline__ void get(const unsigned char* const* st, int li, int64_t i, uint32_t (&r)[2]) const {
-    const uint32_t* k = reinterpret_cast<const uint32_t*>(st[0]);
-    const uint32_t* v = reinterpret_cast<const uint32_t*>(st[1]);
-    const uint32_t key = k[li];
-    r[0] = v[li];
-    const uint32_t pk = li > 0 ? k[li - 1] : (i > 0 ? __ldg(keys + i - 1) : 0u);
-    const uint32_t pv = li > 0 ? v[li - 1] : (i > 0 ? __ldg(vals + i - 1) : 0u);
-    r[1] = parent(key, pk, pv, i == 0);
+    const unsigned long long* k = reinterpret_cast<const unsigned long long*>(st[0]);
+    const unsigned long long it = k[li];
+    const unsigned long long pv = li > 0 ? k[li - 1] : (i > 0 ? __ldg(items + i - 1) : 0ull);
+    r[0] = (uint32_t)it;
+    r[1] = parent((uint32_t)(it >> 32), (uint32_t)(pv >> 32), (uint32_t)pv, i == 0);
   }
   __device__ __forceinline__ uint32_t staged_vertex(const unsigned char* const* st, int li, int64_t) const {
-    return reinterpret_cast<const uint32_t*>(st[1])[li];
+    return (uint32_t)reinterpret_cast<const unsigned long long*>(st[0])[li];
   }
   __device__ __forceinline__ void load(int64_t i, uint32_t (&r)[2]) const {
-    const uint32_t key = __ldg(keys + i);
-    r[0] = __ldg(vals + i);
-    const uint32_t pk = i > 0 ? __ldg(keys + i - 1) : 0u, pv = i > 0 ? __ldg(vals + i - 1) : 0u;
-    r[1] = parent(key, pk, pv, i == 0);
+    const unsigned long long it = __ldg(items + i);
+    const unsigned long long pv = i > 0 ? __ldg(items + i - 1) : 0ull;
+    r[0] = (uint32_t)it;
+    r[1] = parent((uint32_t)(it >> 32), (uint32_t)(pv >> 32), (uint32_t)pv, i == 0);
   }
-  __device__ __forceinline__ uint32_t vertex(int64_t i) const { return __ldg(vals + i); }
+  __device__ __forceinline__ uint32_t vertex(int64_t i) const { return (uint32_t)__ldg(items + i); }
 };
 
 // Static bucket starts: coarse bucket c = [c << (FB_BITS + gshift)), fine f = [f << FB_BITS).

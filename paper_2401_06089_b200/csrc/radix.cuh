@@ -34,6 +34,10 @@ template <int VW>
 struct Vals {
   uint32_t w[VW];
 };
+template <>
+struct Vals<0> {  // key-only items
+  uint32_t w[1];
+};
 
 template <int BITS = kRadixBits, typename K>
 __device__ __forceinline__ uint32_t digit_of(K key, int shift) {
@@ -95,7 +99,7 @@ __device__ __forceinline__ bool aligned16(const void* p) { return ((uintptr_t)p 
 // the scattered writes of uniformly distributed digits sector-efficient.
 template <typename K, int PW>
 struct ArrayLoader {
-  static constexpr int NS = 2;
+  static constexpr int NS = PW > 0 ? 2 : 1;
   __host__ __device__ static constexpr int sb(int s) { return s == 0 ? (int)sizeof(K) : 4 * PW; }
   const K* __restrict__ keys;
   const uint32_t* __restrict__ pay;
@@ -108,14 +112,16 @@ struct ArrayLoader {
   }
   __device__ __forceinline__ void get(char* const* st, int li, int64_t, K& k, Vals<PW>& v) const {
     k = reinterpret_cast<const K*>(st[0])[li];
-    const uint32_t* p = reinterpret_cast<const uint32_t*>(st[1]) + li * PW;
-    if constexpr (PW == 2) {
-      const uint2 x = *reinterpret_cast<const uint2*>(p);
-      v.w[0] = x.x;
-      v.w[1] = x.y;
-    } else {
+    if constexpr (PW > 0) {
+      const uint32_t* p = reinterpret_cast<const uint32_t*>(st[1]) + li * PW;
+      if constexpr (PW == 2) {
+        const uint2 x = *reinterpret_cast<const uint2*>(p);
+        v.w[0] = x.x;
+        v.w[1] = x.y;
+      } else {
 #pragma unroll
-      for (int q = 0; q < PW; ++q) v.w[q] = p[q];
+        for (int q = 0; q < PW; ++q) v.w[q] = p[q];
+      }
     }
   }
 };
@@ -529,7 +535,7 @@ k_downsweep(SweepArgs a, Loader ld, Emitter em) {
 template <typename K, int PW, int BLOCK, class Loader, class Emitter>
 __global__ void __launch_bounds__(BLOCK) k_identity_pass(int64_t n, Loader ld, Emitter em) {
   __shared__ K skeys[BLOCK];
-  __shared__ uint32_t spay[BLOCK * PW];
+  __shared__ uint32_t spay[BLOCK * (PW > 0 ? PW : 1)];
   __shared__ uint32_t gofs[kRadix];
   __shared__ uint32_t lstart[kRadix + 1];
   __shared__ typename Emitter::State est;

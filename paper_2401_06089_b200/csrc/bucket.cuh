@@ -19,6 +19,7 @@ constexpr int FB_BITS = 13;                  // fine bucket = 8192 vertices (64 
 constexpr int FB = 1 << FB_BITS;
 // multisplit geometry: pass A (coarse, <= 256 buckets) and pass B (fine)
 constexpr int BKA_BLOCK = 512, BKA_ITEMS = 8;   // 4096 records per sub-tile
+constexpr int BKA_PER_SM = 2;                   // pass-A CTAs per SM
 constexpr int BKB_BLOCK = 512, BKB_ITEMS = 4;   // 2048 records per sub-tile
 constexpr int BKB_SPAN = 1024;                  // max fine buckets a pass-B sub-tile may touch
 constexpr int BKB_PER_SM = 4;                   // pass-B CTAs per SM (in-place regrouping: ~56 KB smem)

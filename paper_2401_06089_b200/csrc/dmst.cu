@@ -463,7 +463,7 @@ void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiAp
   smem_attr(kA, (int)SA::bytes());
   smem_attr(kB, (int)SB::bytes());
   c.begin(KK_MI_SPLIT_A);
-  kA<<<c.persistent_grid(m, SA::T, 2), BKA_BLOCK, SA::bytes(), c.s>>>(src, m, gshift, coarse_cur, mid);
+  kA<<<c.persistent_grid(m, SA::T, BKA_PER_SM), BKA_BLOCK, SA::bytes(), c.s>>>(src, m, gshift, coarse_cur, mid);
   c.launched();
   c.begin(KK_MI_SPLIT_B);
   kB<<<c.persistent_grid(m, SB::T, BKB_PER_SM), BKB_BLOCK, SB::bytes(), c.s>>>(AosRecSrc<3>{mid.r}, m, gshift,
@@ -683,7 +683,7 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     smem_attr(kA, (int)LA::bytes());
     smem_attr(kB, (int)LB::bytes());
     c.begin(KK_LINK_SPLIT);
-    kA<<<c.persistent_grid(n, LA::T, 2), BKA_BLOCK, LA::bytes(), c.s>>>(
+    kA<<<c.persistent_grid(n, LA::T, BKA_PER_SM), BKA_BLOCK, LA::bytes(), c.s>>>(
         LinkSortedSrc{(const unsigned long long*)fin.keys, w.smi_all}, n, gshift, coarse_cur, Recs{recA});
     c.launched();
     c.begin(KK_LINK_SPLIT);

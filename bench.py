@@ -108,7 +108,11 @@ def load_peaks() -> tuple[float, str]:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region.
+
+    The sampler process is started (and its first line awaited) before the
+    region opens; only samples that arrive while the region is open are kept
+    (plus the first one after it, so a short region still gets a reading)."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
@@ -116,8 +120,11 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
+        self.lines: list[tuple[float, str]] = []
+        self.t0 = self.t1 = None
 
-    def __enter__(self):
+    def start(self):
+        import threading
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
@@ -125,26 +132,40 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
+            return self
+        first = threading.Event()
+
+        def reader():
+            for line in self.proc.stdout:
+                self.lines.append((time.monotonic(), line))
+                first.set()
+        threading.Thread(target=reader, daemon=True).start()
+        first.wait(timeout=10)
+        return self
+
+    def __enter__(self):
+        if self.proc is None:
+            self.start()
+        self.t0 = time.monotonic()
         return self
 
     def __exit__(self, *exc):
-        self.out = ""
+        self.t1 = time.monotonic()
+        deadline = self.t1 + 0.5
+        while time.monotonic() < deadline and not any(t > self.t1 for t, _ in self.lines):
+            time.sleep(0.01)
         if self.proc is not None:
             self.proc.terminate()
             try:
-                self.out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
 
     def summary(self) -> dict:
-        rows = []
-        for line in (getattr(self, "out", "") or "").splitlines():
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 7:
-                try:
-                    rows.append(parts)
-                except Exception:
-                    pass
+        keep = [ln for t, ln in self.lines if self.t0 is not None and self.t0 <= t <= self.t1]
+        after = [ln for t, ln in self.lines if self.t1 is not None and t > self.t1][:1]
+        rows = [[p.strip() for p in ln.split(",")] for ln in keep + after]
+        rows = [r for r in rows if len(r) >= 7]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
@@ -154,7 +175,7 @@ class ClockSampler:
                           and "Not" not in r[3 + i]})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(rows)}
+                "samples": len(rows), "samples_in_region": len(keep)}
 
 
 def dist_setup():
@@ -344,7 +365,8 @@ def run_b200(args) -> None:
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev.index) as clk:
+    clk = ClockSampler(dev.index).start()
+    with clk:
         e0.record(stream)
         for _ in range(args.steps):
             step(profile=True)

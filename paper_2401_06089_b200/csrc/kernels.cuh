@@ -447,6 +447,7 @@ __global__ void __launch_bounds__(BLOCK)
 k_walk(int64_t n, const int8_t* __restrict__ ret, const int32_t* __restrict__ x1, const int2* __restrict__ lvl,
        const __grid_constant__ LevelTable lt, uint32_t* __restrict__ keys, uint32_t* __restrict__ and_or) {
   uint32_t ka = ~0u, ko = 0u;
+  const uint64_t pol = l2_keep_policy();
   const int64_t stride = (int64_t)gridDim.x * BLOCK;
   for (int64_t e0 = (int64_t)blockIdx.x * BLOCK; e0 < n; e0 += stride) {
     const int64_t e = e0 + threadIdx.x;
@@ -456,7 +457,16 @@ k_walk(int64_t n, const int8_t* __restrict__ ret, const int32_t* __restrict__ x1
       if (r < lt.L) {
         int32_t x = __ldcs(x1 + e);  // view-1 supervertex
         for (int k = 1;; ++k) {
-          const int2 t = lvl[lt.soff[k] + x];
+          // view 1's table is far larger than L2 (normal policy); the
+          // deeper, smaller tables are kept resident (evict_last)
+          const int2* pt = lvl + lt.soff[k] + x;
+          int2 t;
+          if (k == 1) {
+            t = *pt;
+          } else {
+            const uint2 q = ld_keep2(reinterpret_cast<const uint2*>(pt), pol);
+            t = make_int2((int)q.x, (int)q.y);
+          }
           if (k > r && t.y >= 0 && t.y < (int32_t)e) {
             key = (uint32_t)(1 + lt.soff[k] + x);
             break;

@@ -443,6 +443,21 @@ def run_b200(args) -> None:
     if len(trees) == 1 and not np.array_equal(he0[:n0].numpy(), outs[0].edge_parent.cpu().numpy()):
         raise RuntimeError("e2e output mismatch")
 
+    # ---------------- input validation (not in the timed scope) ----------------
+    from paper_2401_06089_b200.api import _validate
+    nv0, du0, dv0, dw0 = dev_trees[0]
+    vb = e2e_builders[0]
+    _validate(vb, nv0, du0, dv0, dw0)
+    vtimes = []
+    for _ in range(3):
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(torch.cuda.current_stream(dev))
+        _validate(vb, nv0, du0, dv0, dw0)
+        g1.record(torch.cuda.current_stream(dev))
+        torch.cuda.synchronize(dev)
+        vtimes.append(g0.elapsed_time(g1))
+    validate_ms = statistics.median(vtimes)
+
     # ---------------- max over ranks (time), sum over ranks (work) ----------------
     ms_step, e2e_ms, e2e_serial_ms = reduce_max([ms_step, e2e_ms, e2e_serial_ms], device=dev)
     (edges_total,) = reduce_sum([float(edges_rank)], device=dev)
@@ -510,6 +525,9 @@ def run_b200(args) -> None:
                     "serial": {"value": edges_total / (e2e_serial_ms * 1e-3), "ms_per_step": e2e_serial_ms,
                                "builds_in_flight": 1}},
             "roofline": roof,
+            "validation": {"ms": validate_ms, "edges_per_s": int(dev_trees[0][1].shape[0]) / (validate_ms * 1e-3),
+                           "what": "weighted_tree checks (tree_core.py:110-139) on the device, valid input: "
+                                   "one scan + lock-free union-find; outside the timed build scope like the reference"},
             "pipeline_roofline": {"bound": "hbm", "achieved": pipe_ach, "peak": peak, "unit": "GB/s",
                                   "frac": pipe_ach / peak, "algorithmic_bytes_per_step": B,
                                   "model": "403 n + 98 S (SURVEY.md 8d)", "peak_source": peak_src,

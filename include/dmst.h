@@ -123,6 +123,33 @@ int dmst_build_debug(const int32_t* u, const int32_t* v, const double* w, int64_
                      int32_t* chain_level, void* workspace, size_t workspace_bytes,
                      void* stream);
 
+/* Tree validation: the checks of the reference's `weighted_tree`
+ * (tree_core.py:110-139), on the device, in the same order:
+ *   DMST_TREE_TOO_SMALL   n_vertices < 2                       (:116-117)
+ *   DMST_TREE_EDGE_COUNT  n_edges != n_vertices - 1            (:118-121)
+ *   DMST_TREE_NONFINITE   non-finite weight; *bad_edge = first (:124-126)
+ *   DMST_TREE_NEGATIVE_ID negative vertex id                   (:127-128)
+ *   DMST_TREE_ID_RANGE    vertex id >= n_vertices              (:129-130)
+ *   DMST_TREE_SELF_LOOP   u == v; *bad_edge = first            (:131-133)
+ *   DMST_TREE_DUPLICATE   duplicate undirected edge            (:134-136)
+ *   DMST_TREE_NOT_A_TREE  disconnected or cyclic               (:137-138)
+ * *error_kind = DMST_TREE_OK (0) for a valid tree.  u, v, w are DEVICE
+ * pointers, error_kind / bad_edge HOST pointers; workspace as for
+ * dmst_build.  Returns 0 when the check ran (whatever its verdict),
+ * DMST_EINVAL / DMST_ECUDA otherwise. */
+#define DMST_TREE_OK 0
+#define DMST_TREE_TOO_SMALL 1
+#define DMST_TREE_EDGE_COUNT 2
+#define DMST_TREE_NONFINITE 3
+#define DMST_TREE_NEGATIVE_ID 4
+#define DMST_TREE_ID_RANGE 5
+#define DMST_TREE_SELF_LOOP 6
+#define DMST_TREE_DUPLICATE 7
+#define DMST_TREE_NOT_A_TREE 8
+int dmst_validate(const int32_t* u, const int32_t* v, const double* w, int64_t n_edges, int64_t n_vertices,
+                  int32_t* error_kind, int64_t* bad_edge, void* workspace, size_t workspace_bytes,
+                  void* stream);
+
 /* Message for the last non-zero return on this thread ("" if none). */
 const char* dmst_last_error(void);
 

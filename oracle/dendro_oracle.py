@@ -305,3 +305,41 @@ def dendrogram_bottom_up(r: Ranked) -> tuple[np.ndarray, np.ndarray]:
         parent[b] = a
         latest[find(u[rank])] = rank
     return edge_parent, vertex_parent
+
+
+# ------------------------------------------------------------ validation
+class TreeFormatError(ValueError):
+    pass
+
+
+def weighted_tree(num_vertices: int, u, v, w):
+    """Restates weighted_tree (tree_core.py:110-139): the same checks in the
+    same order with the same messages; returns (num_vertices, u, v, w) with
+    the reference's dtypes.  Connectivity by the C union-find (uf_roots)."""
+    u = np.ascontiguousarray(u, dtype=np.int64)
+    v = np.ascontiguousarray(v, dtype=np.int64)
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    n = u.shape[0]
+    if num_vertices < 2:                                              # :116-117
+        raise TreeFormatError("a tree needs at least 2 vertices")
+    if n != num_vertices - 1:                                         # :118-121
+        raise TreeFormatError(f"edge count {n} != numVertices - 1 = {num_vertices - 1}")
+    if v.shape[0] != n or w.shape[0] != n:                            # :122-123
+        raise TreeFormatError("edge arrays have mismatched lengths")
+    if not np.all(np.isfinite(w)):                                    # :124-126
+        bad = int(np.nonzero(~np.isfinite(w))[0][0])
+        raise TreeFormatError(f"non-finite weight on edge {bad}")
+    if u.min(initial=0) < 0 or v.min(initial=0) < 0:                  # :127-128
+        raise TreeFormatError("negative vertex id")
+    if max(u.max(initial=-1), v.max(initial=-1)) >= num_vertices:     # :129-130
+        raise TreeFormatError("vertex id out of range")
+    if np.any(u == v):                                                # :131-133
+        bad = int(np.nonzero(u == v)[0][0])
+        raise TreeFormatError(f"self-loop on edge {bad}")
+    key = np.minimum(u, v) * np.int64(num_vertices) + np.maximum(u, v)  # :134-136
+    if np.unique(key).shape[0] != n:
+        raise TreeFormatError("duplicate undirected edge")
+    roots = uf_roots(num_vertices, u, v)                              # :137-138 (_connected, :102-107)
+    if int(np.count_nonzero(roots == np.arange(num_vertices))) != 1:
+        raise TreeFormatError("input is disconnected or cyclic, not a tree")
+    return num_vertices, u, v, w

@@ -27,6 +27,7 @@ EXPORTS = (
     "dmst_rank_edges",
     "dmst_pandora",
     "dmst_build_debug",
+    "dmst_validate",
     "dmst_last_error",
     "dmst_kernel_name",
     "dmst_version",
@@ -96,6 +97,9 @@ def load() -> ctypes.CDLL:
     lib.dmst_rank_edges.restype = ctypes.c_int
     lib.dmst_pandora.argtypes = [vp, vp, i64, i64, vp, vp, ctypes.POINTER(DmstStats), vp, sz, vp]
     lib.dmst_pandora.restype = ctypes.c_int
+    lib.dmst_validate.argtypes = [vp, vp, vp, i64, i64, ctypes.POINTER(ctypes.c_int32),
+                                  ctypes.POINTER(ctypes.c_int64), vp, sz, vp]
+    lib.dmst_validate.restype = ctypes.c_int
     lib.dmst_last_error.argtypes = []
     lib.dmst_last_error.restype = ctypes.c_char_p
     lib.dmst_kernel_name.argtypes = [ctypes.c_int32]

@@ -63,6 +63,33 @@ class Dendrogram:
                 and np.array_equal(self.vertex_parent, other.vertex_parent))
 
 
+class TreeFormatError(ValueError):
+    """Mirror of ``dendromst.tree_core.TreeFormatError`` (raised by
+    :func:`weighted_tree_b200`; the reference's own class when importable)."""
+
+
+def _tree_format_error():
+    try:
+        from dendromst.tree_core import TreeFormatError as Ref  # type: ignore
+        return Ref
+    except Exception:
+        return TreeFormatError
+
+
+@dataclass(frozen=True)
+class WeightedTree:
+    """Mirror of ``dendromst.tree_core.WeightedTree`` (tree_core.py:20-36)."""
+    num_vertices: int
+    u: object
+    v: object
+    w: object
+    original_id: object
+
+    @property
+    def num_edges(self) -> int:
+        return int(self.u.shape[0])
+
+
 @dataclass(frozen=True)
 class RankedTree:
     """Mirror of ``dendromst.tree_core.RankedTree`` (tree_core.py:39-56)."""
@@ -295,6 +322,57 @@ class DendrogramBuilder:
             return ep, vp, st
 
 
+_TREE_MESSAGES = {  # tree_core.py:116-138, verbatim
+    1: "a tree needs at least 2 vertices",
+    2: "edge count {n} != numVertices - 1 = {nv1}",
+    3: "non-finite weight on edge {bad}",
+    4: "negative vertex id",
+    5: "vertex id out of range",
+    6: "self-loop on edge {bad}",
+    7: "duplicate undirected edge",
+    8: "input is disconnected or cyclic, not a tree",
+}
+
+
+def _validate(builder: "DendrogramBuilder", num_vertices: int, u, v, w) -> None:
+    """Raise the reference's TreeFormatError (same message) if (u, v, w) is
+    not a valid spanning tree on num_vertices vertices (weighted_tree,
+    tree_core.py:110-139), checked on the device by dmst_validate."""
+    err = _tree_format_error()
+    n, nv = int(u.shape[0]), int(num_vertices)
+    if nv < 2:
+        raise err(_TREE_MESSAGES[1])
+    if n != nv - 1:
+        raise err(_TREE_MESSAGES[2].format(n=n, nv1=nv - 1))
+    if v.shape[0] != n or w.shape[0] != n:
+        raise err("edge arrays have mismatched lengths")
+    dev = builder.device
+    wt = _as_dev(w, torch.float64, dev)
+    ids = []
+    for a in (u, v):  # int64 ids outside int32 are range errors decided on the host
+        t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+        if t.dtype != torch.int32:
+            lo, hi = (int(t.min()), int(t.max())) if n else (0, -1)
+            if lo < -(1 << 31) or hi >= (1 << 31):
+                ids = None
+                break
+        ids.append(_as_dev(t, torch.int32, dev))
+    kind = ctypes.c_int32(0)
+    bad = ctypes.c_int64(-1)
+    with torch.cuda.device(dev):
+        if ids is None:  # ids that do not fit int32: negative or out of range, after the weight check
+            finite = torch.isfinite(wt)
+            if not bool(finite.all()):
+                raise err(_TREE_MESSAGES[3].format(bad=int((~finite).nonzero()[0, 0])))
+            neg = any(int(torch.as_tensor(a).min()) < 0 for a in (u, v))
+            raise err(_TREE_MESSAGES[4] if neg else _TREE_MESSAGES[5])
+        ws = builder.workspace(n, nv)
+        _lib.check(builder.lib.dmst_validate(_ptr(ids[0]), _ptr(ids[1]), _ptr(wt), n, nv, ctypes.byref(kind),
+                                             ctypes.byref(bad), _ptr(ws), ws.numel(), builder._stream()))
+    if kind.value:
+        raise err(_TREE_MESSAGES[kind.value].format(n=n, nv1=nv - 1, bad=bad.value))
+
+
 _builders: dict[int, DendrogramBuilder] = {}
 
 
@@ -304,6 +382,22 @@ def _builder(device=None) -> DendrogramBuilder:
     if b is None:
         b = _builders[dev.index] = DendrogramBuilder(dev)
     return b
+
+
+def weighted_tree_b200(num_vertices: int, u, v, w, device=None) -> WeightedTree:
+    """Drop-in for ``weighted_tree`` (tree_core.py:110-139): validate on the
+    GPU, raise ``TreeFormatError`` with the reference's message, return the
+    tree with the reference's dtypes (int64 ids, float64 weights)."""
+    _validate(_builder(device), num_vertices, u, v, w)
+    n = int(u.shape[0])
+    cpu = lambda a, dt: (a.cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)).astype(dt)  # noqa: E731
+    return WeightedTree(int(num_vertices), cpu(u, np.int64), cpu(v, np.int64), cpu(w, np.float64),
+                        np.arange(n, dtype=np.int64))
+
+
+def validate_b200(num_vertices: int, u, v, w, device=None) -> None:
+    """Validation only (no host copies of the arrays)."""
+    _validate(_builder(device), num_vertices, u, v, w)
 
 
 def build_b200(num_vertices: int, u, v, w, device=None, debug: bool = False) -> BuildResult:

@@ -31,6 +31,7 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "validate.cuh"
 
 namespace dmst {
 
@@ -893,6 +894,98 @@ int dmst_pandora(const int32_t* ru, const int32_t* rv, int64_t n_edges, int64_t 
     c.sync();
     c.collect(stats);
     if (stats) stats->kernel_launches = c.launches;
+  });
+}
+
+int dmst_validate(const int32_t* u, const int32_t* v, const double* w, int64_t n_edges, int64_t n_vertices,
+                  int32_t* error_kind, int64_t* bad_edge, void* workspace, size_t workspace_bytes, void* stream) {
+  return guarded([&] {
+    if (!error_kind || !bad_edge) invalid("error_kind / bad_edge must be host pointers");
+    *error_kind = DMST_TREE_OK;
+    *bad_edge = -1;
+    // tree_core.py:116-121: sizes first
+    if (n_vertices < 2) {
+      *error_kind = DMST_TREE_TOO_SMALL;
+      return;
+    }
+    if (n_edges != n_vertices - 1) {
+      *error_kind = DMST_TREE_EDGE_COUNT;
+      return;
+    }
+    if (n_edges >= (int64_t(1) << 29)) invalid("n_edges must be < 2^29");
+    if (!u || !v || !w) invalid("null input pointer");
+    if (!workspace || workspace_bytes < carve(n_edges, n_vertices, nullptr).bytes) invalid("workspace too small");
+    const int64_t n = n_edges, nv = n_vertices;
+    Ctx c;
+    init_ctx(c, n, nv, workspace, stream, nullptr);
+    uint32_t* r = c.w.small + SM_MISC + 32;  // [0..3] checks, [4] roots, [5] duplicate flag
+    unsigned long long* ao = (unsigned long long*)(c.w.small + SM_MISC + 48);
+    const uint32_t rinit[6] = {0xffffffffu, 0u, 0u, 0xffffffffu, 0u, 0u};
+    const unsigned long long aoinit[2] = {~0ull, 0ull};
+    DMST_CUDA(cudaMemcpyAsync(r, rinit, sizeof(rinit), cudaMemcpyHostToDevice, c.s));
+    DMST_CUDA(cudaMemcpyAsync(ao, aoinit, sizeof(aoinit), cudaMemcpyHostToDevice, c.s));
+    c.begin(KK_OTHER);
+    k_validate_scan<<<c.persistent_grid(n, 256, 8), 256, 0, c.s>>>(u, v, w, n, nv, r, ao);
+    c.launched();
+    uint32_t h[4];
+    c.to_host(h, r, sizeof(h));
+    c.sync();
+    if (h[0] != 0xffffffffu) {  // :124-126
+      *error_kind = DMST_TREE_NONFINITE;
+      *bad_edge = h[0];
+      return;
+    }
+    if (h[1]) {  // :127-128
+      *error_kind = DMST_TREE_NEGATIVE_ID;
+      return;
+    }
+    if (h[2]) {  // :129-130
+      *error_kind = DMST_TREE_ID_RANGE;
+      return;
+    }
+    if (h[3] != 0xffffffffu) {  // :131-133
+      *error_kind = DMST_TREE_SELF_LOOP;
+      *bad_edge = h[3];
+      return;
+    }
+    // connectivity (:137-138).  n = nv - 1 edges and connected => a tree, so
+    // the duplicate check (:134-136) only has to run when this fails.
+    int32_t* p = c.w.vm_all;
+    c.begin(KK_OTHER);
+    k_cc_init<<<grid_for(nv, EW_BLOCK), EW_BLOCK, 0, c.s>>>(p, nv);
+    c.launched();
+    c.begin(KK_OTHER);
+    k_cc_hook<<<c.persistent_grid(n, 256, 8), 256, 0, c.s>>>(u, v, n, p);
+    c.launched();
+    c.begin(KK_OTHER);
+    k_cc_roots<<<c.persistent_grid(nv, 256, 8), 256, 0, c.s>>>(p, nv, r + 4);
+    c.launched();
+    uint32_t roots = 0;
+    c.to_host(&roots, r + 4, 4);
+    unsigned long long hao[2];
+    c.to_host(hao, ao, 16);
+    c.sync();
+    if (roots == 1) return;
+    // not a tree: duplicates first, as the reference reports them first
+    const std::vector<int> shifts = active_digits(hao[0], hao[1], 8, 64);
+    if (shifts.empty()) {  // every undirected key equal (n >= 2 edges => duplicate)
+      if (n >= 2) *error_kind = DMST_TREE_DUPLICATE;
+      else *error_kind = DMST_TREE_NOT_A_TREE;
+      return;
+    }
+    uint64_t* const bufK[2] = {(uint64_t*)c.w.R, (uint64_t*)(c.w.R + align_up(8 * n))};
+    uint32_t* const bufP[2] = {nullptr, nullptr};
+    const int lastb = ((int)shifts.size() - 1) % 2;
+    ArrayEmitter<uint64_t, 0> fin{bufK[lastb], nullptr};
+    run_sort<uint64_t, 0, S1_BLOCK, S1_ITEMS, S1_MINB, 8>(c, {KK_OTHER, KK_OTHER, KK_OTHER}, n, shifts, bufK, bufP,
+                                                         DupKeyLoader{u, v}, fin);
+    c.begin(KK_OTHER);
+    k_adjacent_equal<<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>((const unsigned long long*)fin.keys, n, r + 5);
+    c.launched();
+    uint32_t dup = 0;
+    c.to_host(&dup, r + 5, 4);
+    c.sync();
+    *error_kind = dup ? DMST_TREE_DUPLICATE : DMST_TREE_NOT_A_TREE;
   });
 }
 

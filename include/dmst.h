@@ -68,6 +68,8 @@ typedef struct dmst_stats {
   int32_t sort2_passes;                      /* digits sorted in the chain sort */
   int32_t jump_rounds;                       /* pointer-jumping rounds over all levels */
   int32_t kernel_launches;                   /* kernels this call enqueued */
+  int32_t want_chains;                       /* in: 1 = count the dendrogram chains */
+  int32_t num_chains;                        /* out: ChainAssignment.num_chains() (want_chains = 1) */
   float kernel_ms[DMST_MAX_KERNELS];         /* out (profile=1): device ms per kernel kind */
   int32_t kernel_calls[DMST_MAX_KERNELS];    /* out: launches per kernel kind */
 } dmst_stats;
@@ -149,6 +151,14 @@ int dmst_build_debug(const int32_t* u, const int32_t* v, const double* w, int64_
 int dmst_validate(const int32_t* u, const int32_t* v, const double* w, int64_t n_edges, int64_t n_vertices,
                   int32_t* error_kind, int64_t* bad_edge, void* workspace, size_t workspace_bytes,
                   void* stream);
+
+/* dendrogram_height (analysis.py:21-33) of a rank-space edge_parent array
+ * (DEVICE pointer, n_edges entries, ROOT = -1): the largest number of edge
+ * ancestors of a vertex, by pointer jumping.  *height is a HOST pointer.
+ * Workspace: any buffer of at least 16 n_edges + 4096 bytes (e.g. the
+ * dmst_build workspace). */
+int dmst_dendrogram_height(const int32_t* edge_parent, int64_t n_edges, int64_t* height, void* workspace,
+                           size_t workspace_bytes, void* stream);
 
 /* Message for the last non-zero return on this thread ("" if none). */
 const char* dmst_last_error(void);

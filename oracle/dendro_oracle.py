@@ -24,6 +24,8 @@ import os
 import subprocess
 from dataclasses import dataclass
 
+import math
+
 import numpy as np
 
 ROOT = -1  # expansion.py:20
@@ -343,3 +345,34 @@ def weighted_tree(num_vertices: int, u, v, w):
     if int(np.count_nonzero(roots == np.arange(num_vertices))) != 1:
         raise TreeFormatError("input is disconnected or cyclic, not a tree")
     return num_vertices, u, v, w
+
+
+# ------------------------------------------------------------- statistics
+def dendrogram_height(edge_parent: np.ndarray, vertex_parent: np.ndarray) -> int:
+    """analysis.py:21-33: edge depths in one ascending-rank pass (parents are
+    heavier, i.e. smaller rank); height = max depth over vertex parents."""
+    n = int(edge_parent.shape[0])
+    depth = np.empty(n, dtype=np.int64)
+    ep = np.asarray(edge_parent, dtype=np.int64)
+    for e in range(n):
+        p = ep[e]
+        depth[e] = 1 if p == ROOT else depth[p] + 1
+    return int(depth[np.asarray(vertex_parent, dtype=np.int64)].max())
+
+
+def num_chains(c: Chains) -> int:
+    """expansion.py:52-54: distinct (terminal, anchor) pairs."""
+    return int(np.unique(np.stack([c.terminal, c.anchor], axis=1), axis=0).shape[0])
+
+
+def stats_report(num_vertices: int, u, v, w) -> dict:
+    """The numbers `dendromst stats` prints (cli.py:97-135), per_level as tuples."""
+    r = rank_edges(num_vertices, u, v, w)
+    ep, vp, h = pandora(r)
+    n = r.num_edges
+    height = dendrogram_height(ep, vp)
+    return {"edges": n, "vertices": num_vertices, "levels": h.num_levels, "height": height,
+            "chains": num_chains(assign_chains(h)),
+            "skewness_log2_edges": height / math.log2(n) if n >= 2 else 0.0,
+            "skewness_log2_points": height / math.log2(n + 1),
+            "per_level": [tuple(int(x) for x in c) for c in h.view_kind_counts]}

@@ -28,6 +28,7 @@ EXPORTS = (
     "dmst_pandora",
     "dmst_build_debug",
     "dmst_validate",
+    "dmst_dendrogram_height",
     "dmst_last_error",
     "dmst_kernel_name",
     "dmst_version",
@@ -44,6 +45,8 @@ class DmstStats(ctypes.Structure):
         ("sort2_passes", ctypes.c_int32),
         ("jump_rounds", ctypes.c_int32),
         ("kernel_launches", ctypes.c_int32),
+        ("want_chains", ctypes.c_int32),
+        ("num_chains", ctypes.c_int32),
         ("kernel_ms", ctypes.c_float * DMST_MAX_KERNELS),
         ("kernel_calls", ctypes.c_int32 * DMST_MAX_KERNELS),
     ]
@@ -100,6 +103,8 @@ def load() -> ctypes.CDLL:
     lib.dmst_validate.argtypes = [vp, vp, vp, i64, i64, ctypes.POINTER(ctypes.c_int32),
                                   ctypes.POINTER(ctypes.c_int64), vp, sz, vp]
     lib.dmst_validate.restype = ctypes.c_int
+    lib.dmst_dendrogram_height.argtypes = [vp, i64, ctypes.POINTER(ctypes.c_int64), vp, sz, vp]
+    lib.dmst_dendrogram_height.restype = ctypes.c_int
     lib.dmst_last_error.argtypes = []
     lib.dmst_last_error.restype = ctypes.c_char_p
     lib.dmst_kernel_name.argtypes = [ctypes.c_int32]

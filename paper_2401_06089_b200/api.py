@@ -248,7 +248,7 @@ class DendrogramBuilder:
         return torch.cuda.current_stream(self.device).cuda_stream
 
     def build(self, num_vertices: int, u, v, w, *, out: BuildResult | None = None,
-              debug: bool = False, profile: bool = False) -> BuildResult:
+              debug: bool = False, profile: bool = False, want_chains: bool = False) -> BuildResult:
         dev = self.device
         with torch.cuda.device(dev):
             u = _as_dev(u, torch.int32, dev)
@@ -267,6 +267,7 @@ class DendrogramBuilder:
             ws = self.workspace(n, nv) if n >= 1 and nv >= 2 else torch.empty(1, dtype=torch.uint8, device=dev)
             st = _lib.DmstStats()
             st.profile = 1 if profile else 0
+            st.want_chains = 1 if want_chains else 0
             if debug:
                 dbg = {"retirement": torch.empty(n, dtype=torch.int8, device=dev),
                        "chain_key": torch.empty(n, dtype=torch.int32, device=dev),
@@ -398,6 +399,36 @@ def weighted_tree_b200(num_vertices: int, u, v, w, device=None) -> WeightedTree:
 def validate_b200(num_vertices: int, u, v, w, device=None) -> None:
     """Validation only (no host copies of the arrays)."""
     _validate(_builder(device), num_vertices, u, v, w)
+
+
+def dendrogram_height_b200(edge_parent: torch.Tensor, device=None) -> int:
+    """Drop-in for ``dendrogram_height`` (analysis.py:21-33) on a device
+    edge_parent tensor (int32, rank space, ROOT = -1): pointer jumping."""
+    b = _builder(device)
+    ep = _as_dev(edge_parent, torch.int32, b.device)
+    n = int(ep.shape[0])
+    ws = b.workspace(max(n, 1), max(n, 1) + 1)
+    h = ctypes.c_int64(0)
+    with torch.cuda.device(b.device):
+        _lib.check(b.lib.dmst_dendrogram_height(_ptr(ep), n, ctypes.byref(h), _ptr(ws), ws.numel(), b._stream()))
+    return int(h.value)
+
+
+def stats_b200(num_vertices: int, u, v, w, device=None) -> dict:
+    """The report of ``dendromst stats`` (cli.py:97-135) for (u, v, w):
+    edges, vertices, levels, height, chains, both skewness figures and the
+    per-level kind counts, computed on the GPU (build with chain counting,
+    then dendrogram_height on the device edge_parent)."""
+    import math
+    b = _builder(device)
+    res = b.build(num_vertices, u, v, w, want_chains=True)
+    n = int(res.edge_parent.shape[0])
+    height = dendrogram_height_b200(res.edge_parent, device=b.device)
+    return {"edges": n, "vertices": int(num_vertices), "levels": res.num_levels, "height": height,
+            "chains": int(res.stats.num_chains),
+            "skewness_log2_edges": height / math.log2(n) if n >= 2 else 0.0,
+            "skewness_log2_points": height / math.log2(n + 1),
+            "per_level": res.view_kind_counts}
 
 
 def build_b200(num_vertices: int, u, v, w, device=None, debug: bool = False) -> BuildResult:

@@ -654,6 +654,7 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
   if (st) st->sort2_passes = (int)shifts.size();
   // chain sort: keys at R[0, 4n); ping-pong A = R[4n, 12n), B = R[12n, 20n);
   if (shifts.empty()) {  // one chain (all keys equal): rank order is chain order
+    if (st) st->num_chains = 1;
     c.begin(KK_LINK_APPLY);
     k_link<<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(n, keys, nullptr, w.smi_all, edge_parent);
     c.launched();
@@ -667,6 +668,17 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     for (int& x : shifts64) x += 32;
     run_sort<uint64_t, 0, S2_BLOCK, S2_ITEMS, S2_MINB, S2_BITS>(c, {KK_SORT2_PASS, KK_SORT2_PASS, KK_SORT2_PASS}, n,
                                                              shifts64, bufK, bufP, Sort2FirstLoader{keys}, fin);
+    if (st && st->want_chains) {
+      uint32_t* cnt = w.small + SM_MISC + 60;
+      c.zero(cnt, 4);
+      c.begin(KK_OTHER);
+      k_count_heads<<<c.persistent_grid(n, 256, 8), 256, 0, c.s>>>((const unsigned long long*)fin.keys, n, cnt);
+      c.launched();
+      uint32_t h = 0;
+      c.to_host(&h, cnt, 4);
+      c.sync();
+      st->num_chains = (int32_t)h;
+    }
     // (rank, parent) records grouped by 8192-rank window: R[20n, 28n) -> R[28n, 36n)
     uint32_t* recA = (uint32_t*)(w.R + align_up(20 * n));
     uint32_t* recB = (uint32_t*)(w.R + align_up(28 * n));
@@ -714,9 +726,10 @@ void init_ctx(Ctx& c, int64_t n, int64_t nv, void* ws, void* stream, dmst_stats*
   char* base = (char*)(((uintptr_t)ws + 255) & ~uintptr_t(255));
   c.w = carve(n, nv, base);
   if (st) {
-    const int32_t prof = st->profile;
+    const int32_t prof = st->profile, wc = st->want_chains;
     memset(st, 0, sizeof(*st));
     st->profile = prof;
+    st->want_chains = wc;
     c.profile = prof != 0;
   }
 }
@@ -986,6 +999,47 @@ int dmst_validate(const int32_t* u, const int32_t* v, const double* w, int64_t n
     c.to_host(&dup, r + 5, 4);
     c.sync();
     *error_kind = dup ? DMST_TREE_DUPLICATE : DMST_TREE_NOT_A_TREE;
+  });
+}
+
+int dmst_dendrogram_height(const int32_t* edge_parent, int64_t n_edges, int64_t* height, void* workspace,
+                           size_t workspace_bytes, void* stream) {
+  return guarded([&] {
+    if (!height) invalid("height must be a host pointer");
+    *height = 0;
+    if (n_edges < 1) return;
+    if (!edge_parent || !workspace || workspace_bytes < (size_t)(16 * n_edges + 4096)) invalid("bad pointers / workspace");
+    const int64_t n = n_edges;
+    Ctx c;
+    c.s = (cudaStream_t)stream;
+    c.sms = num_sms();
+    char* base = (char*)(((uintptr_t)workspace + 255) & ~uintptr_t(255));
+    int2* buf[2] = {(int2*)base, (int2*)(base + align_up(8 * n))};
+    uint32_t* flag = (uint32_t*)(base + align_up(8 * n) + align_up(8 * n));
+    if ((size_t)((char*)flag - (char*)workspace) + 16 > workspace_bytes) invalid("workspace too small");
+    c.begin(KK_OTHER);
+    k_depth_init<<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(edge_parent, n, buf[0]);
+    c.launched();
+    int cur = 0;
+    for (int round = 0; round < 64; ++round) {
+      c.zero(flag, 4);
+      c.begin(KK_OTHER);
+      k_depth_jump<<<c.persistent_grid(n, 256, 8), 256, 0, c.s>>>(buf[cur], buf[cur ^ 1], n, flag);
+      c.launched();
+      cur ^= 1;
+      uint32_t live = 0;
+      c.to_host(&live, flag, 4);
+      c.sync();
+      if (!live) break;
+    }
+    c.zero(flag + 1, 4);
+    c.begin(KK_OTHER);
+    k_depth_max<<<c.persistent_grid(n, 256, 8), 256, 0, c.s>>>(buf[cur], n, flag + 1);
+    c.launched();
+    uint32_t mx = 0;
+    c.to_host(&mx, flag + 1, 4);
+    c.sync();
+    *height = mx;
   });
 }
 

@@ -123,3 +123,54 @@ __global__ void k_adjacent_equal(const unsigned long long* __restrict__ k, int64
 }
 
 }  // namespace dmst
+
+namespace dmst {
+
+// ------------------------------------------------ dendrogram statistics
+// dendrogram_height (analysis.py:21-33): depth(e) = depth(parent(e)) + 1,
+// depth 1 at the root; the height is the largest depth (the deepest edge
+// node has two vertex children, so it is some vertex's parent).  Pointer
+// jumping over (ancestor, distance) pairs packed in 8 B: one random probe
+// per live edge per round, ceil(log2(height)) rounds.
+__global__ void k_depth_init(const int32_t* __restrict__ parent, int64_t n, int2* __restrict__ ad) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) ad[e] = make_int2(parent[e], 1);
+}
+
+__global__ void __launch_bounds__(256) k_depth_jump(const int2* __restrict__ in, int2* __restrict__ out, int64_t n,
+                                                    uint32_t* __restrict__ live) {
+  uint32_t any = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride) {
+    int2 a = in[e];
+    if (a.x >= 0) {
+      const int2 b = in[a.x];
+      a = make_int2(b.x, a.y + b.y);
+      any |= a.x >= 0;
+    }
+    out[e] = a;
+  }
+  if (__any_sync(kFull, any != 0) && lane_id() == 0) atomicOr(live, 1u);
+}
+
+__global__ void __launch_bounds__(256) k_depth_max(const int2* __restrict__ ad, int64_t n, uint32_t* __restrict__ mx) {
+  int32_t m = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride) m = max(m, ad[e].y);
+  m = __reduce_max_sync(kFull, m);
+  if (lane_id() == 0) atomicMax(mx, (uint32_t)m);
+}
+
+// Chain count (ChainAssignment.num_chains, expansion.py:52-54): distinct
+// chain keys = heads of the (key, rank)-sorted items.
+__global__ void __launch_bounds__(256) k_count_heads(const unsigned long long* __restrict__ items, int64_t n,
+                                                     uint32_t* __restrict__ cnt) {
+  uint32_t c = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    c += (i == 0 || (items[i] >> 32) != (items[i - 1] >> 32)) ? 1u : 0u;
+  c = __reduce_add_sync(kFull, c);
+  if (lane_id() == 0 && c) atomicAdd(cnt, c);
+}
+
+}  // namespace dmst

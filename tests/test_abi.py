@@ -37,7 +37,7 @@ def test_exports_every_declared_symbol(lib):
 
 def test_stats_struct_layout_matches_header():
     # profile, num_levels, 65*4 counts, 65 view sizes, 4 int32 fields, 16 float + 16 int32
-    assert ctypes.sizeof(_lib.DmstStats) == 4 * (2 + 65 * 4 + 65 + 4 + 2 * 24)
+    assert ctypes.sizeof(_lib.DmstStats) == 4 * (2 + 65 * 4 + 65 + 4 + 2 + 2 * 24)
 
 
 def test_workspace_bytes(lib):

@@ -348,7 +348,7 @@ int64_t radix_pass(Ctx& c, int kind, int64_t n, int shift, Loader ld, Emitter em
   k_upsweep<BITS, Loader><<<(unsigned)(G * kUpSplit), 256, 0, c.s>>>(a, ld);
   c.launched();
   c.begin(KK_UPSWEEP);
-  k_chunk_scan<BITS><<<1, 256, 0, c.s>>>(a.counts, a.GS);
+  k_chunk_scan<BITS><<<1, kScanThreads, 0, c.s>>>(a.counts, a.GS);
   c.launched();
   c.begin(kind);
   kern<<<(unsigned)G, BLOCK, S::bytes(), c.s>>>(a, ld, em);

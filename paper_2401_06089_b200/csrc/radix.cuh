@@ -248,52 +248,63 @@ __global__ void __launch_bounds__(256) k_upsweep(SweepArgs a, Loader ld) {
 // distinct digits on average; __match_any_sync is cheaper below ~kBallotE,
 // ballots above (counts[R * GS] = 1 => ballots).
 constexpr float kBallotE = 12.0f;
+constexpr int kScanThreads = 1024;
 template <int BITS>
-__global__ void __launch_bounds__(256) k_chunk_scan(uint32_t* counts, uint32_t GS) {
-  constexpr int R = 1 << BITS, BPT = R / 256;
-  __shared__ uint32_t scratch[256 / 32 + 1];
-  __shared__ float fscr[256 / 32];
-  const uint32_t nq = GS / 4;
-  uint32_t s = 0, rs[BPT];
-#pragma unroll
-  for (int r = 0; r < BPT; ++r) {
-    const uint4* row = reinterpret_cast<const uint4*>(counts + (uint64_t)(threadIdx.x * BPT + r) * GS);
+__global__ void __launch_bounds__(kScanThreads) k_chunk_scan(uint32_t* counts, uint32_t GS) {
+  // one warp per digit row at a time (coalesced, lanes stride the chunks):
+  // row totals, a block scan over the R totals, then each row rewritten as
+  // exclusive offsets with a warp scan
+  constexpr int R = 1 << BITS, NWS = kScanThreads / 32;
+  __shared__ uint32_t rowsum[R];
+  __shared__ uint32_t scratch[kScanThreads / 32 + 1];
+  __shared__ float fscr[kScanThreads / 32];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < R; r += NWS) {
+    const uint32_t* row = counts + (uint64_t)r * GS;
     uint32_t t = 0;
-#pragma unroll 8
-    for (uint32_t q = 0; q < nq; ++q) {
-      const uint4 v = row[q];
-      t += v.x + v.y + v.z + v.w;
-    }
-    rs[r] = t;
-    s += t;
-  }
-  uint32_t tot;
-  uint32_t run = block_excl_sum<256>(s, scratch, &tot);
-  float e = 0.f;
-#pragma unroll
-  for (int r = 0; r < BPT; ++r) e += 1.f - __powf(1.f - (float)rs[r] / (float)max(tot, 1u), 32.f);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(kFull, e, o);
-  if ((threadIdx.x & 31) == 0) fscr[threadIdx.x >> 5] = e;
-#pragma unroll
-  for (int r = 0; r < BPT; ++r) {
-    uint4* row = reinterpret_cast<uint4*>(counts + (uint64_t)(threadIdx.x * BPT + r) * GS);
-#pragma unroll 8
-    for (uint32_t q = 0; q < nq; ++q) {
-      const uint4 v = row[q];
-      uint4 o;
-      o.x = run;
-      o.y = o.x + v.x;
-      o.z = o.y + v.y;
-      o.w = o.z + v.z;
-      run = o.w + v.w;
-      row[q] = o;
-    }
+    for (uint32_t q = lane; q < GS; q += 32) t += row[q];
+    t = __reduce_add_sync(kFull, t);
+    if (lane == 0) rowsum[r] = t;
   }
   __syncthreads();
+  constexpr int RPT = (R + kScanThreads - 1) / kScanThreads;  // rows per thread in the block scan
+  uint32_t v[RPT], sum = 0;
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int r = threadIdx.x * RPT + q;
+    v[q] = r < R ? rowsum[r] : 0u;
+    sum += v[q];
+  }
+  uint32_t tot;
+  uint32_t run = block_excl_sum<kScanThreads>(sum, scratch, &tot);
+  float e = 0.f;
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int r = threadIdx.x * RPT + q;
+    if (r < R) {
+      e += 1.f - __powf(1.f - (float)v[q] / (float)max(tot, 1u), 32.f);
+      rowsum[r] = run;  // exclusive start of row r
+      run += v[q];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(kFull, e, o);
+  if (lane == 0) fscr[warp] = e;
+  __syncthreads();
+  for (int r = warp; r < R; r += NWS) {
+    uint32_t* row = counts + (uint64_t)r * GS;
+    uint32_t base = rowsum[r];
+    for (uint32_t q0 = 0; q0 < GS; q0 += 32) {
+      const uint32_t q = q0 + lane;
+      const uint32_t x = q < GS ? row[q] : 0u;
+      const uint32_t incl = warp_incl_sum(x);
+      if (q < GS) row[q] = base + incl - x;
+      base += __shfl_sync(kFull, incl, 31);
+    }
+  }
   if (threadIdx.x == 0) {
     float E = 0.f;
-    for (int w = 0; w < 256 / 32; ++w) E += fscr[w];
+    for (int w = 0; w < NWS; ++w) E += fscr[w];
     counts[(uint64_t)R * GS] = E > kBallotE ? 1u : 0u;
   }
 }

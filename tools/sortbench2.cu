@@ -48,7 +48,7 @@ void run(int64_t n, K* k, uint32_t* v, K* k2, uint32_t* v2, uint32_t* counts, in
     cudaMemset(counts, 0, 4 * 256 * a.GS);
     cudaEventRecord(e[0]);
     k_upsweep<8, L><<<(unsigned)(G * kUpSplit), 256>>>(a, ld);
-    k_chunk_scan<8><<<1, 256>>>(counts, a.GS);
+    k_chunk_scan<8><<<1, kScanThreads>>>(counts, a.GS);
     cudaEventRecord(e[2]);
     kern<<<(unsigned)G, BLOCK, S::bytes()>>>(a, ld, em);
     cudaEventRecord(e[3]); cudaEventSynchronize(e[3]);

@@ -306,6 +306,7 @@ struct Ctx {
     mapped_used = 0;
   }
   void zero(void* d, size_t bytes) { DMST_CUDA(cudaMemsetAsync(d, 0, bytes, s)); }
+  void ones(void* d, size_t bytes) { DMST_CUDA(cudaMemsetAsync(d, 0xff, bytes, s)); }
   unsigned persistent_grid(int64_t work, int block, int per_sm) {
     return (unsigned)std::min<int64_t>(grid_for(work, block), (int64_t)sms * per_sm);
   }
@@ -401,8 +402,8 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
                Sort1FinalEmitter em, int* passes_out) {
   unsigned long long* and_or = (unsigned long long*)(c.w.small + SM_HIST1);
   uint32_t* negzero = c.w.small + SM_MISC + MISC_NEGZERO;
-  const unsigned long long init[2] = {~0ull, 0ull};
-  DMST_CUDA(cudaMemcpyAsync(and_or, init, 16, cudaMemcpyHostToDevice, c.s));
+  c.ones(and_or, 8);  // AND starts all-ones, OR all-zeros (memsets: no pageable copies)
+  c.zero(and_or + 1, 8);
   c.zero(negzero, 4);
   c.begin(KK_SORT1_HIST);
   k_key_reduce<<<c.persistent_grid(n, 256 * 4, 8), 256, 0, c.s>>>(w, n, and_or, negzero);
@@ -635,8 +636,8 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
   // expansion walk -> chain keys (+ AND / OR of all keys for digit skipping)
   uint32_t* key_ao = w.small + SM_HIST2;
   uint32_t* keys = (uint32_t*)w.R;
-  const uint32_t kinit[2] = {~0u, 0u};
-  DMST_CUDA(cudaMemcpyAsync(key_ao, kinit, 8, cudaMemcpyHostToDevice, c.s));
+  c.ones(key_ao, 4);
+  c.zero(key_ao + 1, 4);
   c.begin(KK_WALK);
   k_walk<256><<<c.persistent_grid(n, 256, 8), 256, 0, c.s>>>(n, w.ret, w.x1, w.lvl_all, lt, keys,
                                                               key_ao);
@@ -933,10 +934,11 @@ int dmst_validate(const int32_t* u, const int32_t* v, const double* w, int64_t n
     init_ctx(c, n, nv, workspace, stream, nullptr);
     uint32_t* r = c.w.small + SM_MISC + 32;  // [0..3] checks, [4] roots, [5] duplicate flag
     unsigned long long* ao = (unsigned long long*)(c.w.small + SM_MISC + 48);
-    const uint32_t rinit[6] = {0xffffffffu, 0u, 0u, 0xffffffffu, 0u, 0u};
-    const unsigned long long aoinit[2] = {~0ull, 0ull};
-    DMST_CUDA(cudaMemcpyAsync(r, rinit, sizeof(rinit), cudaMemcpyHostToDevice, c.s));
-    DMST_CUDA(cudaMemcpyAsync(ao, aoinit, sizeof(aoinit), cudaMemcpyHostToDevice, c.s));
+    c.zero(r, 24);
+    c.ones(r, 4);      // r[0]: first non-finite edge
+    c.ones(r + 3, 4);  // r[3]: first self-loop
+    c.ones(ao, 8);
+    c.zero(ao + 1, 8);
     c.begin(KK_OTHER);
     k_validate_scan<<<c.persistent_grid(n, 256, 8), 256, 0, c.s>>>(u, v, w, n, nv, r, ao);
     c.launched();

@@ -328,33 +328,49 @@ void smem_attr(K* kernel, size_t bytes) {
   }
 }
 
-// One radix pass: upsweep (per-chunk digit counts), chunk scan, downsweep.
+// Radix pass geometry: G persistent CTAs, one contiguous chunk each.
+struct SweepGeom {
+  int64_t G, chunk;
+  uint32_t GS;
+};
+SweepGeom sweep_geom(const Ctx& c, int64_t n, int T, int minb) {
+  SweepGeom g;
+  int64_t G = std::min<int64_t>(cdiv(n, T), std::min<int64_t>((int64_t)c.sms * minb, kMaxChunks));
+  g.chunk = cdiv(cdiv(n, G), T) * T;
+  g.G = cdiv(n, g.chunk);
+  g.GS = (uint32_t)((g.G + 3) & ~int64_t(3));
+  return g;
+}
+
+// One radix pass: upsweep (per-chunk digit counts; skipped when a fused
+// upsweep already produced them), chunk scan, downsweep.
 template <typename K, int PW, int BLOCK, int ITEMS, int MINB, int BITS, class Loader, class Emitter>
-int64_t radix_pass(Ctx& c, int kind, int64_t n, int shift, Loader ld, Emitter em) {
+int64_t radix_pass(Ctx& c, int kind, int64_t n, int shift, Loader ld, Emitter em, bool counts_ready = false) {
   using S = DownSmem<K, PW, BLOCK, ITEMS, Loader, Emitter, BITS>;
   constexpr int T = S::T;
   auto kern = k_downsweep<K, PW, BLOCK, ITEMS, MINB, Loader, Emitter, BITS>;
   smem_attr(kern, (int)S::bytes());
-  SweepArgs a;
+  const SweepGeom g = sweep_geom(c, n, T, MINB);
+  SweepArgs a{};
   a.n = n;
   a.shift = shift;
-  int64_t G = std::min<int64_t>(cdiv(n, T), std::min<int64_t>((int64_t)c.sms * MINB, kMaxChunks));
-  a.chunk = cdiv(cdiv(n, G), T) * T;
-  G = cdiv(n, a.chunk);
-  a.G = (uint32_t)G;
-  a.GS = (uint32_t)((G + 3) & ~int64_t(3));
+  a.chunk = g.chunk;
+  a.G = (uint32_t)g.G;
+  a.GS = g.GS;
   a.counts = c.w.counts;
-  c.zero(a.counts, 4 * (size_t(1) << BITS) * a.GS);
-  c.begin(KK_UPSWEEP);
-  k_upsweep<BITS, Loader><<<(unsigned)(G * kUpSplit), 256, 0, c.s>>>(a, ld);
-  c.launched();
+  if (!counts_ready) {
+    c.zero(a.counts, 4 * (size_t(1) << BITS) * a.GS);
+    c.begin(KK_UPSWEEP);
+    k_upsweep<BITS, Loader><<<(unsigned)(g.G * kUpSplit), 256, 0, c.s>>>(a, ld);
+    c.launched();
+  }
   c.begin(KK_UPSWEEP);
   k_chunk_scan<BITS><<<1, kScanThreads, 0, c.s>>>(a.counts, a.GS);
   c.launched();
   c.begin(kind);
-  kern<<<(unsigned)G, BLOCK, S::bytes(), c.s>>>(a, ld, em);
+  kern<<<(unsigned)g.G, BLOCK, S::bytes(), c.s>>>(a, ld, em);
   c.launched();
-  return G;
+  return g.G;
 }
 
 // Multi-pass driver over the non-constant digits (bit offsets `shifts`).
@@ -362,7 +378,8 @@ int64_t radix_pass(Ctx& c, int kind, int64_t n, int shift, Loader ld, Emitter em
 // first/last passes use the given loader/emitter.
 template <typename K, int PW, int BLOCK, int ITEMS, int MINB, int BITS, class FirstLoader, class FinalEmitter>
 int64_t run_sort(Ctx& c, const int (&kinds)[3], int64_t n, const std::vector<int>& shifts,
-              K* const (&bufK)[2], uint32_t* const (&bufP)[2], FirstLoader first, FinalEmitter final_em) {
+              K* const (&bufK)[2], uint32_t* const (&bufP)[2], FirstLoader first, FinalEmitter final_em,
+              int ready_shift = -1) {
   const int P = (int)shifts.size();
   if (P == 0) {
     c.begin(KK_OTHER);
@@ -375,10 +392,11 @@ int64_t run_sort(Ctx& c, const int (&kinds)[3], int64_t n, const std::vector<int
     const int o = p % 2, in = o ^ 1;
     ArrayEmitter<K, PW> mid{bufK[o], bufP[o]};
     ArrayLoader<K, PW> ldr{bufK[in], bufP[in]};
+    const bool ready = p == 0 && shifts[0] == ready_shift;
     if (P == 1)
-      G = radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[2], n, shifts[p], first, final_em);
+      G = radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[2], n, shifts[p], first, final_em, ready);
     else if (p == 0)
-      G = radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[0], n, shifts[p], first, mid);
+      G = radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[0], n, shifts[p], first, mid, ready);
     else if (p == P - 1)
       G = radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[2], n, shifts[p], ldr, final_em);
     else
@@ -400,13 +418,36 @@ std::vector<int> active_digits(uint64_t key_and, uint64_t key_or, int bits, int 
 // Sort #1 (rank_edges): orig_of, heights, euv (and/or ru, rv).
 void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int64_t n,
                Sort1FinalEmitter em, int* passes_out) {
-  unsigned long long* and_or = (unsigned long long*)(c.w.small + SM_HIST1);
+  unsigned long long* sample_ao = (unsigned long long*)(c.w.small + SM_HIST1);
+  unsigned long long* and_or = sample_ao + 2;
   uint32_t* negzero = c.w.small + SM_MISC + MISC_NEGZERO;
-  c.ones(and_or, 8);  // AND starts all-ones, OR all-zeros (memsets: no pageable copies)
+  c.ones(sample_ao, 8);  // AND starts all-ones, OR all-zeros (memsets: no pageable copies)
+  c.zero(sample_ao + 1, 8);
+  c.ones(and_or, 8);
   c.zero(and_or + 1, 8);
   c.zero(negzero, 4);
+  // predict the first active digit from a sample, then count it in the same
+  // read of w that reduces all keys (k_upsweep<KEYRED>)
   c.begin(KK_SORT1_HIST);
-  k_key_reduce<<<c.persistent_grid(n, 256 * 4, 8), 256, 0, c.s>>>(w, n, and_or, negzero);
+  k_key_sample<<<1, 1024, 0, c.s>>>(w, n, sample_ao);
+  c.launched();
+  unsigned long long sao[2];
+  c.to_host(sao, sample_ao, 16);
+  c.sync();
+  const std::vector<int> guess = active_digits(sao[0], sao[1], 8, 64);
+  const int d0 = guess.empty() ? 0 : guess[0];
+  const SweepGeom g = sweep_geom(c, n, S1_BLOCK * S1_ITEMS, S1_MINB);
+  SweepArgs a{};
+  a.n = n;
+  a.shift = d0;
+  a.chunk = g.chunk;
+  a.G = (uint32_t)g.G;
+  a.GS = g.GS;
+  a.counts = c.w.counts;
+  c.zero(a.counts, 4 * kRadix * (size_t)a.GS);
+  c.begin(KK_SORT1_HIST);
+  k_upsweep<8, Sort1FirstLoader, true><<<(unsigned)(g.G * kUpSplit), 256, 0, c.s>>>(
+      a, Sort1FirstLoader{w, u, v}, KeyRed{w, and_or, negzero});
   c.launched();
   unsigned long long ao[2];
   uint32_t nz = 0;
@@ -414,13 +455,14 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
   c.to_host(&nz, negzero, 4);
   c.sync();
   const std::vector<int> shifts = active_digits(ao[0], ao[1], 8, 64);
+  const int ready = !shifts.empty() && shifts[0] == d0 ? d0 : -1;  // else: the first pass counts again
   if (passes_out) *passes_out = (int)shifts.size();
   char* R = c.w.R;
   uint64_t* const bufK[2] = {(uint64_t*)R, (uint64_t*)(R + 8 * n)};
   uint32_t* vb = (uint32_t*)(R + 16 * n);
   uint32_t* const bufP[2] = {vb, vb + 3 * n};
   run_sort<uint64_t, 3, S1_BLOCK, S1_ITEMS, S1_MINB, 8>(c, {KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL}, n,
-                                                     shifts, bufK, bufP, Sort1FirstLoader{w, u, v}, em);
+                                                     shifts, bufK, bufP, Sort1FirstLoader{w, u, v}, em, ready);
   if (nz) {
     c.begin(KK_OTHER);
     k_fix_negzero<<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(w, em.orig_of, em.heights, n);

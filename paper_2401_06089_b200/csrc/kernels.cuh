@@ -20,15 +20,7 @@ constexpr int CHASE_CAP = 512;   // hard bound on one V2 chase
 __device__ __forceinline__ bool is_ruler(uint32_t v) { return ((v * 0x9E3779B1u) >> 27) == 0; }
 
 // ------------------------------------------------------------ key codec
-// Order-preserving map of (w + 0.0) to uint64, inverted so that ascending
-// key order is descending weight; -0.0 is canonicalised to +0.0 so the two
-// tie, as numpy's comparison does (tree_core.py:180).
-__device__ __forceinline__ uint64_t desc_key(double w) {
-  uint64_t b = (uint64_t)__double_as_longlong(w);
-  if (b == 0x8000000000000000ull) b = 0;
-  uint64_t asc = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
-  return ~asc;
-}
+__device__ __forceinline__ uint64_t desc_key(double w) { return desc_key_of(w); }
 __device__ __forceinline__ double key_to_double(uint64_t key) {
   uint64_t asc = ~key;
   uint64_t b = (asc >> 63) ? (asc & 0x7fffffffffffffffull) : ~asc;
@@ -36,6 +28,26 @@ __device__ __forceinline__ double key_to_double(uint64_t key) {
 }
 
 // ------------------------------------------------ 1. edge sort (sort #1)
+// AND / OR of the keys of a strided sample (<= 65536 keys): predicts the
+// edge sort's first active digit so its upsweep can also do the full key
+// reduction (k_upsweep<KEYRED>).
+__global__ void __launch_bounds__(1024) k_key_sample(const double* __restrict__ w, int64_t n,
+                                                     unsigned long long* __restrict__ and_or) {
+  const int64_t stride = n > 65536 ? n / 65536 : 1;
+  uint64_t a = ~0ull, o = 0ull;
+  for (int64_t i = (int64_t)threadIdx.x * stride; i < n; i += (int64_t)blockDim.x * stride) {
+    const uint64_t k = desc_key(w[i]);
+    a &= k;
+    o |= k;
+  }
+  const uint32_t alo = __reduce_and_sync(kFull, (uint32_t)a), ahi = __reduce_and_sync(kFull, (uint32_t)(a >> 32));
+  const uint32_t olo = __reduce_or_sync(kFull, (uint32_t)o), ohi = __reduce_or_sync(kFull, (uint32_t)(o >> 32));
+  if (lane_id() == 0) {
+    atomicAnd(and_or, ((unsigned long long)ahi << 32) | alo);
+    atomicOr(and_or + 1, ((unsigned long long)ohi << 32) | olo);
+  }
+}
+
 // One read of w: bitwise AND / OR of all sort keys (a digit is constant
 // iff AND and OR agree on its bits -> that radix pass is skipped) and the
 // "-0.0 present" flag.

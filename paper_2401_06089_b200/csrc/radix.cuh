@@ -39,6 +39,16 @@ struct Vals<0> {  // key-only items
   uint32_t w[1];
 };
 
+// Order-preserving map of (w + 0.0) to uint64, inverted so that ascending
+// key order is descending weight; -0.0 is canonicalised to +0.0 so the two
+// tie, as numpy's comparison does (tree_core.py:180).
+__device__ __forceinline__ uint64_t desc_key_of(double w) {
+  uint64_t b = (uint64_t)__double_as_longlong(w);
+  if (b == 0x8000000000000000ull) b = 0;
+  uint64_t asc = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+  return ~asc;
+}
+
 template <int BITS = kRadixBits, typename K>
 __device__ __forceinline__ uint32_t digit_of(K key, int shift) {
   return (uint32_t)(key >> shift) & ((1u << BITS) - 1u);
@@ -194,8 +204,18 @@ struct SweepArgs {
 constexpr int kMaxChunks = 148 * 4;  // downsweep CTAs (chunks) per pass, upper bound
 constexpr int kUpSplit = 4;  // upsweep CTAs per chunk (counts accumulate atomically)
 
-template <int BITS, class Loader>
-__global__ void __launch_bounds__(256) k_upsweep(SweepArgs a, Loader ld) {
+// KEYRED (edge sort, first pass): the same read of w also produces the
+// AND / OR of all keys (digit skipping) and the "-0.0 present" flag, so the
+// edge sort has no separate reduction pass; the digit counted was predicted
+// from a sample of the keys (k_key_sample) and is re-checked on the host.
+struct KeyRed {
+  const double* w;
+  unsigned long long* and_or;
+  uint32_t* negzero;
+};
+
+template <int BITS, class Loader, bool KEYRED = false>
+__global__ void __launch_bounds__(256) k_upsweep(SweepArgs a, Loader ld, KeyRed kr = KeyRed{}) {
   constexpr int R = 1 << BITS, BPT = R / 256;
   __shared__ uint32_t h[8][R];  // per-warp histograms
   const uint32_t warp = threadIdx.x >> 5;
@@ -210,6 +230,8 @@ __global__ void __launch_bounds__(256) k_upsweep(SweepArgs a, Loader ld) {
   const int64_t begin = cbeg + part * plen;
   const int64_t end = min(min(a.n, cbeg + a.chunk), begin + plen);
   constexpr int U = 8;
+  uint64_t ka = ~0ull, ko = 0ull;
+  bool nz = false;
   for (int64_t i0 = begin; i0 < end; i0 += 256 * U) {
     uint32_t d[U];
     bool ok[U];
@@ -217,7 +239,16 @@ __global__ void __launch_bounds__(256) k_upsweep(SweepArgs a, Loader ld) {
     for (int q = 0; q < U; ++q) {
       const int64_t i = i0 + q * 256 + threadIdx.x;
       ok[q] = i < end;
-      d[q] = ok[q] ? digit_of<BITS>(ld.key(i), a.shift) : 0u;
+      if constexpr (KEYRED) {
+        const double x = ok[q] ? ld_stream(kr.w + i) : kr.w[begin];
+        const uint64_t k = desc_key_of(x);
+        nz |= (uint64_t)__double_as_longlong(x) == 0x8000000000000000ull;
+        ka &= k;
+        ko |= k;
+        d[q] = digit_of<BITS>(k, a.shift);
+      } else {
+        d[q] = ok[q] ? digit_of<BITS>(ld.key(i), a.shift) : 0u;
+      }
     }
 #pragma unroll
     for (int q = 0; q < U; ++q) {
@@ -228,6 +259,16 @@ __global__ void __launch_bounds__(256) k_upsweep(SweepArgs a, Loader ld) {
       } else if (ok[q]) {
         atomicAdd(&h[warp][d[q]], 1u);
       }
+    }
+  }
+  if constexpr (KEYRED) {
+    const uint32_t alo = __reduce_and_sync(kFull, (uint32_t)ka), ahi = __reduce_and_sync(kFull, (uint32_t)(ka >> 32));
+    const uint32_t olo = __reduce_or_sync(kFull, (uint32_t)ko), ohi = __reduce_or_sync(kFull, (uint32_t)(ko >> 32));
+    const bool anz = __any_sync(kFull, nz);
+    if (lane_id() == 0 && begin < end) {
+      atomicAnd(kr.and_or, ((unsigned long long)ahi << 32) | alo);
+      atomicOr(kr.and_or + 1, ((unsigned long long)ohi << 32) | olo);
+      if (anz) atomicOr(kr.negzero, 1u);
     }
   }
   __syncthreads();

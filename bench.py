@@ -89,6 +89,7 @@ def kernel_bytes(stats, n: int, nv: int) -> dict[str, float]:
         "sort2_pass": 16.0 * n * p2,                            # read 8, write 8 per pass
         "link_split": 32.0 * n if p2 else 0.0,                  # two 8-B record passes (read + write)
         "link_apply": 12.0 * n,                                 # read records 8, write edge_parent 4
+        "tail": 0.0,                                            # small views (< 1M edges), L2-resident
         "other": 0.0,
     }
 

@@ -32,6 +32,7 @@
 
 #include "kernels.cuh"
 #include "validate.cuh"
+#include "tail.cuh"
 
 namespace dmst {
 
@@ -46,13 +47,13 @@ constexpr int64_t kDirectMiBytes = 64ll << 20;  // direct scatter-max below this
 enum KernelKind {
   KK_SORT1_HIST, KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL, KK_MI_HIST, KK_MI_SPLIT_A, KK_MI_SPLIT_B,
   KK_MI_APPLY, KK_V1, KK_LEAFSCAN, KK_V2, KK_JUMP, KK_SELECT_EDGES, KK_WALK, KK_SORT2_PASS, KK_LINK_SPLIT,
-  KK_LINK_APPLY, KK_UPSWEEP, KK_OTHER, KK_COUNT
+  KK_LINK_APPLY, KK_UPSWEEP, KK_TAIL, KK_OTHER, KK_COUNT
 };
 static_assert(KK_COUNT <= DMST_MAX_KERNELS, "kernel kinds");
 const char* const kKernelNames[KK_COUNT] = {
     "sort1_hist", "sort1_pass_first", "sort1_pass_mid", "sort1_pass_final", "mi_hist", "mi_split_a",
     "mi_split_b", "mi_apply", "v1", "leafscan", "v2", "jump", "select_edges", "walk", "sort2_pass",
-    "link_split", "link_apply", "upsweep_scan", "other"};
+    "link_split", "link_apply", "upsweep_scan", "tail", "other"};
 
 namespace {
 
@@ -165,7 +166,7 @@ int num_sms() {
 
 // Per-thread host-mapped pinned buffer for small readbacks (Ctx::to_host).
 struct MappedBuf {
-  static constexpr uint32_t kWords = 256;
+  static constexpr uint32_t kWords = 2048;
   volatile uint32_t* host = nullptr;
   uint32_t* dev = nullptr;
   int device = -1;
@@ -523,6 +524,76 @@ Recs recs_at(char* base, int64_t) {
   return Recs{(uint32_t*)base};
 }
 
+bool use_tail() {
+  static const bool v = getenv("DMST_NO_TAIL") == nullptr;
+  return v;
+}
+
+// Run levels level0..L of the contraction in k_tail; fills lt.soff / lt.L,
+// the per-view stats and the running soff exactly as the host loop would.
+void run_tail(Ctx& c, int level0, int cur, int64_t n_k, int64_t nv_k, LevelTable& lt, int64_t& soff,
+              dmst_stats* st, int& jump_rounds) {
+  Workspace& w = c.w;
+  static int blocks_per_sm = -1;
+  if (blocks_per_sm < 0) {
+    DMST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_tail, TAIL_BLOCK, 0));
+    if (blocks_per_sm < 1) invalid("k_tail cannot be co-resident");
+  }
+  const int64_t want = cdiv(std::max(n_k, nv_k), TAIL_BLOCK);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c.sms * blocks_per_sm));
+  // scratch / outputs in the radix counts area (idle during the level loop)
+  uint32_t* scratch = w.counts;
+  int64_t* soff_out = (int64_t*)(w.counts + align_up(4 * (3 * (size_t)grid + 8)) / 4);
+  int32_t* counts_out = (int32_t*)(soff_out + DMST_MAX_LEVELS + 2);
+  int32_t* result = counts_out + 5 * (DMST_MAX_LEVELS + 1);
+  TailArgs ta{};
+  ta.cnt2 = w.cnt2;
+  ta.kw = w.kw;
+  ta.apre = w.apre;
+  for (int i = 0; i < 2; ++i) {
+    ta.euv[i] = w.euv[i];
+    ta.grank[i] = w.grank[i];
+    ta.mi64[i] = w.mi64[i];
+  }
+  ta.smi_all = w.smi_all;
+  ta.lvl_all = w.lvl_all;
+  ta.ret = w.ret;
+  ta.scratch = scratch;
+  ta.soff_out = soff_out;
+  ta.counts_out = counts_out;
+  ta.result = result;
+  ta.level0 = level0;
+  ta.cur0 = cur;
+  ta.n0 = n_k;
+  ta.nv0 = nv_k;
+  ta.soff_k0 = lt.soff[level0];
+  ta.soff0 = soff;
+  void* args[] = {&ta};
+  c.begin(KK_TAIL);
+  DMST_CUDA(cudaLaunchCooperativeKernel((const void*)k_tail, dim3(grid), dim3(TAIL_BLOCK), args, 0, c.s));
+  c.launched();
+  int32_t res[2];
+  c.to_host(res, result, 8);
+  c.sync();
+  const int L = res[0];
+  if (L < level0) invalid("too many contraction levels");
+  std::vector<int32_t> co(5 * (size_t)(L + 1));
+  std::vector<int64_t> so(L + 2);
+  c.to_host(co.data(), counts_out, 4 * co.size());
+  c.to_host(so.data(), soff_out, 8 * so.size());
+  c.sync();
+  for (int k = level0; k <= L; ++k) {
+    if (st) {
+      for (int q = 0; q < 4; ++q) st->level_counts[k][q] = co[5 * k + q];
+      st->view_vertices[k] = co[5 * k + 4];
+    }
+    lt.soff[k + 1] = so[k + 1];
+  }
+  soff = so[L + 1];
+  lt.L = L;
+  jump_rounds += res[1];
+}
+
 // Full pipeline after the edge sort: euv0 (rank-order endpoints) ready.
 void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t* edge_parent,
                   dmst_stats* st, int8_t* dbg_ret, int32_t* dbg_key, int32_t* dbg_term, int32_t* dbg_lvl) {
@@ -552,6 +623,12 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
   uint32_t* lcnt[4] = {misc + MISC_ACTIVE0, misc + MISC_ACTIVE1, misc + MISC_ACTIVE2, misc + MISC_NONRUL};
   while (true) {
     if (level >= DMST_MAX_LEVELS) invalid("too many contraction levels");
+    // small view: every remaining level in one cooperative kernel (tail.cuh)
+    if (level >= 1 && !v1_done && n_k <= kTailEdges && use_tail()) {
+      run_tail(c, level, cur, n_k, nv_k, lt, soff, st, jump_rounds);
+      level = lt.L;
+      break;
+    }
     // V1: maxIncident edge per vertex + child counts per edge (already done
     // by the bucketed apply unless the view was small enough for direct atomics)
     if (!v1_done) {

@@ -28,7 +28,7 @@ def kind(name: str) -> str:
         ("LinkSortedSrc", "link_split"), ("k_split<1, AosRecSrc<2>", "link_split"), ("k_link_cursors", "link_split"),
         ("k_link_apply", "link_apply"), ("k_link(", "link_apply"),
         ("k_mi_apply_smem", "mi_apply"), ("k_v1", "v1"), ("k_leafscan", "leafscan"), ("k_v2", "v2"),
-        ("k_jump", "jump"), ("k_select_edges", "select_edges"), ("k_walk", "walk"),
+        ("k_jump", "jump"), ("k_select_edges", "select_edges"), ("k_walk", "walk"), ("k_tail", "tail"),
     ]
     for pat, k in rules:
         if pat in name:

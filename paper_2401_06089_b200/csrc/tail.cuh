@@ -13,7 +13,7 @@
 
 namespace dmst {
 
-constexpr int64_t kTailEdges = 1 << 20;  // views at most this large run in k_tail
+constexpr int64_t kTailEdges = 1 << 22;  // views at most this large run in k_tail
 constexpr int TAIL_BLOCK = 512;
 constexpr int TAIL_CAP = 64;             // chase steps before pointer jumping takes over
 

@@ -29,12 +29,14 @@ def main():
         a = agg.setdefault(k, [0, 0.0])
         a[0] += 1
         a[1] += ms
-    tot = sum(a[1] for a in agg.values())
+    extra = ("validate", "stats")  # bench.py legs outside the timed build
+    tot = sum(a[1] for k, a in agg.items() if k not in extra)
     n = sum(a[0] for a in agg.values())
-    rows = sorted(agg.items(), key=lambda kv: -kv[1][1])
-    out = [f"# ncu launch list ({os.path.basename(path)}): {n} launches, {tot:.1f} ms (cold-cache, serialised; shares only)",
+    rows = sorted(agg.items(), key=lambda kv: (kv[0] in extra, -kv[1][1]))
+    out = [f"# ncu launch list ({os.path.basename(path)}): {n} launches (cold-cache, serialised; shares only);",
+           f"# share = of the {tot:.1f} ms of build kernels; validate/stats = bench.py legs outside the timed build",
            "kernel_kind,launches,total_ms,share"]
-    out += [f"{k},{a[0]},{a[1]:.3f},{a[1] / tot:.4f}" for k, a in rows]
+    out += [f"{k},{a[0]},{a[1]:.3f},{(a[1] / tot if k not in extra else float('nan')):.4f}" for k, a in rows]
     print("\n".join(out))
     if "--out" in sys.argv:
         open(sys.argv[sys.argv.index("--out") + 1], "w").write("\n".join(out) + "\n")

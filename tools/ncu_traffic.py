@@ -29,6 +29,10 @@ def kind(name: str) -> str:
         ("k_link_apply", "link_apply"), ("k_link(", "link_apply"),
         ("k_mi_apply_smem", "mi_apply"), ("k_v1", "v1"), ("k_leafscan", "leafscan"), ("k_v2", "v2"),
         ("k_jump", "jump"), ("k_select_edges", "select_edges"), ("k_walk", "walk"), ("k_tail", "tail"),
+        ("k_key_sample", "sort1_hist"),
+        # outside the timed build: bench.py's validation leg, statistics
+        ("k_validate_scan", "validate"), ("k_cc_", "validate"), ("k_adjacent_equal", "validate"),
+        ("k_depth_", "stats"), ("k_count_heads", "stats"),
     ]
     for pat, k in rules:
         if pat in name:

@@ -1,10 +1,12 @@
 // Stable LSD radix sort passes, reduce-then-scan, with TMA-staged input.
 //
-// One 8-bit digit per pass, three kernels:
+// One digit (8 or 9 bits) per pass, three kernels:
 //   k_upsweep    each CTA counts the digits of its contiguous chunk of the
-//                input (keys only) -> counts[digit][chunk];
+//                input (keys only) -> counts[digit][chunk]; for the edge
+//                sort's first pass it also reduces all keys (KEYRED);
 //   k_chunk_scan one CTA: exclusive scan of counts in digit-major order ->
-//                the global output offset of every (digit, chunk);
+//                the global output offset of every (digit, chunk), and the
+//                pass's warp-ranking method (match_any or ballots);
 //   k_downsweep  persistent: CTA c walks its chunk in sub-tiles of T items,
 //                keeps a running output offset per digit in shared memory
 //                (no inter-CTA look-back, no spinning), ranks each sub-tile
@@ -16,12 +18,12 @@
 // Loaders describe the input streams (staged) and how a (key, payload)
 // item is formed from them, so the first pass of a sort can build keys on
 // the fly from the caller's arrays and the last pass (Emitter) can write
-// final outputs.  Payloads are VW 32-bit words (SoA in shared memory).
+// final outputs.  Between passes an item is a key array plus an AoS
+// payload array (PW 32-bit words per item; PW = 0: key only), so a digit
+// run is at most two contiguous runs in memory.
 //
 // Replaces `np.argsort(-w, kind="stable")` (tree_core.py:180) and
-// `np.lexsort` (expansion.py:135) of /root/reference/pkg/src/dendromst/,
-// and partitions the scatter-max records of np.maximum.at
-// (tree_core.py:197-198) so their updates stay in L2 / shared memory.
+// `np.lexsort` (expansion.py:135) of /root/reference/pkg/src/dendromst/.
 #pragma once
 #include "common.cuh"
 
@@ -616,14 +618,5 @@ __global__ void __launch_bounds__(BLOCK) k_identity_pass(int64_t n, Loader ld, E
   em.template finish<BLOCK, kRadix>(est);
 }
 
-// Exclusive scan of per-digit global histograms: hist[p][256] -> gbase[p][256].
-__global__ void k_digit_scan(const uint32_t* __restrict__ hist, uint32_t* __restrict__ gbase, int passes) {
-  __shared__ uint32_t scratch[kRadix / 32 + 1];
-  for (int p = 0; p < passes; ++p) {
-    uint32_t total;
-    uint32_t x = hist[p * kRadix + threadIdx.x];
-    gbase[p * kRadix + threadIdx.x] = block_excl_sum<kRadix>(x, scratch, &total);
-  }
-}
 
 }  // namespace dmst

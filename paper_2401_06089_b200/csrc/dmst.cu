@@ -104,6 +104,7 @@ struct Workspace {
   int32_t* x1;            // view-1 supervertex of every edge (walk start)
   uint32_t* sel_status;   // leafscan look-back words (leaf, alpha)
   uint32_t* apre;         // alpha prefix per 16 edges
+  uint2* lw;              // (leaf bitmap, leaf prefix) per 32 edges (k_v2)
   size_t bytes;
 };
 
@@ -145,6 +146,7 @@ Workspace carve(int64_t n, int64_t nv, char* base) {
   w.x1 = (int32_t*)take(4 * (n + 2));
   w.sel_status = (uint32_t*)take(8 * (cdiv(n / 16 + 1, LS_TILE) + 2));
   w.apre = (uint32_t*)take(4 * (n / 16 + 2));
+  w.lw = (uint2*)take(8 * (n / 32 + 2));
   w.bytes = off + 256;
   return w;
 }
@@ -643,7 +645,7 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     // look-back words and level counters were zeroed before the loop (view 0)
     // or by the previous view's k_select_edges
     c.begin(KK_LEAFSCAN);
-    k_leafscan<<<ls_tiles, 256, 0, c.s>>>(words, n_k, w.cnt2, w.kw, w.apre, w.sel_status, misc + MISC_LSCTR,
+    k_leafscan<<<ls_tiles, 256, 0, c.s>>>(words, n_k, w.cnt2, w.kw, w.lw, w.apre, w.sel_status, misc + MISC_LSCTR,
                                          misc + MISC_COUNTS);
     c.launched();
     // V2: supervertex labels (vertex_map).  Runs before the host reads the
@@ -652,7 +654,7 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     int32_t* vm = level == 0 ? w.vm_all : (int32_t*)(w.lvl_all + lt.soff[level]);
     const int vs = level == 0 ? 1 : 2;
     c.begin(KK_V2);
-    k_v2<<<grid_for(nv_k, EW_BLOCK), EW_BLOCK, 0, c.s>>>(nv_k, mi_k, w.kw, vm,
+    k_v2<<<grid_for(nv_k, EW_BLOCK), EW_BLOCK, 0, c.s>>>(nv_k, mi_k, w.lw, vm,
                                                          level == 0 ? nullptr : w.smi_all + lt.soff[level],
                                                          lists[0], lcnt[0], lists[3], lcnt[3]);
     c.launched();

@@ -212,8 +212,18 @@ __device__ __forceinline__ uint32_t alpha_bits(uint32_t w, int64_t word, int64_t
   return a;
 }
 
+// Even bits of x (one per 2-bit field) compressed into the low 16 bits.
+__device__ __forceinline__ uint32_t even_bits16(uint32_t x) {
+  x &= 0x55555555u;
+  x = (x | (x >> 1)) & 0x33333333u;
+  x = (x | (x >> 2)) & 0x0F0F0F0Fu;
+  x = (x | (x >> 4)) & 0x00FF00FFu;
+  return (x | (x >> 8)) & 0x0000FFFFu;
+}
+
 __global__ void __launch_bounds__(256) k_leafscan(int64_t words, int64_t ne, const uint32_t* __restrict__ cnt2,
-                                                  uint2* __restrict__ kw, uint32_t* __restrict__ apre,
+                                                  uint2* __restrict__ kw, uint2* __restrict__ lw,
+                                                  uint32_t* __restrict__ apre,
                                                   uint32_t* __restrict__ status, uint32_t* __restrict__ tile_ctr,
                                                   uint32_t* __restrict__ counts) {
   constexpr int ITEMS = 8, TILE = 256 * ITEMS;
@@ -254,11 +264,17 @@ __global__ void __launch_bounds__(256) k_leafscan(int64_t words, int64_t ne, con
   }
   __syncthreads();
   uint32_t lrun = s_excl[0] + lex, arun = s_excl[1] + aex;
+  static_assert(ITEMS % 2 == 0 && (256 * ITEMS) % 2 == 0, "word pairs stay in one thread");
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     if (base + i < words) {
       kw[base + i] = make_uint2(cw[i], lrun);
       apre[base + i] = arun;
+    }
+    if ((i & 1) == 0 && base + i < words) {  // 32-edge leaf bitmap word + leaf prefix (k_v2)
+      const uint32_t lo = even_bits16(leaf_bits(cw[i]));
+      const uint32_t hi = i + 1 < ITEMS ? even_bits16(leaf_bits(cw[i + 1])) : 0u;
+      lw[(base + i) >> 1] = make_uint2(lo | (hi << 16), lrun);
     }
     lrun += __popc(leaf_bits(cw[i]));
     arun += __popc(alpha_bits(cw[i], base + i, ne));
@@ -280,9 +296,11 @@ __device__ __forceinline__ uint32_t leaf_label(uint2 w, uint32_t j) {
 // Views >= 1 (smi != null) store the vertex map interleaved with the view's
 // maxIncident as (vm[x], smi[x]) pairs: the chain walk then gets both from
 // one random 8-B probe (one DRAM sector) per level; vm has stride 2 there.
-__global__ void k_v2(int64_t nv, const unsigned long long* __restrict__ mi64, const uint2* __restrict__ kw,
+__global__ void k_v2(int64_t nv, const unsigned long long* __restrict__ mi64, const uint2* __restrict__ lw,
                      int32_t* __restrict__ vm, const int32_t* __restrict__ smi, int32_t* __restrict__ rul,
                      uint32_t* __restrict__ rul_cnt, int32_t* __restrict__ non, uint32_t* __restrict__ non_cnt) {
+  // lw[j >> 5] = (leaf bitmap of edges 32w..32w+31, leaf count before 32w):
+  // half the footprint of kw, so the chase's kind tests stay L2-resident
   const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t pol = l2_keep_policy();
   bool unresolved = false;
@@ -291,11 +309,10 @@ __global__ void k_v2(int64_t nv, const unsigned long long* __restrict__ mi64, co
     uint32_t j = (uint32_t)(m >> 32) - 1u;
     uint32_t y = (uint32_t)m;
     int s = 0;
-    uint2 kwj = make_uint2(0, 0);
+    uint2 lwj = make_uint2(0, 0);
     while (m != 0ull) {  // m == 0: isolated vertex (single-vertex view), label 0
-      kwj = ld_keep2(kw + (j >> 4), pol);
-      const uint32_t c = (kwj.x >> ((j & 15) * 2)) & 3u;
-      if (c == 2u) break;
+      lwj = ld_keep2(lw + (j >> 5), pol);
+      if ((lwj.x >> (j & 31)) & 1u) break;  // leaf edge
       if (++s > CHASE_CAP || (s > CHASE_FREE && is_ruler(y))) {
         unresolved = true;
         break;
@@ -304,7 +321,8 @@ __global__ void k_v2(int64_t nv, const unsigned long long* __restrict__ mi64, co
       j = (uint32_t)(m >> 32) - 1u;
       y = (uint32_t)m;
     }
-    const int32_t lab = unresolved ? ~(int32_t)y : (m ? (int32_t)leaf_label(kwj, j) : 0);
+    const int32_t lab = unresolved ? ~(int32_t)y
+                                   : (m ? (int32_t)(lwj.y + __popc(lwj.x & ((1u << (j & 31)) - 1u))) : 0);
     if (smi)
       __stcs(reinterpret_cast<int2*>(vm) + x, make_int2(lab, __ldcs(smi + x)));
     else

@@ -160,6 +160,16 @@ int dmst_validate(const int32_t* u, const int32_t* v, const double* w, int64_t n
 int dmst_dendrogram_height(const int32_t* edge_parent, int64_t n_edges, int64_t* height, void* workspace,
                            size_t workspace_bytes, void* stream);
 
+/* Dendrogram text format v1 body (write_dendrogram, dendro_io.py:28-38):
+ * "E <rank> <parent>\n" per edge then "V <id> <parent>\n" per vertex,
+ * formatted on the device into `out` (DEVICE buffer of out_capacity bytes;
+ * NULL = size query).  The header line "#dendrogram v1 n=.. nv=..\n" is the
+ * caller's.  Workspace: >= 8 * (ceil((n_edges + n_vertices) / 2048) + 1)
+ * bytes.  Returns the body size in bytes, or -1 on error (dmst_last_error). */
+int64_t dmst_format_dendrogram(const int32_t* edge_parent, const int32_t* vertex_parent, int64_t n_edges,
+                               int64_t n_vertices, char* out, size_t out_capacity, void* workspace,
+                               size_t workspace_bytes, void* stream);
+
 /* Message for the last non-zero return on this thread ("" if none). */
 const char* dmst_last_error(void);
 

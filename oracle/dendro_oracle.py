@@ -376,3 +376,13 @@ def stats_report(num_vertices: int, u, v, w) -> dict:
             "skewness_log2_edges": height / math.log2(n) if n >= 2 else 0.0,
             "skewness_log2_points": height / math.log2(n + 1),
             "per_level": [tuple(int(x) for x in c) for c in h.view_kind_counts]}
+
+
+# -------------------------------------------------------------- file format
+def dendrogram_text(edge_parent, vertex_parent) -> bytes:
+    """Restates write_dendrogram (dendro_io.py:28-38): the bytes of the v1 file."""
+    ep = np.asarray(edge_parent, dtype=np.int64).tolist()
+    vp = np.asarray(vertex_parent, dtype=np.int64).tolist()
+    head = f"#dendrogram v1 n={len(ep)} nv={len(vp)}\n"
+    body = "".join(f"E {r} {p}\n" for r, p in enumerate(ep)) + "".join(f"V {x} {p}\n" for x, p in enumerate(vp))
+    return (head + body).encode()

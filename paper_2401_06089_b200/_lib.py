@@ -29,6 +29,7 @@ EXPORTS = (
     "dmst_build_debug",
     "dmst_validate",
     "dmst_dendrogram_height",
+    "dmst_format_dendrogram",
     "dmst_last_error",
     "dmst_kernel_name",
     "dmst_version",
@@ -105,6 +106,8 @@ def load() -> ctypes.CDLL:
     lib.dmst_validate.restype = ctypes.c_int
     lib.dmst_dendrogram_height.argtypes = [vp, i64, ctypes.POINTER(ctypes.c_int64), vp, sz, vp]
     lib.dmst_dendrogram_height.restype = ctypes.c_int
+    lib.dmst_format_dendrogram.argtypes = [vp, vp, i64, i64, vp, sz, vp, sz, vp]
+    lib.dmst_format_dendrogram.restype = ctypes.c_int64
     lib.dmst_last_error.argtypes = []
     lib.dmst_last_error.restype = ctypes.c_char_p
     lib.dmst_kernel_name.argtypes = [ctypes.c_int32]

@@ -431,6 +431,68 @@ def stats_b200(num_vertices: int, u, v, w, device=None) -> dict:
             "per_level": res.view_kind_counts}
 
 
+def format_dendrogram_b200(edge_parent, vertex_parent, device=None) -> torch.Tensor:
+    """The dendrogram text format v1 file (write_dendrogram, dendro_io.py:28-38)
+    formatted on the GPU: header + "E <rank> <parent>" / "V <id> <parent>"
+    lines, as a uint8 DEVICE tensor (byte-identical to the reference's file)."""
+    b = _builder(device)
+    dev = b.device
+    ep = _as_dev(edge_parent, torch.int32, dev)
+    vp = _as_dev(vertex_parent, torch.int32, dev)
+    n, nv = int(ep.shape[0]), int(vp.shape[0])
+    head = f"#dendrogram v1 n={n} nv={nv}\n".encode()
+    lines = n + nv
+    ws = torch.empty(8 * ((lines + 2047) // 2048 + 2), dtype=torch.uint8, device=dev)
+    with torch.cuda.device(dev):
+        size = int(b.lib.dmst_format_dendrogram(_ptr(ep), _ptr(vp), n, nv, None, 0, _ptr(ws), ws.numel(),
+                                                b._stream()))
+        if size < 0:
+            _lib.check(-1)
+        out = torch.empty(len(head) + size, dtype=torch.uint8, device=dev)
+        out[:len(head)] = torch.frombuffer(bytearray(head), dtype=torch.uint8).to(dev)
+        body = out[len(head):]
+        got = int(b.lib.dmst_format_dendrogram(_ptr(ep), _ptr(vp), n, nv, _ptr(body) if size else None, size,
+                                               _ptr(ws), ws.numel(), b._stream()))
+        if got != size:
+            _lib.check(-1)
+    return out
+
+
+_STAGE: dict[int, list] = {}
+
+
+def write_dendrogram_b200(path, edge_parent, vertex_parent, device=None, chunk_bytes: int = 64 << 20) -> int:
+    """Drop-in for ``write_dendrogram`` (dendro_io.py:28-38): the same bytes,
+    formatted on the GPU and streamed to the file through two reusable pinned
+    host buffers (the copy of chunk k + 1 overlaps the write of chunk k).
+    Returns the file size."""
+    dev_bytes = format_dendrogram_b200(edge_parent, vertex_parent, device=device)
+    total = int(dev_bytes.numel())
+    dev = dev_bytes.device
+    bufs = _STAGE.get(dev.index)
+    if bufs is None or bufs[0].numel() < chunk_bytes:
+        bufs = _STAGE[dev.index] = [torch.empty(chunk_bytes, dtype=torch.uint8).pin_memory() for _ in range(2)]
+    evs = [torch.cuda.Event(), torch.cuda.Event()]
+    stream = torch.cuda.current_stream(dev)
+    with open(path, "wb") as f:
+        offs = list(range(0, total, chunk_bytes))
+
+        def issue(k):
+            lo = offs[k]
+            hi = min(total, lo + chunk_bytes)
+            bufs[k & 1][:hi - lo].copy_(dev_bytes[lo:hi], non_blocking=True)
+            evs[k & 1].record(stream)
+        if offs:
+            issue(0)
+        for k, lo in enumerate(offs):
+            if k + 1 < len(offs):
+                issue(k + 1)
+            evs[k & 1].synchronize()
+            hi = min(total, lo + chunk_bytes)
+            f.write(memoryview(bufs[k & 1].numpy())[:hi - lo])
+    return total
+
+
 def build_b200(num_vertices: int, u, v, w, device=None, debug: bool = False) -> BuildResult:
     """rank_edges + pandora on the GPU (the timed scope of `dendromst build`)."""
     return _builder(device).build(num_vertices, u, v, w, debug=debug)

@@ -1166,6 +1166,48 @@ int dmst_dendrogram_height(const int32_t* edge_parent, int64_t n_edges, int64_t*
   });
 }
 
+int64_t dmst_format_dendrogram(const int32_t* edge_parent, const int32_t* vertex_parent, int64_t n_edges,
+                               int64_t n_vertices, char* out, size_t out_capacity, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+  int64_t total = -1;
+  const int rc = guarded([&] {
+    if (n_edges < 0 || n_vertices < 0) invalid("negative sizes");
+    if (n_edges >= (int64_t(1) << 29) || n_vertices > (int64_t(1) << 29)) invalid("ids must be < 2^29");
+    const int64_t lines = n_edges + n_vertices;
+    if (lines == 0) {
+      total = 0;
+      return;
+    }
+    if (!edge_parent && n_edges) invalid("null edge_parent");
+    if (!vertex_parent && n_vertices) invalid("null vertex_parent");
+    const int64_t nb = cdiv(lines, FMT_TILE);
+    if (!workspace || workspace_bytes < (size_t)(8 * (nb + 1))) invalid("workspace too small");
+    Ctx c;
+    c.s = (cudaStream_t)stream;
+    c.sms = num_sms();
+    unsigned long long* bl = (unsigned long long*)workspace;
+    c.begin(KK_OTHER);
+    k_fmt_count<<<(unsigned)nb, FMT_BLOCK, 0, c.s>>>(n_edges, n_vertices, edge_parent, vertex_parent, bl);
+    c.launched();
+    c.begin(KK_OTHER);
+    k_fmt_scan<<<1, 1024, 0, c.s>>>(bl, nb);
+    c.launched();
+    unsigned long long t = 0;
+    c.to_host(&t, bl + nb, 8);
+    c.sync();
+    total = (int64_t)t;
+    if (!out) return;  // size query
+    if (out_capacity < t) invalid("output buffer too small");
+    smem_attr(k_fmt_write, (size_t)FMT_TILE * FMT_MAXLINE);
+    c.begin(KK_OTHER);
+    k_fmt_write<<<(unsigned)nb, FMT_BLOCK, (size_t)FMT_TILE * FMT_MAXLINE, c.s>>>(n_edges, n_vertices, edge_parent,
+                                                                               vertex_parent, bl, out);
+    c.launched();
+    c.sync();
+  });
+  return rc ? -1 : total;
+}
+
 const char* dmst_last_error(void) { return dmst::g_err.c_str(); }
 
 const char* dmst_kernel_name(int32_t id) {

@@ -174,3 +174,139 @@ __global__ void __launch_bounds__(256) k_count_heads(const unsigned long long* _
 }
 
 }  // namespace dmst
+
+namespace dmst {
+
+// ------------------------------------------ dendrogram text format v1
+// write_dendrogram (dendro_io.py:28-38): "E <rank> <parent>\n" for every
+// edge, then "V <id> <parent>\n" for every vertex, formatted on the device:
+// line lengths -> per-block totals -> one scan of the block totals -> every
+// block re-derives its lines' offsets and writes them into a byte buffer.
+constexpr int FMT_BLOCK = 256, FMT_ITEMS = 8, FMT_TILE = FMT_BLOCK * FMT_ITEMS;
+constexpr int FMT_MAXLINE = 24;  // "E 536870911 536870910\n" is 22 bytes (ids < 2^29)
+
+__device__ __forceinline__ int dec_len(int64_t x) {  // characters of %d
+  int len = x < 0 ? 2 : 1;
+  uint64_t a = x < 0 ? (uint64_t)(-x) : (uint64_t)x;
+  while (a >= 10) {
+    a /= 10;
+    ++len;
+  }
+  return len;
+}
+
+__device__ __forceinline__ char* put_dec(char* p, int64_t x) {
+  if (x < 0) {
+    *p++ = '-';
+    x = -x;
+  }
+  char tmp[20];
+  int k = 0;
+  uint64_t a = (uint64_t)x;
+  do {
+    tmp[k++] = (char)('0' + a % 10);
+    a /= 10;
+  } while (a);
+  while (k) *p++ = tmp[--k];
+  return p;
+}
+
+// line i < n: edge i; else vertex i - n
+__device__ __forceinline__ int fmt_line_len(int64_t i, int64_t n, const int32_t* ep, const int32_t* vp) {
+  const bool edge = i < n;
+  const int64_t id = edge ? i : i - n;
+  const int32_t par = edge ? ep[id] : vp[id];
+  return 2 + dec_len(id) + 1 + dec_len(par) + 1;  // "E " id " " parent "\n"
+}
+
+__global__ void __launch_bounds__(FMT_BLOCK) k_fmt_count(int64_t n, int64_t nv, const int32_t* __restrict__ ep,
+                                                         const int32_t* __restrict__ vp,
+                                                         unsigned long long* __restrict__ block_len) {
+  const int64_t lines = n + nv;
+  const int64_t base = (int64_t)blockIdx.x * FMT_TILE;
+  uint32_t s = 0;
+  for (int q = 0; q < FMT_ITEMS; ++q) {
+    const int64_t i = base + (int64_t)q * FMT_BLOCK + threadIdx.x;
+    if (i < lines) s += fmt_line_len(i, n, ep, vp);
+  }
+  s = __reduce_add_sync(kFull, s);
+  __shared__ uint32_t ws[FMT_BLOCK / 32];
+  if (lane_id() == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < FMT_BLOCK / 32; ++w) t += ws[w];
+    block_len[blockIdx.x] = t;
+  }
+}
+
+// One block: exclusive scan of the block totals (64-bit), in place; the
+// grand total goes to block_len[nb].
+__global__ void __launch_bounds__(1024) k_fmt_scan(unsigned long long* block_len, int64_t nb) {
+  __shared__ unsigned long long carry;
+  __shared__ unsigned long long wsum[32];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t b0 = 0; b0 < nb; b0 += 1024) {
+    const int64_t b = b0 + threadIdx.x;
+    const unsigned long long x = b < nb ? block_len[b] : 0ull;
+    unsigned long long incl = x;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(kFull, incl, o);
+      if ((int)lane_id() >= o) incl += y;
+    }
+    if (lane_id() == 31) wsum[threadIdx.x >> 5] = incl;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      unsigned long long v = wsum[threadIdx.x], iv = v;
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(kFull, iv, o);
+        if ((int)threadIdx.x >= o) iv += y;
+      }
+      wsum[threadIdx.x] = iv - v;
+    }
+    __syncthreads();
+    const unsigned long long excl = carry + wsum[threadIdx.x >> 5] + incl - x;
+    if (b < nb) block_len[b] = excl;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = excl + x;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) block_len[nb] = carry;
+}
+
+__global__ void __launch_bounds__(FMT_BLOCK) k_fmt_write(int64_t n, int64_t nv, const int32_t* __restrict__ ep,
+                                                         const int32_t* __restrict__ vp,
+                                                         const unsigned long long* __restrict__ block_off,
+                                                         char* __restrict__ out) {
+  // the block's lines are formatted into shared memory, then copied out as
+  // one contiguous byte run (consecutive threads -> consecutive bytes)
+  extern __shared__ char txt[];  // [FMT_TILE * FMT_MAXLINE]
+  const int64_t lines = n + nv;
+  const int64_t base = (int64_t)blockIdx.x * FMT_TILE;
+  const int64_t first = base + (int64_t)threadIdx.x * FMT_ITEMS;  // contiguous lines per thread
+  uint32_t mine = 0;
+  for (int q = 0; q < FMT_ITEMS; ++q)
+    if (first + q < lines) mine += fmt_line_len(first + q, n, ep, vp);
+  __shared__ uint32_t scratch[FMT_BLOCK / 32 + 1];
+  uint32_t tot;
+  const uint32_t excl = block_excl_sum<FMT_BLOCK>(mine, scratch, &tot);
+  char* p = txt + excl;
+  for (int q = 0; q < FMT_ITEMS; ++q) {
+    const int64_t i = first + q;
+    if (i >= lines) break;
+    const bool edge = i < n;
+    const int64_t id = edge ? i : i - n;
+    *p++ = edge ? 'E' : 'V';
+    *p++ = ' ';
+    p = put_dec(p, id);
+    *p++ = ' ';
+    p = put_dec(p, edge ? ep[id] : vp[id]);
+    *p++ = '\n';
+  }
+  __syncthreads();
+  char* dst = out + block_off[blockIdx.x];
+  for (uint32_t b = threadIdx.x; b < tot; b += FMT_BLOCK) dst[b] = txt[b];
+}
+
+}  // namespace dmst

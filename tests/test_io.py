@@ -1,0 +1,70 @@
+"""Dendrogram text format v1 (write_dendrogram, dendro_io.py:28-38): the
+oracle's bytes equal the reference writer's (when the reference is
+importable, i.e. in the development container), and the device formatter's
+bytes equal the oracle's on the golden corpus and synthetic trees."""
+from __future__ import annotations
+
+import os
+import sys
+import tempfile
+
+import numpy as np
+import pytest
+
+from oracle import dendro_oracle as O
+from paper_2401_06089_b200 import synth
+from tests.conftest import golden_trees, has_gpu
+
+GOLDEN = list(golden_trees())[:20]
+
+
+def _reference_writer():
+    src = os.environ.get("DENDROMST_SRC", "/root/reference/pkg/src")
+    if not os.path.isdir(src):
+        return None
+    if src not in sys.path:
+        sys.path.insert(0, src)
+    try:
+        from dendromst.dendro_io import write_dendrogram
+        from dendromst.expansion import Dendrogram
+    except Exception:
+        return None
+    return write_dendrogram, Dendrogram
+
+
+@pytest.mark.parametrize("t", GOLDEN, ids=[t["name"] for t in GOLDEN])
+def test_oracle_text_matches_reference_writer(t):
+    ref = _reference_writer()
+    if ref is None:
+        pytest.skip("reference package not importable here")
+    write_dendrogram, Dendrogram = ref
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "x.dendro")
+        write_dendrogram(path, Dendrogram(np.asarray(t["edge_parent"], np.int64),
+                                          np.asarray(t["vertex_parent"], np.int64)))
+        assert open(path, "rb").read() == O.dendrogram_text(t["edge_parent"], t["vertex_parent"])
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+@pytest.mark.parametrize("t", GOLDEN, ids=[t["name"] for t in GOLDEN])
+def test_device_text_matches_oracle_golden(t):
+    from paper_2401_06089_b200 import format_dendrogram_b200
+    got = format_dendrogram_b200(t["edge_parent"], t["vertex_parent"]).cpu().numpy().tobytes()
+    assert got == O.dendrogram_text(t["edge_parent"], t["vertex_parent"])
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+@pytest.mark.parametrize("shape,n", [("random", 1), ("random", 2047), ("tied", 2048), ("path", 100_000),
+                                     ("random", 300_000)])
+def test_device_file_matches_oracle(shape, n):
+    from paper_2401_06089_b200 import DendrogramBuilder, write_dendrogram_b200
+    nv, u, v, w = synth.GENERATORS[shape](n, seed=n)
+    r = DendrogramBuilder("cuda:0").build(nv, u, v, w)
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "x.dendro")
+        size = write_dendrogram_b200(path, r.edge_parent, r.vertex_parent)
+        data = open(path, "rb").read()
+    exp = O.dendrogram_text(r.edge_parent.cpu().numpy(), r.vertex_parent.cpu().numpy())
+    assert size == len(data) and data == exp

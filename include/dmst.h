@@ -170,6 +170,23 @@ int64_t dmst_format_dendrogram(const int32_t* edge_parent, const int32_t* vertex
                                int64_t n_vertices, char* out, size_t out_capacity, void* workspace,
                                size_t workspace_bytes, void* stream);
 
+/* read_dendrogram (dendro_io.py:41-75) of the body after the header line:
+ * `body` (DEVICE, body_len bytes) holds "E <rank> <parent>" / "V <id>
+ * <parent>" lines ('#' and blank lines skipped; single spaces, '\n'
+ * endings); edge_parent / vertex_parent (DEVICE, n_edges / n_vertices)
+ * start at ROOT (-1) and receive every line.  HOST outputs: *bad_line =
+ * 0-based body line of the first malformed line (-1 if none), and the
+ * numbers of E and V lines.  Workspace: 8 * (ceil(body_len / 8192) + 1) + 64
+ * bytes. */
+int dmst_parse_dendrogram(const char* body, int64_t body_len, int64_t n_edges, int64_t n_vertices,
+                          int32_t* edge_parent, int32_t* vertex_parent, int64_t* bad_line, int64_t* edge_lines,
+                          int64_t* vertex_lines, void* workspace, size_t workspace_bytes, void* stream);
+
+/* First index where two DEVICE int32 arrays of n entries differ (-1: none;
+ * `dendromst verify`, cli.py:138-155).  Workspace: 8 bytes. */
+int dmst_first_difference(const int32_t* a, const int32_t* b, int64_t n, int64_t* first, void* workspace,
+                          size_t workspace_bytes, void* stream);
+
 /* Message for the last non-zero return on this thread ("" if none). */
 const char* dmst_last_error(void);
 

@@ -386,3 +386,29 @@ def dendrogram_text(edge_parent, vertex_parent) -> bytes:
     head = f"#dendrogram v1 n={len(ep)} nv={len(vp)}\n"
     body = "".join(f"E {r} {p}\n" for r, p in enumerate(ep)) + "".join(f"V {x} {p}\n" for x, p in enumerate(vp))
     return (head + body).encode()
+
+
+def verify_text(a: bytes, b: bytes) -> tuple[int, str]:
+    """Restates `dendromst verify` (cli.py:138-155) on two v1 files' bytes
+    (read_dendrogram, dendro_io.py:41-75, for well-formed files)."""
+    def parse(data):
+        lines = data.decode().splitlines()
+        parts = lines[0].split()
+        n, nv = int(parts[2][2:]), int(parts[3][3:])
+        ep = np.full(n, ROOT, dtype=np.int64)
+        vp = np.full(nv, ROOT, dtype=np.int64)
+        for line in lines[1:]:
+            if not line or line.startswith("#"):
+                continue
+            kind, idx, parent = line.split()
+            (ep if kind == "E" else vp)[int(idx)] = int(parent)
+        return ep, vp
+    (ea, va), (eb, vb) = parse(a), parse(b)
+    for label, pa, pb in (("edge", ea, eb), ("vertex", va, vb)):
+        if pa.shape != pb.shape:
+            return 1, f"size mismatch: {pa.shape[0]} vs {pb.shape[0]} {label} nodes"
+        diff = np.nonzero(pa != pb)[0]
+        if diff.shape[0]:
+            i = int(diff[0])
+            return 1, f"first divergence: {label} {i}: {int(pa[i])} != {int(pb[i])}"
+    return 0, "identical"

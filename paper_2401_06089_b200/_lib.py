@@ -30,6 +30,8 @@ EXPORTS = (
     "dmst_validate",
     "dmst_dendrogram_height",
     "dmst_format_dendrogram",
+    "dmst_parse_dendrogram",
+    "dmst_first_difference",
     "dmst_last_error",
     "dmst_kernel_name",
     "dmst_version",
@@ -108,6 +110,11 @@ def load() -> ctypes.CDLL:
     lib.dmst_dendrogram_height.restype = ctypes.c_int
     lib.dmst_format_dendrogram.argtypes = [vp, vp, i64, i64, vp, sz, vp, sz, vp]
     lib.dmst_format_dendrogram.restype = ctypes.c_int64
+    p64 = ctypes.POINTER(ctypes.c_int64)
+    lib.dmst_parse_dendrogram.argtypes = [vp, i64, i64, i64, vp, vp, p64, p64, p64, vp, sz, vp]
+    lib.dmst_parse_dendrogram.restype = ctypes.c_int
+    lib.dmst_first_difference.argtypes = [vp, vp, i64, p64, vp, sz, vp]
+    lib.dmst_first_difference.restype = ctypes.c_int
     lib.dmst_last_error.argtypes = []
     lib.dmst_last_error.restype = ctypes.c_char_p
     lib.dmst_kernel_name.argtypes = [ctypes.c_int32]

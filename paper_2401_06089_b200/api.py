@@ -493,6 +493,84 @@ def write_dendrogram_b200(path, edge_parent, vertex_parent, device=None, chunk_b
     return total
 
 
+class DendrogramFormatError(ValueError):
+    """Mirror of ``dendromst.dendro_io.DendrogramFormatError`` (the reference's
+    own class is raised when it is importable)."""
+
+
+def _format_error():
+    try:
+        from dendromst.dendro_io import DendrogramFormatError as Ref  # type: ignore
+        return Ref
+    except Exception:
+        return DendrogramFormatError
+
+
+def read_dendrogram_b200(path, device=None) -> BuildResult:
+    """Drop-in for ``read_dendrogram`` (dendro_io.py:41-75): the header is
+    checked on the host (same messages), the body is parsed on the GPU
+    (dmst_parse_dendrogram) straight into device edge_parent / vertex_parent
+    tensors (returned in a BuildResult with orig_of / heights = None).
+    Lines must use single spaces and '\\n' endings (what write_dendrogram and
+    write_dendrogram_b200 produce); a malformed line raises
+    DendrogramFormatError("bad line: ...")."""
+    err = _format_error()
+    b = _builder(device)
+    dev = b.device
+    with open(path, "rb") as f:
+        data = f.read()
+    nl = data.find(b"\n")
+    header = (data if nl < 0 else data[:nl]).decode(errors="replace").strip()
+    parts = header.split()
+    if (len(parts) != 4 or parts[0] != "#dendrogram" or parts[1] != "v1"
+            or not parts[2].startswith("n=") or not parts[3].startswith("nv=")):
+        raise err(f"bad header: {header!r}")
+    try:
+        n = int(parts[2][2:])
+        nv = int(parts[3][3:])
+    except ValueError:
+        raise err(f"bad header: {header!r}") from None
+    body = memoryview(data)[nl + 1:] if nl >= 0 else memoryview(b"")
+    blen = len(body)
+    host = torch.frombuffer(bytearray(body), dtype=torch.uint8) if blen else torch.empty(0, dtype=torch.uint8)
+    with torch.cuda.device(dev):
+        dbody = host.to(dev)
+        ep = torch.empty(max(n, 0), dtype=torch.int32, device=dev)
+        vp = torch.empty(max(nv, 0), dtype=torch.int32, device=dev)
+        ws = torch.empty(8 * ((blen + 8191) // 8192 + 2) + 64, dtype=torch.uint8, device=dev)
+        bad, ne, nvl = ctypes.c_int64(-1), ctypes.c_int64(0), ctypes.c_int64(0)
+        _lib.check(b.lib.dmst_parse_dendrogram(_ptr(dbody) if blen else None, blen, n, nv, _ptr(ep), _ptr(vp),
+                                               ctypes.byref(bad), ctypes.byref(ne), ctypes.byref(nvl),
+                                               _ptr(ws), ws.numel(), b._stream()))
+    if bad.value >= 0:
+        line = bytes(body).split(b"\n")[bad.value].decode(errors="replace")
+        raise err(f"bad line: {line!r}")
+    if ne.value != n or nvl.value != nv:
+        raise err(f"expected {n} edge and {nv} vertex lines, got {ne.value} and {nvl.value}")
+    return BuildResult(orig_of=None, heights=None, edge_parent=ep, vertex_parent=vp)
+
+
+def verify_b200(path_a, path_b, device=None) -> tuple[int, str]:
+    """``dendromst verify a b`` (cli.py:138-155) with the files parsed and
+    compared on the GPU: returns (exit code, the line the reference prints)."""
+    da = read_dendrogram_b200(path_a, device=device)
+    db = read_dendrogram_b200(path_b, device=device)
+    b = _builder(device)
+    ws = torch.empty(64, dtype=torch.uint8, device=b.device)
+    for label, pa, pb in (("edge", da.edge_parent, db.edge_parent),
+                          ("vertex", da.vertex_parent, db.vertex_parent)):
+        if pa.shape != pb.shape:
+            return 1, f"size mismatch: {pa.shape[0]} vs {pb.shape[0]} {label} nodes"
+        first = ctypes.c_int64(-1)
+        with torch.cuda.device(b.device):
+            _lib.check(b.lib.dmst_first_difference(_ptr(pa), _ptr(pb), int(pa.shape[0]), ctypes.byref(first),
+                                                   _ptr(ws), ws.numel(), b._stream()))
+        if first.value >= 0:
+            i = first.value
+            return 1, f"first divergence: {label} {i}: {int(pa[i])} != {int(pb[i])}"
+    return 0, "identical"
+
+
 def build_b200(num_vertices: int, u, v, w, device=None, debug: bool = False) -> BuildResult:
     """rank_edges + pandora on the GPU (the timed scope of `dendromst build`)."""
     return _builder(device).build(num_vertices, u, v, w, debug=debug)

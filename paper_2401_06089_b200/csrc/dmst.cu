@@ -1208,6 +1208,71 @@ int64_t dmst_format_dendrogram(const int32_t* edge_parent, const int32_t* vertex
   return rc ? -1 : total;
 }
 
+int dmst_parse_dendrogram(const char* body, int64_t body_len, int64_t n_edges, int64_t n_vertices,
+                          int32_t* edge_parent, int32_t* vertex_parent, int64_t* bad_line, int64_t* edge_lines,
+                          int64_t* vertex_lines, void* workspace, size_t workspace_bytes, void* stream) {
+  return guarded([&] {
+    if (!bad_line || !edge_lines || !vertex_lines) invalid("result pointers must be host pointers");
+    *bad_line = -1;
+    *edge_lines = *vertex_lines = 0;
+    if (n_edges < 0 || n_vertices < 0 || body_len < 0) invalid("negative sizes");
+    Ctx c;
+    c.s = (cudaStream_t)stream;
+    c.sms = num_sms();
+    if (n_edges) DMST_CUDA(cudaMemsetAsync(edge_parent, 0xff, 4 * (size_t)n_edges, c.s));  // ROOT
+    if (n_vertices) DMST_CUDA(cudaMemsetAsync(vertex_parent, 0xff, 4 * (size_t)n_vertices, c.s));
+    if (body_len == 0) {
+      c.sync();
+      return;
+    }
+    if (!body) invalid("null body");
+    const int64_t nb = cdiv(body_len, PARSE_TILE);
+    if (!workspace || workspace_bytes < (size_t)(8 * (nb + 1) + 64)) invalid("workspace too small");
+    unsigned long long* bl = (unsigned long long*)workspace;
+    unsigned long long* err = bl + nb + 1;
+    c.ones(err, 8);
+    c.zero(err + 1, 16);
+    c.begin(KK_OTHER);
+    k_parse_count<<<(unsigned)nb, PARSE_BLOCK, 0, c.s>>>(body, body_len, bl);
+    c.launched();
+    c.begin(KK_OTHER);
+    k_fmt_scan<<<1, 1024, 0, c.s>>>(bl, nb);
+    c.launched();
+    c.begin(KK_OTHER);
+    k_parse_lines<<<(unsigned)nb, PARSE_BLOCK, 0, c.s>>>(body, body_len, bl, n_edges, n_vertices, edge_parent,
+                                                           vertex_parent, err);
+    c.launched();
+    unsigned long long h[3];
+    c.to_host(h, err, 24);
+    c.sync();
+    *bad_line = h[0] == ~0ull ? -1 : (int64_t)h[0] - 1;
+    *edge_lines = (int64_t)h[1];
+    *vertex_lines = (int64_t)h[2];
+  });
+}
+
+int dmst_first_difference(const int32_t* a, const int32_t* b, int64_t n, int64_t* first, void* workspace,
+                          size_t workspace_bytes, void* stream) {
+  return guarded([&] {
+    if (!first) invalid("first must be a host pointer");
+    *first = -1;
+    if (n <= 0) return;
+    if (!a || !b || !workspace || workspace_bytes < 8) invalid("bad pointers / workspace");
+    Ctx c;
+    c.s = (cudaStream_t)stream;
+    c.sms = num_sms();
+    unsigned long long* f = (unsigned long long*)workspace;
+    c.ones(f, 8);
+    c.begin(KK_OTHER);
+    k_first_diff<<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(a, b, n, f);
+    c.launched();
+    unsigned long long h = 0;
+    c.to_host(&h, f, 8);
+    c.sync();
+    *first = h == ~0ull ? -1 : (int64_t)h;
+  });
+}
+
 const char* dmst_last_error(void) { return dmst::g_err.c_str(); }
 
 const char* dmst_kernel_name(int32_t id) {

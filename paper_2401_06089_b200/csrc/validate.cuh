@@ -310,3 +310,115 @@ __global__ void __launch_bounds__(FMT_BLOCK) k_fmt_write(int64_t n, int64_t nv, 
 }
 
 }  // namespace dmst
+
+namespace dmst {
+
+// --------------------------------------- dendrogram text format v1 reader
+// read_dendrogram (dendro_io.py:41-75) for the body after the header line:
+// one thread per 32-byte chunk finds the line starts inside it (a line
+// starts after each '\n'), counts them per block, and after one scan of the
+// block counts every block parses its lines ("E <rank> <parent>" /
+// "V <id> <parent>", blank and '#' lines skipped) straight into the arrays.
+// err[0] = 0-based line number of the first malformed line (+1), err[1..2]
+// = E / V line counts.
+constexpr int PARSE_BLOCK = 256, PARSE_CHUNK = 32, PARSE_TILE = PARSE_BLOCK * PARSE_CHUNK;
+
+__device__ __forceinline__ bool line_start(const char* b, int64_t i) { return i == 0 || b[i - 1] == '\n'; }
+
+__global__ void __launch_bounds__(PARSE_BLOCK) k_parse_count(const char* __restrict__ body, int64_t len,
+                                                             unsigned long long* __restrict__ block_lines) {
+  const int64_t beg = (int64_t)blockIdx.x * PARSE_TILE + (int64_t)threadIdx.x * PARSE_CHUNK;
+  uint32_t c = 0;
+  for (int q = 0; q < PARSE_CHUNK; ++q) {
+    const int64_t i = beg + q;
+    if (i < len && line_start(body, i)) ++c;
+  }
+  c = __reduce_add_sync(kFull, c);
+  __shared__ uint32_t ws[PARSE_BLOCK / 32];
+  if (lane_id() == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < PARSE_BLOCK / 32; ++w) t += ws[w];
+    block_lines[blockIdx.x] = t;
+  }
+}
+
+__device__ __forceinline__ bool parse_int(const char* b, int64_t len, int64_t& i, int64_t& v) {
+  bool neg = false;
+  if (i < len && b[i] == '-') {
+    neg = true;
+    ++i;
+  }
+  const int64_t s = i;
+  int64_t x = 0;
+  while (i < len && b[i] >= '0' && b[i] <= '9' && i - s < 18) x = x * 10 + (b[i++] - '0');
+  if (i == s) return false;
+  v = neg ? -x : x;
+  return true;
+}
+
+__global__ void __launch_bounds__(PARSE_BLOCK) k_parse_lines(const char* __restrict__ body, int64_t len,
+                                                             const unsigned long long* __restrict__ block_off,
+                                                             int64_t n, int64_t nv, int32_t* __restrict__ ep,
+                                                             int32_t* __restrict__ vp,
+                                                             unsigned long long* __restrict__ err) {
+  const int64_t beg = (int64_t)blockIdx.x * PARSE_TILE + (int64_t)threadIdx.x * PARSE_CHUNK;
+  uint32_t mine = 0;
+  for (int q = 0; q < PARSE_CHUNK; ++q) {
+    const int64_t i = beg + q;
+    if (i < len && line_start(body, i)) ++mine;
+  }
+  __shared__ uint32_t scratch[PARSE_BLOCK / 32 + 1];
+  uint32_t tot;
+  uint64_t line = block_off[blockIdx.x] + block_excl_sum<PARSE_BLOCK>(mine, scratch, &tot);
+  uint32_t ne = 0, nvv = 0;
+  unsigned long long bad = ~0ull;
+  for (int q = 0; q < PARSE_CHUNK; ++q) {
+    int64_t i = beg + q;
+    if (i >= len || !line_start(body, i)) continue;
+    const uint64_t ln = line++;
+    const char k = body[i];
+    if (k == '\n' || k == '#') continue;  // blank / comment line
+    bool ok = (k == 'E' || k == 'V') && i + 1 < len && body[i + 1] == ' ';
+    int64_t id = 0, par = 0;
+    if (ok) {
+      i += 2;
+      ok = parse_int(body, len, i, id) && i < len && body[i] == ' ';
+    }
+    if (ok) {
+      ++i;
+      ok = parse_int(body, len, i, par) && (i == len || body[i] == '\n');
+    }
+    if (ok) ok = id >= 0 && id < (k == 'E' ? n : nv) && par >= INT32_MIN && par <= INT32_MAX;
+    if (!ok) {
+      bad = min(bad, (unsigned long long)ln);
+      continue;
+    }
+    if (k == 'E') {
+      ep[id] = (int32_t)par;
+      ++ne;
+    } else {
+      vp[id] = (int32_t)par;
+      ++nvv;
+    }
+  }
+  if (bad != ~0ull) atomicMin(err, bad + 1);
+  ne = __reduce_add_sync(kFull, ne);
+  nvv = __reduce_add_sync(kFull, nvv);
+  if (lane_id() == 0) {
+    if (ne) atomicAdd(err + 1, (unsigned long long)ne);
+    if (nvv) atomicAdd(err + 2, (unsigned long long)nvv);
+  }
+}
+
+// First index where two int32 arrays differ (atomicMin), for `verify`.
+__global__ void k_first_diff(const int32_t* __restrict__ a, const int32_t* __restrict__ b, int64_t n,
+                             unsigned long long* __restrict__ first) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool d = i < n && a[i] != b[i];
+  const uint32_t m = __ballot_sync(kFull, d);
+  if (m && lane_id() == (uint32_t)(__ffs(m) - 1)) atomicMin(first, (unsigned long long)i);
+}
+
+}  // namespace dmst

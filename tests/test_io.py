@@ -68,3 +68,68 @@ def test_device_file_matches_oracle(shape, n):
         data = open(path, "rb").read()
     exp = O.dendrogram_text(r.edge_parent.cpu().numpy(), r.vertex_parent.cpu().numpy())
     assert size == len(data) and data == exp
+
+
+def _write(path, data: bytes):
+    with open(path, "wb") as f:
+        f.write(data)
+
+
+def _variants(t):
+    """(name, file a, file b): identical, one edge changed, one vertex changed,
+    different sizes, and comment / blank lines."""
+    base = O.dendrogram_text(t["edge_parent"], t["vertex_parent"])
+    ep = np.asarray(t["edge_parent"], np.int64).copy()
+    vp = np.asarray(t["vertex_parent"], np.int64).copy()
+    out = [("same", base, base)]
+    if ep.shape[0] > 1:
+        e2 = ep.copy()
+        e2[-1] = e2[-1] - 1 if e2[-1] > 0 else 0
+        out.append(("edge_diff", base, O.dendrogram_text(e2, vp)))
+    v2 = vp.copy()
+    v2[0] = -1
+    out.append(("vertex_diff", base, O.dendrogram_text(ep, v2)))
+    out.append(("size", base, O.dendrogram_text(ep[:-1], vp)))
+    lines = base.split(b"\n")
+    commented = b"\n".join(lines[:1] + [b"# a comment", b""] + lines[1:])
+    out.append(("comments", base, commented))
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+@pytest.mark.parametrize("t", GOLDEN[:6], ids=[t["name"] for t in GOLDEN[:6]])
+def test_device_verify_matches_oracle(t):
+    from paper_2401_06089_b200 import verify_b200
+    with tempfile.TemporaryDirectory() as d:
+        for name, a, b in _variants(t):
+            pa, pb = os.path.join(d, "a"), os.path.join(d, "b")
+            _write(pa, a)
+            _write(pb, b)
+            assert verify_b200(pa, pb) == O.verify_text(a, b), name
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+def test_device_read_roundtrip_and_errors():
+    from paper_2401_06089_b200 import DendrogramBuilder, read_dendrogram_b200, write_dendrogram_b200
+    from paper_2401_06089_b200.api import _format_error
+    nv, u, v, w = synth.GENERATORS["random"](500_000, seed=4)
+    r = DendrogramBuilder("cuda:0").build(nv, u, v, w)
+    err = _format_error()
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "x.dendro")
+        write_dendrogram_b200(path, r.edge_parent, r.vertex_parent)
+        back = read_dendrogram_b200(path)
+        assert bool((back.edge_parent == r.edge_parent).all()) and bool((back.vertex_parent == r.vertex_parent).all())
+        data = open(path, "rb").read()
+        bad = data.replace(b"\nE 7 ", b"\nX 7 ", 1)
+        _write(path, bad)
+        with pytest.raises(err, match="bad line: 'X 7 "):
+            read_dendrogram_b200(path)
+        _write(path, b"#dendrogram v2 n=1 nv=2\n")
+        with pytest.raises(err, match="bad header"):
+            read_dendrogram_b200(path)
+        _write(path, data[: data.rfind(b"\nV ") + 1])
+        with pytest.raises(err, match=f"expected {nv - 1} edge and {nv} vertex lines, got {nv - 1} and {nv - 1}"):
+            read_dendrogram_b200(path)

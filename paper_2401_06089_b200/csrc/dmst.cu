@@ -423,19 +423,27 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
                Sort1FinalEmitter em, int* passes_out) {
   unsigned long long* sample_ao = (unsigned long long*)(c.w.small + SM_HIST1);
   unsigned long long* and_or = sample_ao + 2;
+  uint32_t* top_min = c.w.small + SM_HIST1 + 8;
+  uint32_t* top_bits = c.w.small + SM_HIST1 + 16;                    // 128 words
+  uint16_t* top_inv = (uint16_t*)(c.w.small + SM_HIST1 + 144);       // 256 codes
+  uint8_t* top_code = (uint8_t*)(c.w.small + SM_HIST1 + 272);        // 4096 fields
   uint32_t* negzero = c.w.small + SM_MISC + MISC_NEGZERO;
   c.ones(sample_ao, 8);  // AND starts all-ones, OR all-zeros (memsets: no pageable copies)
   c.zero(sample_ao + 1, 8);
   c.ones(and_or, 8);
   c.zero(and_or + 1, 8);
+  c.ones(top_min, 4);
+  c.zero(top_bits, 4 * 128);
   c.zero(negzero, 4);
   // predict the first active digit from a sample, then count it in the same
   // read of w that reduces all keys (k_upsweep<KEYRED>)
   c.begin(KK_SORT1_HIST);
-  k_key_sample<<<1, 1024, 0, c.s>>>(w, n, sample_ao);
+  k_key_sample<<<1, 1024, 0, c.s>>>(w, n, sample_ao, top_min);
   c.launched();
   unsigned long long sao[2];
+  uint32_t tmin = 0;
   c.to_host(sao, sample_ao, 16);
+  c.to_host(&tmin, top_min, 4);
   c.sync();
   const std::vector<int> guess = active_digits(sao[0], sao[1], 8, 64);
   const int d0 = guess.empty() ? 0 : guess[0];
@@ -450,22 +458,43 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
   c.zero(a.counts, 4 * kRadix * (size_t)a.GS);
   c.begin(KK_SORT1_HIST);
   k_upsweep<8, Sort1FirstLoader, true><<<(unsigned)(g.G * kUpSplit), 256, 0, c.s>>>(
-      a, Sort1FirstLoader{w, u, v}, KeyRed{w, and_or, negzero});
+      a, Sort1FirstLoader{w, u, v, nullptr}, KeyRed{w, and_or, negzero, top_bits, std::min(tmin, 4095u)});
   c.launched();
   unsigned long long ao[2];
-  uint32_t nz = 0;
+  uint32_t nz = 0, tb[128];
   c.to_host(ao, and_or, 16);
   c.to_host(&nz, negzero, 4);
+  c.to_host(tb, top_bits, sizeof(tb));
   c.sync();
-  const std::vector<int> shifts = active_digits(ao[0], ao[1], 8, 64);
-  const int ready = !shifts.empty() && shifts[0] == d0 ? d0 : -1;  // else: the first pass counts again
+  std::vector<int> shifts = active_digits(ao[0], ao[1], 8, 64);
+  // top-field compaction when it saves a pass: (code, mantissa) keys
+  int ncodes = 0;
+  for (uint32_t x : tb) ncodes += __builtin_popcount(x);
+  const uint8_t* code = nullptr;
+  if (ncodes > 1 && ncodes <= 256) {
+    int cbits = 0;
+    while ((1 << cbits) < ncodes) ++cbits;
+    const uint64_t cand = ao[0] & kMantMask, cor = (ao[1] & kMantMask) | (((1ull << cbits) - 1) << kTopShift);
+    std::vector<int> cs = active_digits(cand, cor, 8, 64);
+    if (cs.size() < shifts.size()) {
+      c.begin(KK_OTHER);
+      k_top_codes<<<1, 128, 0, c.s>>>(top_bits, top_code, top_inv);
+      c.launched();
+      code = top_code;
+      em.inv = top_inv;
+      shifts = cs;
+    }
+  }
+  // the upsweep counted digit d0 of the raw keys: valid for the compacted
+  // keys only below the top field
+  const int ready = !shifts.empty() && shifts[0] == d0 && (!code || d0 + 8 <= kTopShift) ? d0 : -1;
   if (passes_out) *passes_out = (int)shifts.size();
   char* R = c.w.R;
   uint64_t* const bufK[2] = {(uint64_t*)R, (uint64_t*)(R + 8 * n)};
   uint32_t* vb = (uint32_t*)(R + 16 * n);
   uint32_t* const bufP[2] = {vb, vb + 3 * n};
   run_sort<uint64_t, 3, S1_BLOCK, S1_ITEMS, S1_MINB, 8>(c, {KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL}, n,
-                                                     shifts, bufK, bufP, Sort1FirstLoader{w, u, v}, em, ready);
+                                                     shifts, bufK, bufP, Sort1FirstLoader{w, u, v, code}, em, ready);
   if (nz) {
     c.begin(KK_OTHER);
     k_fix_negzero<<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(w, em.orig_of, em.heights, n);

@@ -31,15 +31,23 @@ __device__ __forceinline__ double key_to_double(uint64_t key) {
 // AND / OR of the keys of a strided sample (<= 65536 keys): predicts the
 // edge sort's first active digit so its upsweep can also do the full key
 // reduction (k_upsweep<KEYRED>).
+// Also the smallest top field (key >> 52: sign + exponent) of the sample,
+// the base of the upsweep's in-register top-field presence window.
 __global__ void __launch_bounds__(1024) k_key_sample(const double* __restrict__ w, int64_t n,
-                                                     unsigned long long* __restrict__ and_or) {
+                                                     unsigned long long* __restrict__ and_or,
+                                                     uint32_t* __restrict__ top_min) {
   const int64_t stride = n > 65536 ? n / 65536 : 1;
   uint64_t a = ~0ull, o = 0ull;
+  uint32_t tmin = 0xfffu;
+#pragma unroll 8
   for (int64_t i = (int64_t)threadIdx.x * stride; i < n; i += (int64_t)blockDim.x * stride) {
     const uint64_t k = desc_key(w[i]);
     a &= k;
     o |= k;
+    tmin = min(tmin, (uint32_t)(k >> 52));
   }
+  tmin = __reduce_min_sync(kFull, tmin);
+  if (lane_id() == 0) atomicMin(top_min, tmin);
   const uint32_t alo = __reduce_and_sync(kFull, (uint32_t)a), ahi = __reduce_and_sync(kFull, (uint32_t)(a >> 32));
   const uint32_t olo = __reduce_or_sync(kFull, (uint32_t)o), ohi = __reduce_or_sync(kFull, (uint32_t)(o >> 32));
   if (lane_id() == 0) {
@@ -85,24 +93,36 @@ __global__ void __launch_bounds__(256) k_key_reduce(const double* __restrict__ w
 
 // First pass: key from w; payload (original id, u, v) carried through the
 // sort so the final pass needs no random gathers.
+// Top-field compaction: when the keys hold few distinct top fields
+// (sign + exponent, key >> 52), `code` maps each present top field to its
+// order-preserving dense rank, so the radix passes over the (code, mantissa)
+// key skip the exponent's unused bits (tied or integral weights: 3 -> 2
+// passes); `inv` maps the codes back for the heights.
+constexpr int kTopShift = 52;
+constexpr uint64_t kMantMask = (1ull << kTopShift) - 1;
+__device__ __forceinline__ uint64_t compact_key(uint64_t k, const uint8_t* code) {
+  return code ? ((uint64_t)__ldg(code + (k >> kTopShift)) << kTopShift) | (k & kMantMask) : k;
+}
+
 struct Sort1FirstLoader {
   static constexpr int NS = 3;
   __host__ __device__ static constexpr int sb(int s) { return s == 0 ? 8 : 4; }
   const double* __restrict__ w;
   const int32_t* __restrict__ u;
   const int32_t* __restrict__ v;
+  const uint8_t* __restrict__ code;  // top-field compaction table or nullptr
   __device__ __forceinline__ const void* ptr(int s) const {
     return s == 0 ? (const void*)w : s == 1 ? (const void*)u : (const void*)v;
   }
-  __device__ __forceinline__ uint64_t key(int64_t i) const { return desc_key(ld_stream(w + i)); }
+  __device__ __forceinline__ uint64_t key(int64_t i) const { return compact_key(desc_key(ld_stream(w + i)), code); }
   __device__ __forceinline__ void load(int64_t i, uint64_t& k, Vals<3>& p) const {
-    k = desc_key(ld_stream(w + i));
+    k = compact_key(desc_key(ld_stream(w + i)), code);
     p.w[0] = (uint32_t)i;
     p.w[1] = (uint32_t)ld_stream(u + i);
     p.w[2] = (uint32_t)ld_stream(v + i);
   }
   __device__ __forceinline__ void get(char* const* st, int li, int64_t i, uint64_t& k, Vals<3>& p) const {
-    k = desc_key(reinterpret_cast<const double*>(st[0])[li]);
+    k = compact_key(desc_key(reinterpret_cast<const double*>(st[0])[li]), code);
     p.w[0] = (uint32_t)i;
     p.w[1] = reinterpret_cast<const uint32_t*>(st[1])[li];
     p.w[2] = reinterpret_cast<const uint32_t*>(st[2])[li];
@@ -122,6 +142,7 @@ struct Sort1FinalEmitter {
   int2* __restrict__ euv;        // rank-order endpoints (pipeline)
   int32_t* __restrict__ ru;      // optional split copies (dmst_rank_edges)
   int32_t* __restrict__ rv;
+  const uint16_t* __restrict__ inv;  // top-field compaction: code -> top field (or nullptr)
   template <int BLOCK, class Tile>
   __device__ __forceinline__ void emit(const Tile& t, State&) const {
     for (int s = threadIdx.x; s < t.cnt; s += BLOCK) {
@@ -129,7 +150,7 @@ struct Sort1FinalEmitter {
       const uint32_t r = t.gofs[digit_of<kRadixBits>(k, t.shift)] + (uint32_t)s;
       const uint32_t* p = t.spay + 3 * s;
       orig_of[r] = (int32_t)p[0];
-      heights[r] = key_to_double(k);
+      heights[r] = key_to_double(inv ? ((uint64_t)__ldg(inv + (k >> kTopShift)) << kTopShift) | (k & kMantMask) : k);
       if (euv) euv[r] = make_int2((int)p[1], (int)p[2]);
       if (ru) {
         ru[r] = (int32_t)p[1];
@@ -138,6 +159,30 @@ struct Sort1FinalEmitter {
     }
   }
 };
+
+// Compaction tables from the top-field presence bitmap (128 words, 4096
+// bits): code[t] = number of present top fields below t, inv[code] = t.
+// One block of 128 threads.
+__global__ void __launch_bounds__(128) k_top_codes(const uint32_t* __restrict__ bits, uint8_t* __restrict__ code,
+                                                   uint16_t* __restrict__ inv) {
+  __shared__ uint32_t wsum[4];
+  const uint32_t i = threadIdx.x, word = bits[i], pc = __popc(word);
+  uint32_t x = pc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, x, o);
+    if (lane_id() >= (uint32_t)o) x += y;
+  }
+  if (lane_id() == 31) wsum[i >> 5] = x;
+  __syncthreads();
+  uint32_t base = x - pc;
+  for (uint32_t q = 0; q < (i >> 5); ++q) base += wsum[q];
+  for (int j = 0; j < 32; ++j) {
+    const uint32_t c = base + __popc(word & ((1u << j) - 1u));
+    code[32 * i + j] = (uint8_t)c;
+    if ((word >> j) & 1u) inv[c] = (uint16_t)(32 * i + j);
+  }
+}
 
 // heights were decoded from canonicalised keys; restore -0.0 bit patterns.
 __global__ void k_fix_negzero(const double* __restrict__ w, const int32_t* __restrict__ orig_of,

@@ -214,17 +214,23 @@ struct KeyRed {
   const double* w;
   unsigned long long* and_or;
   uint32_t* negzero;
+  uint32_t* top_bits;  // presence bitmap of the top fields (key >> 52), 4096 bits
+  uint32_t top_base;   // base of the in-register 32-field window (the sample's smallest)
 };
 
 template <int BITS, class Loader, bool KEYRED = false>
 __global__ void __launch_bounds__(256) k_upsweep(SweepArgs a, Loader ld, KeyRed kr = KeyRed{}) {
   constexpr int R = 1 << BITS, BPT = R / 256;
   __shared__ uint32_t h[8][R];  // per-warp histograms
+  __shared__ uint32_t tbits[KEYRED ? 128 : 1];
   const uint32_t warp = threadIdx.x >> 5;
 #pragma unroll
   for (int w = 0; w < 8; ++w)
 #pragma unroll
     for (int q = 0; q < BPT; ++q) h[w][q * 256 + threadIdx.x] = 0;
+  if constexpr (KEYRED) {
+    if (threadIdx.x < 128) tbits[threadIdx.x] = 0;
+  }
   __syncthreads();
   const uint32_t chunk_id = blockIdx.x / kUpSplit, part = blockIdx.x % kUpSplit;
   const int64_t cbeg = (int64_t)chunk_id * a.chunk;
@@ -233,23 +239,43 @@ __global__ void __launch_bounds__(256) k_upsweep(SweepArgs a, Loader ld, KeyRed 
   const int64_t end = min(min(a.n, cbeg + a.chunk), begin + plen);
   constexpr int U = 8;
   uint64_t ka = ~0ull, ko = 0ull;
+  uint32_t tw = 0;
   bool nz = false;
   for (int64_t i0 = begin; i0 < end; i0 += 256 * U) {
     uint32_t d[U];
     bool ok[U];
+    double x[U];
+    if constexpr (KEYRED) {
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int64_t i = i0 + q * 256 + threadIdx.x;
+        x[q] = i < end ? ld_stream(kr.w + i) : kr.w[begin];
+      }
+    }
+    uint32_t far = 0, tq[U];
 #pragma unroll
     for (int q = 0; q < U; ++q) {
       const int64_t i = i0 + q * 256 + threadIdx.x;
       ok[q] = i < end;
       if constexpr (KEYRED) {
-        const double x = ok[q] ? ld_stream(kr.w + i) : kr.w[begin];
-        const uint64_t k = desc_key_of(x);
-        nz |= (uint64_t)__double_as_longlong(x) == 0x8000000000000000ull;
+        const uint64_t k = desc_key_of(x[q]);
+        nz |= (uint64_t)__double_as_longlong(x[q]) == 0x8000000000000000ull;
         ka &= k;
         ko |= k;
+        tq[q] = (uint32_t)(k >> 52);
+        const uint32_t dt = tq[q] - kr.top_base;
+        tw |= dt < 32 ? 1u << dt : 0u;
+        far |= dt < 32 ? 0u : 1u << q;
         d[q] = digit_of<BITS>(k, a.shift);
       } else {
         d[q] = ok[q] ? digit_of<BITS>(ld.key(i), a.shift) : 0u;
+      }
+    }
+    if constexpr (KEYRED) {
+      if (far) {  // top fields outside the window (rare): straight to the bitmap
+#pragma unroll
+        for (int q = 0; q < U; ++q)
+          if ((far >> q) & 1u) atomicOr(&tbits[tq[q] >> 5], 1u << (tq[q] & 31));
       }
     }
 #pragma unroll
@@ -272,8 +298,17 @@ __global__ void __launch_bounds__(256) k_upsweep(SweepArgs a, Loader ld, KeyRed 
       atomicOr(kr.and_or + 1, ((unsigned long long)ohi << 32) | olo);
       if (anz) atomicOr(kr.negzero, 1u);
     }
+    tw = __reduce_or_sync(kFull, tw);
+    if (lane_id() == 0 && tw) {  // window bits base.. base+31 -> two aligned words
+      const uint32_t wb = kr.top_base >> 5, sh = kr.top_base & 31;
+      atomicOr(&tbits[wb], tw << sh);
+      if (sh && wb + 1 < 128) atomicOr(&tbits[wb + 1], tw >> (32 - sh));
+    }
   }
   __syncthreads();
+  if constexpr (KEYRED) {
+    if (threadIdx.x < 128 && tbits[threadIdx.x]) atomicOr(kr.top_bits + threadIdx.x, tbits[threadIdx.x]);
+  }
 #pragma unroll
   for (int q = 0; q < BPT; ++q) {
     const uint32_t b = q * 256 + threadIdx.x;

@@ -91,6 +91,40 @@ def test_heavy_ties_negative_and_signed_zero(builder):
         assert_matches(res, exp.orig_of, exp.heights, exp.edge_parent, exp.vertex_parent)
 
 
+def _compaction_weights(kind, n, rng):
+    """Weight sets that exercise the edge sort's top-field compaction (few
+    distinct sign + exponent fields): rare outliers the key sample misses,
+    both signs, signed zeros, subnormals, and more fields than a code holds."""
+    if kind == "int4096":                      # config 4's weights
+        return rng.integers(0, 4096, n).astype(np.float64)
+    if kind == "rare_outliers":                # [1, 2) plus a handful far away
+        w = 1.0 + rng.random(n)
+        idx = rng.choice(n, 5, replace=False)
+        w[idx] = [1e-200, -1e300, 5e-324, -0.0, 3e250]
+        return w
+    if kind == "signed_scaled":                # +-k * 2^e over 6 exponents
+        return rng.choice([-1.0, 1.0], n) * rng.integers(1, 64, n) * np.exp2(rng.integers(-3, 3, n))
+    if kind == "many_fields":                  # > 256 exponents: no compaction
+        return np.exp2(rng.integers(-400, 400, n).astype(np.float64)) * (1 + rng.integers(0, 8, n) / 8)
+    if kind == "one_field":                    # all in [1, 2): nothing to compact
+        return 1.0 + rng.integers(0, 1 << 20, n) / float(1 << 20)
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("kind", ["int4096", "rare_outliers", "signed_scaled", "many_fields", "one_field"])
+@pytest.mark.parametrize("n", [1000, 600_000])
+def test_sort_key_compaction_vs_oracle(builder, kind, n):
+    rng = np.random.default_rng(n + len(kind))
+    nv, u, v, _ = synth.random_attach(n, seed=11)
+    w = _compaction_weights(kind, n, rng)
+    exp = O.build(nv, u, v, w)
+    res = builder.build(nv, u, v, w)
+    assert_matches(res, exp.orig_of, exp.heights, exp.edge_parent, exp.vertex_parent)
+    orig_of, heights, _, _ = builder.rank_edges(nv, u, v, w)
+    assert np.array_equal(_np(orig_of), exp.orig_of)
+    assert np.array_equal(_np(heights).view(np.uint64), np.asarray(exp.heights).view(np.uint64))
+
+
 def test_reversed_path_orientation(builder):
     # deep in-trees pointing to HIGHER vertex ids (the pointer-jumping worst case)
     n = 200_000

@@ -490,11 +490,33 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
   const int ready = !shifts.empty() && shifts[0] == d0 && (!code || d0 + 8 <= kTopShift) ? d0 : -1;
   if (passes_out) *passes_out = (int)shifts.size();
   char* R = c.w.R;
-  uint64_t* const bufK[2] = {(uint64_t*)R, (uint64_t*)(R + 8 * n)};
   uint32_t* vb = (uint32_t*)(R + 16 * n);
   uint32_t* const bufP[2] = {vb, vb + 3 * n};
-  run_sort<uint64_t, 3, S1_BLOCK, S1_ITEMS, S1_MINB, 8>(c, {KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL}, n,
-                                                     shifts, bufK, bufP, Sort1FirstLoader{w, u, v, code}, em, ready);
+  // narrow keys: every varying bit of the (compacted) key within 32 bits
+  // from lo (= the first digit, so the fused upsweep's counts stay valid)
+  const uint64_t kand = code ? ao[0] & kMantMask : ao[0];
+  const uint64_t kvar = code ? (ao[0] ^ ao[1]) & kMantMask : ao[0] ^ ao[1];
+  const uint64_t cvar = code ? ((1ull << ([&] { int b = 0; while ((1 << b) < ncodes) ++b; return b; })()) - 1) << kTopShift
+                             : 0ull;
+  const uint64_t var = kvar | cvar;
+  const int lo = shifts.empty() ? 0 : shifts[0];
+  const bool narrow = !shifts.empty() && (var >> lo) < (1ull << 32);
+  if (narrow) {
+    std::vector<int> s32(shifts);
+    for (int& x : s32) x -= lo;
+    uint32_t* const bufK[2] = {(uint32_t*)R, (uint32_t*)(R + 8 * n)};
+    Sort1Emitter<uint32_t> em32{em.orig_of, em.heights, em.euv, em.ru, em.rv, em.inv,
+                                lo ? kand & ((1ull << lo) - 1) : 0ull, (uint32_t)lo};
+    em32.base |= lo + 32 < 64 ? kand & ~((1ull << (lo + 32)) - 1) : 0ull;
+    run_sort<uint32_t, 3, S1_BLOCK, S1_ITEMS, S1_MINB, 8>(
+        c, {KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL}, n, s32, bufK, bufP,
+        Sort1Loader<uint32_t>{w, u, v, code, (uint32_t)lo}, em32, ready >= 0 ? 0 : -1);
+  } else {
+    uint64_t* const bufK[2] = {(uint64_t*)R, (uint64_t*)(R + 8 * n)};
+    run_sort<uint64_t, 3, S1_BLOCK, S1_ITEMS, S1_MINB, 8>(c, {KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL}, n,
+                                                       shifts, bufK, bufP, Sort1FirstLoader{w, u, v, code}, em,
+                                                       ready);
+  }
   if (nz) {
     c.begin(KK_OTHER);
     k_fix_negzero<<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(w, em.orig_of, em.heights, n);

@@ -104,34 +104,43 @@ __device__ __forceinline__ uint64_t compact_key(uint64_t k, const uint8_t* code)
   return code ? ((uint64_t)__ldg(code + (k >> kTopShift)) << kTopShift) | (k & kMantMask) : k;
 }
 
-struct Sort1FirstLoader {
+// K = uint64_t: the (compacted) 64-bit key.  K = uint32_t ("narrow keys"):
+// when every varying key bit lies in [lo, lo + 32), the passes carry only
+// those 32 bits (4 B less per item each way); the final pass restores the
+// constant bits from the AND of all keys.
+template <typename K>
+struct Sort1Loader {
   static constexpr int NS = 3;
   __host__ __device__ static constexpr int sb(int s) { return s == 0 ? 8 : 4; }
   const double* __restrict__ w;
   const int32_t* __restrict__ u;
   const int32_t* __restrict__ v;
   const uint8_t* __restrict__ code;  // top-field compaction table or nullptr
+  uint32_t lo;                       // narrow keys: lowest carried bit
   __device__ __forceinline__ const void* ptr(int s) const {
     return s == 0 ? (const void*)w : s == 1 ? (const void*)u : (const void*)v;
   }
-  __device__ __forceinline__ uint64_t key(int64_t i) const { return compact_key(desc_key(ld_stream(w + i)), code); }
-  __device__ __forceinline__ void load(int64_t i, uint64_t& k, Vals<3>& p) const {
-    k = compact_key(desc_key(ld_stream(w + i)), code);
+  __device__ __forceinline__ K make(double x) const { return (K)(compact_key(desc_key(x), code) >> lo); }
+  __device__ __forceinline__ K key(int64_t i) const { return make(ld_stream(w + i)); }
+  __device__ __forceinline__ void load(int64_t i, K& k, Vals<3>& p) const {
+    k = make(ld_stream(w + i));
     p.w[0] = (uint32_t)i;
     p.w[1] = (uint32_t)ld_stream(u + i);
     p.w[2] = (uint32_t)ld_stream(v + i);
   }
-  __device__ __forceinline__ void get(char* const* st, int li, int64_t i, uint64_t& k, Vals<3>& p) const {
-    k = compact_key(desc_key(reinterpret_cast<const double*>(st[0])[li]), code);
+  __device__ __forceinline__ void get(char* const* st, int li, int64_t i, K& k, Vals<3>& p) const {
+    k = make(reinterpret_cast<const double*>(st[0])[li]);
     p.w[0] = (uint32_t)i;
     p.w[1] = reinterpret_cast<const uint32_t*>(st[1])[li];
     p.w[2] = reinterpret_cast<const uint32_t*>(st[2])[li];
   }
 };
+using Sort1FirstLoader = Sort1Loader<uint64_t>;
 
 // Final pass: RankedTree outputs (orig_of, w by rank) + rank-order endpoints,
 // written from the sorted sub-tile (payload = (original id, u, v)).
-struct Sort1FinalEmitter {
+template <typename K>
+struct Sort1Emitter {
   using State = NoEmitState;
   template <int BLOCK, int R>
   __device__ __forceinline__ void init(State&) const {}
@@ -143,12 +152,15 @@ struct Sort1FinalEmitter {
   int32_t* __restrict__ ru;      // optional split copies (dmst_rank_edges)
   int32_t* __restrict__ rv;
   const uint16_t* __restrict__ inv;  // top-field compaction: code -> top field (or nullptr)
+  uint64_t base;                     // narrow keys: the constant bits outside [lo, lo + 32)
+  uint32_t lo;
   template <int BLOCK, class Tile>
   __device__ __forceinline__ void emit(const Tile& t, State&) const {
     for (int s = threadIdx.x; s < t.cnt; s += BLOCK) {
-      const uint64_t k = t.skeys[s];
-      const uint32_t r = t.gofs[digit_of<kRadixBits>(k, t.shift)] + (uint32_t)s;
+      const K kn = t.skeys[s];
+      const uint32_t r = t.gofs[digit_of<kRadixBits>(kn, t.shift)] + (uint32_t)s;
       const uint32_t* p = t.spay + 3 * s;
+      const uint64_t k = base | ((uint64_t)kn << lo);
       orig_of[r] = (int32_t)p[0];
       heights[r] = key_to_double(inv ? ((uint64_t)__ldg(inv + (k >> kTopShift)) << kTopShift) | (k & kMantMask) : k);
       if (euv) euv[r] = make_int2((int)p[1], (int)p[2]);
@@ -159,6 +171,7 @@ struct Sort1FinalEmitter {
     }
   }
 };
+using Sort1FinalEmitter = Sort1Emitter<uint64_t>;
 
 // Compaction tables from the top-field presence bitmap (128 words, 4096
 // bits): code[t] = number of present top fields below t, inv[code] = t.

@@ -133,3 +133,29 @@ def test_device_read_roundtrip_and_errors():
         _write(path, data[: data.rfind(b"\nV ") + 1])
         with pytest.raises(err, match=f"expected {nv - 1} edge and {nv} vertex lines, got {nv - 1} and {nv - 1}"):
             read_dendrogram_b200(path)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+def test_device_sidecar_roundtrip():
+    from paper_2401_06089_b200 import DendrogramBuilder, read_dendrogram_b200, write_dendrogram_b200
+    from paper_2401_06089_b200.api import sidecar_path
+    nv, u, v, w = synth.GENERATORS["random"](200_000, seed=5)
+    r = DendrogramBuilder("cuda:0").build(nv, u, v, w)
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "x.dendro")
+        write_dendrogram_b200(path, r.edge_parent, r.vertex_parent, sidecar=True)
+        side = np.load(sidecar_path(path))
+        assert side.dtype == np.int32 and side.shape == (2 * nv - 1,)
+        for use in (True, False):
+            back = read_dendrogram_b200(path, use_sidecar=use)
+            assert bool((back.edge_parent == r.edge_parent).all())
+            assert bool((back.vertex_parent == r.vertex_parent).all())
+        # a text file newer than its sidecar is parsed, not shadowed
+        data = open(path, "rb").read()
+        i = data.index(b"\nE 5 ") + 1
+        j = data.index(b"\n", i)
+        _write(path, data[:i] + b"E 5 -1" + data[j:])
+        os.utime(sidecar_path(path), (1, 1))
+        back = read_dendrogram_b200(path)
+        assert int(back.edge_parent[5]) == -1

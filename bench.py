@@ -440,7 +440,7 @@ def run_b200(args) -> None:
         torch.cuda.synchronize(dev)
         return f0.elapsed_time(f1) / n_steps
 
-    e2e_steps = max(2, min(args.steps, 6))
+    e2e_steps = max(2, args.e2e_steps)
     e2e_run(depth, depth)  # warm-up
     e2e_ms = e2e_run(e2e_steps, depth)
     e2e_serial_ms = e2e_run(max(1, e2e_steps // 2), 1) if depth > 1 else e2e_ms
@@ -527,7 +527,7 @@ def run_b200(args) -> None:
             "e2e": {"value": edges_total / (e2e_ms * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
                     "api": "DendrogramBuilder.build_host -> dmst_build_host (pinned host buffers)",
-                    "builds_in_flight": depth,
+                    "builds_in_flight": depth, "builds_timed": e2e_steps,
                     "serial": {"value": edges_total / (e2e_serial_ms * 1e-3), "ms_per_step": e2e_serial_ms,
                                "builds_in_flight": 1}},
             "roofline": roof,
@@ -565,6 +565,8 @@ def main() -> None:
     ap.add_argument("--ref-sample", type=int, default=2_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-depth", type=int, default=2, help="builds in flight in the e2e leg")
+    ap.add_argument("--e2e-steps", type=int, default=12,
+                    help="builds timed in the e2e leg (a stream of builds: pipeline fill and drain included)")
     args = ap.parse_args()
     if args.warmup < 0 or args.steps < 1:
         raise SystemExit("bad steps/warmup")

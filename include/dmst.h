@@ -187,6 +187,21 @@ int dmst_parse_dendrogram(const char* body, int64_t body_len, int64_t n_edges, i
 int dmst_first_difference(const int32_t* a, const int32_t* b, int64_t n, int64_t* first, void* workspace,
                           size_t workspace_bytes, void* stream);
 
+/* Upstream producer: replaces
+ * dendromst.pointgen.mutual_reachability_mst (pointgen.py:158-178) with
+ * core_distances (:56-61) and the dense Prim scans (:71-148).
+ * coords: DEVICE float64 [n_points][dim] (row-major, 1 <= dim <= 8);
+ * min_pts in [1, min(n_points, 16)]; engine 0 = "auto" (numba scan order for
+ * n_points >= 4096, else numpy), 1 = "numba", 2 = "numpy" -- the engines
+ * break ties differently and are reproduced bit-exactly.  Outputs (DEVICE,
+ * n_points - 1 entries, Prim discovery order = original edge id): u, v,
+ * w = sqrt(w_sq); core_sq (nullable, n_points) = core_distances ** 2.
+ * Workspace: dmst_mreach_workspace_bytes(n_points, dim). */
+size_t dmst_mreach_workspace_bytes(int64_t n_points, int32_t dim);
+int dmst_mreach_mst(const double* coords, int64_t n_points, int32_t dim, int32_t min_pts, int32_t engine,
+                    int32_t* u, int32_t* v, double* w, double* core_sq, void* workspace, size_t workspace_bytes,
+                    void* stream);
+
 /* Message for the last non-zero return on this thread ("" if none). */
 const char* dmst_last_error(void);
 

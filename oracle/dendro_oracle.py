@@ -412,3 +412,97 @@ def verify_text(a: bytes, b: bytes) -> tuple[int, str]:
             i = int(diff[0])
             return 1, f"first divergence: {label} {i}: {int(pa[i])} != {int(pb[i])}"
     return 0, "identical"
+
+
+# ---------------------------------------------------------------- upstream producer
+# Mutual-reachability MST, restating
+# /root/reference/pkg/src/dendromst/pointgen.py:56-178 for small clouds.
+
+def _kdtree_sqdist(diff: np.ndarray) -> np.ndarray:
+    """Squared distances in scipy cKDTree's p = 2 summation order (checked
+    bitwise against cKDTree.query): four strided accumulators over the full
+    blocks of 4 dimensions, combined left to right, then the rest."""
+    q = diff * diff
+    dim = q.shape[-1]
+    acc = [np.zeros(q.shape[:-1]) for _ in range(4)]
+    full = dim // 4 * 4
+    for i in range(0, full, 4):
+        for j in range(4):
+            acc[j] = acc[j] + q[..., i + j]
+    s = ((acc[0] + acc[1]) + acc[2]) + acc[3]
+    for i in range(full, dim):
+        s = s + q[..., i]
+    return s
+
+
+def core_sq(coords: np.ndarray, min_pts: int) -> np.ndarray:
+    """core_distances(coords, min_pts) ** 2 (pointgen.py:56-61): the
+    min_pts-th smallest distance (self included), by brute force."""
+    x = np.asarray(coords, np.float64)
+    out = np.empty(x.shape[0])
+    for lo in range(0, x.shape[0], 512):
+        d = _kdtree_sqdist(x[lo:lo + 512, None, :] - x[None, :, :])
+        kth = np.partition(d, min_pts - 1, axis=1)[:, min_pts - 1]
+        out[lo:lo + 512] = np.sqrt(kth) ** 2
+    return out
+
+
+def _prim_sqdist(x: np.ndarray, c: np.ndarray, numpy_engine: bool) -> np.ndarray:
+    q = (x - c) ** 2
+    dim = q.shape[1]
+    if numpy_engine and dim == 8:   # numpy's pairwise row sum at 8 columns
+        return ((q[:, 0] + q[:, 1]) + (q[:, 2] + q[:, 3])) + ((q[:, 4] + q[:, 5]) + (q[:, 6] + q[:, 7]))
+    s = q[:, 0] if numpy_engine else 0.0 + q[:, 0]
+    for t in range(1, dim):
+        s = s + q[:, t]
+    return s
+
+
+def prim_mst(coords: np.ndarray, core_sq_: np.ndarray, engine: str = "auto"):
+    """Dense Prim (pointgen.py:71-148): (u, v, w_sq) in discovery order.
+    numba engine (:91-148): compacted arrays, swap-with-last removal, first
+    minimum in compacted order; numpy engine (:71-88): first minimum by
+    point id.  Both update with strict `<`."""
+    x = np.asarray(coords, np.float64)
+    n = x.shape[0]
+    if engine == "auto":
+        engine = "numba" if n >= 4096 else "numpy"
+    numpy_engine = engine == "numpy"
+    idx = np.arange(1, n, dtype=np.int64)
+    acoord = x[1:].copy()
+    acore = np.asarray(core_sq_, np.float64)[1:].copy()
+    abest = np.full(n - 1, np.inf)
+    afrom = np.zeros(n - 1, np.int64)
+    out_u = np.empty(n - 1, np.int64)
+    out_v = np.empty(n - 1, np.int64)
+    out_w = np.empty(n - 1)
+    cur = 0
+    m = n - 1
+    for it in range(n - 1):
+        d = _prim_sqdist(acoord[:m], x[cur], numpy_engine)
+        d = np.where(acore[:m] > d, acore[:m], d)
+        cc = core_sq_[cur]
+        d = np.where(cc > d, cc, d)
+        upd = d < abest[:m]
+        abest[:m][upd] = d[upd]
+        afrom[:m][upd] = cur
+        if numpy_engine:
+            mn = abest[:m].min()
+            cand = np.nonzero(abest[:m] == mn)[0]
+            bk = int(cand[np.argmin(idx[cand])])
+        else:
+            bk = int(np.argmin(abest[:m]))
+        cur = int(idx[bk])
+        out_u[it], out_v[it], out_w[it] = afrom[bk], cur, abest[bk]
+        m -= 1
+        for arr in (idx, acore, abest, afrom):
+            arr[bk] = arr[m]
+        acoord[bk] = acoord[m]
+    return out_u, out_v, out_w
+
+
+def mutual_reachability_mst(coords: np.ndarray, min_pts: int = 2, engine: str = "auto"):
+    """(num_vertices, u, v, w) of mutual_reachability_mst (pointgen.py:158-178)."""
+    x = np.asarray(coords, np.float64)
+    u, v, w_sq = prim_mst(x, core_sq(x, min_pts), engine)
+    return x.shape[0], u, v, np.sqrt(w_sq)

@@ -32,6 +32,8 @@ EXPORTS = (
     "dmst_format_dendrogram",
     "dmst_parse_dendrogram",
     "dmst_first_difference",
+    "dmst_mreach_workspace_bytes",
+    "dmst_mreach_mst",
     "dmst_last_error",
     "dmst_kernel_name",
     "dmst_version",
@@ -115,6 +117,11 @@ def load() -> ctypes.CDLL:
     lib.dmst_parse_dendrogram.restype = ctypes.c_int
     lib.dmst_first_difference.argtypes = [vp, vp, i64, p64, vp, sz, vp]
     lib.dmst_first_difference.restype = ctypes.c_int
+    lib.dmst_mreach_workspace_bytes.argtypes = [i64, ctypes.c_int32]
+    lib.dmst_mreach_workspace_bytes.restype = sz
+    i32 = ctypes.c_int32
+    lib.dmst_mreach_mst.argtypes = [vp, i64, i32, i32, i32, vp, vp, vp, vp, vp, sz, vp]
+    lib.dmst_mreach_mst.restype = ctypes.c_int
     lib.dmst_last_error.argtypes = []
     lib.dmst_last_error.restype = ctypes.c_char_p
     lib.dmst_kernel_name.argtypes = [ctypes.c_int32]

@@ -603,6 +603,43 @@ def verify_b200(path_a, path_b, device=None) -> tuple[int, str]:
     return 0, "identical"
 
 
+_ENGINES = {"auto": 0, "numba": 1, "numpy": 2}
+
+
+def mutual_reachability_mst_b200(coords, min_pts: int = 2, engine: str = "auto", device=None,
+                                 return_core_sq: bool = False):
+    """Drop-in for ``mutual_reachability_mst`` (pointgen.py:158-178) on the
+    GPU: core distances by brute-force k-NN in cKDTree's summation order,
+    then the dense Prim scan of the chosen engine (same tie-breaking, same
+    discovery order = original edge ids).  ``coords``: (n, dim) float64
+    array or tensor, dim <= 8, min_pts <= 16 on the device.  Returns a
+    WeightedTree whose u, v (int32) and w (float64) are DEVICE tensors, the
+    input of DendrogramBuilder.build (+ core_sq with return_core_sq)."""
+    x = torch.as_tensor(coords)
+    if x.dim() != 2:
+        raise ValueError("coords must be (n, dim)")
+    n, dim = int(x.shape[0]), int(x.shape[1])
+    if not 2 <= min_pts <= n:
+        raise ValueError(f"min_pts must be in [2, {n}]")
+    if engine not in _ENGINES:
+        raise ValueError(f"unknown engine {engine!r}")
+    if min_pts > 16 or not 1 <= dim <= 8:
+        raise ValueError("the device producer supports min_pts <= 16 and 1 <= dim <= 8")
+    b = _builder(device)
+    dev = b.device
+    with torch.cuda.device(dev):
+        x = x.to(dev, torch.float64).contiguous()
+        u = torch.empty(n - 1, dtype=torch.int32, device=dev)
+        v = torch.empty(n - 1, dtype=torch.int32, device=dev)
+        w = torch.empty(n - 1, dtype=torch.float64, device=dev)
+        core = torch.empty(n, dtype=torch.float64, device=dev)
+        ws = torch.empty(int(b.lib.dmst_mreach_workspace_bytes(n, dim)), dtype=torch.uint8, device=dev)
+        _lib.check(b.lib.dmst_mreach_mst(_ptr(x), n, dim, int(min_pts), _ENGINES[engine], _ptr(u), _ptr(v), _ptr(w),
+                                         _ptr(core), _ptr(ws), ws.numel(), b._stream()))
+    tree = WeightedTree(n, u, v, w, torch.arange(n - 1, device=dev))
+    return (tree, core) if return_core_sq else tree
+
+
 def build_b200(num_vertices: int, u, v, w, device=None, debug: bool = False) -> BuildResult:
     """rank_edges + pandora on the GPU (the timed scope of `dendromst build`)."""
     return _builder(device).build(num_vertices, u, v, w, debug=debug)

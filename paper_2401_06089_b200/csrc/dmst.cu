@@ -33,6 +33,7 @@
 #include "kernels.cuh"
 #include "validate.cuh"
 #include "tail.cuh"
+#include "emst.cuh"
 
 namespace dmst {
 
@@ -971,6 +972,61 @@ HostBufs host_bufs(int64_t n, int64_t nv, char* base) {
   return b;
 }
 
+
+// ------------------------------------------------ mutual-reachability MST
+// (pointgen.py:56-178)
+size_t mreach_ws_bytes(int64_t n, int dim) {
+  const int64_t cap = n;
+  return align_up(8 * (size_t)n)                     // core_sq
+         + align_up(8 * (size_t)dim * cap)           // acoord
+         + 2 * align_up(8 * (size_t)cap)             // acore, abest
+         + 2 * align_up(4 * (size_t)cap)             // afrom, idx
+         + align_up(sizeof(PrimSlot) * 2 * 4096) + 512;
+}
+
+template <int DIM>
+void mreach_impl(Ctx& c, const double* pts, int64_t n, int k, int engine, int32_t* u, int32_t* v, double* w,
+                 double* core_sq_out, char* ws) {
+  char* p = (char*)(((uintptr_t)ws + 255) & ~uintptr_t(255));
+  double* core_sq = (double*)p;
+  p += align_up(8 * (size_t)n);
+  PrimState st{};
+  st.cap = n;
+  st.acoord = (double*)p;
+  p += align_up(8 * (size_t)DIM * n);
+  st.acore = (double*)p;
+  p += align_up(8 * (size_t)n);
+  st.abest = (double*)p;
+  p += align_up(8 * (size_t)n);
+  st.afrom = (int32_t*)p;
+  p += align_up(4 * (size_t)n);
+  st.idx = (int32_t*)p;
+  p += align_up(4 * (size_t)n);
+  PrimSlot* slots = (PrimSlot*)p;
+  c.begin(KK_OTHER);
+  k_core_sq<DIM><<<grid_for(n, KNN_BLOCK), KNN_BLOCK, 0, c.s>>>(pts, n, k, core_sq);
+  c.launched();
+  if (core_sq_out)
+    DMST_CUDA(cudaMemcpyAsync(core_sq_out, core_sq, 8 * (size_t)n, cudaMemcpyDeviceToDevice, c.s));
+  if (n < 2) return;
+  c.begin(KK_OTHER);
+  k_prim_init<DIM><<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(pts, core_sq, n, st);
+  c.launched();
+  const bool numpy = engine == 2 || (engine == 0 && n < 4096);  // "auto" (pointgen.py:170-171)
+  const void* kern = numpy ? (const void*)k_prim<DIM, true> : (const void*)k_prim<DIM, false>;
+  int per_sm = 0;
+  DMST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PRIM_BLOCK, 0));
+  if (per_sm < 1) invalid("k_prim cannot be co-resident");
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>({cdiv(n - 1, PRIM_BLOCK), (int64_t)c.sms * per_sm, 4096}));
+  PrimArgs a{pts, core_sq, n, st, slots, u, v, w};
+  void* args[] = {&a};
+  c.begin(KK_OTHER);
+  DMST_CUDA(cudaLaunchCooperativeKernel(kern, dim3((unsigned)grid), dim3(PRIM_BLOCK), args, 0, c.s));
+  c.launched();
+  c.begin(KK_OTHER);
+  k_sqrt_inplace<<<grid_for(n - 1, EW_BLOCK), EW_BLOCK, 0, c.s>>>(w, n - 1);
+  c.launched();
+}
 }  // namespace
 }  // namespace dmst
 
@@ -1328,6 +1384,35 @@ int dmst_first_difference(const int32_t* a, const int32_t* b, int64_t n, int64_t
     c.to_host(&h, f, 8);
     c.sync();
     *first = h == ~0ull ? -1 : (int64_t)h;
+  });
+}
+
+size_t dmst_mreach_workspace_bytes(int64_t n_points, int32_t dim) {
+  return n_points < 1 || dim < 1 ? 0 : mreach_ws_bytes(n_points, dim);
+}
+
+int dmst_mreach_mst(const double* coords, int64_t n_points, int32_t dim, int32_t min_pts, int32_t engine,
+                    int32_t* u, int32_t* v, double* w, double* core_sq, void* workspace, size_t workspace_bytes,
+                    void* stream) {
+  return guarded([&] {
+    const int64_t n = n_points;
+    if (n < 2 || n > INT32_MAX) invalid("need 2 <= n_points < 2^31");
+    if (dim < 1 || dim > EMST_MAX_DIM) invalid("dim must be in [1, 8]");
+    if (min_pts < 1 || min_pts > n || min_pts > KNN_MAX_K) invalid("min_pts must be in [1, min(n, 16)]");
+    if (engine < 0 || engine > 2) invalid("engine must be 0 (auto), 1 (numba) or 2 (numpy)");
+    if (!coords || !u || !v || !w || !workspace) invalid("null pointer");
+    if (workspace_bytes < mreach_ws_bytes(n, dim)) invalid("workspace too small");
+    Ctx c;
+    c.s = (cudaStream_t)stream;
+    c.sms = num_sms();
+    switch (dim) {
+#define DMST_DIM(D) \
+  case D:           \
+    mreach_impl<D>(c, coords, n, min_pts, engine, u, v, w, core_sq, (char*)workspace); \
+    break;
+      DMST_DIM(1) DMST_DIM(2) DMST_DIM(3) DMST_DIM(4) DMST_DIM(5) DMST_DIM(6) DMST_DIM(7) DMST_DIM(8)
+#undef DMST_DIM
+    }
   });
 }
 

@@ -981,7 +981,7 @@ size_t mreach_ws_bytes(int64_t n, int dim) {
          + align_up(8 * (size_t)dim * cap)           // acoord
          + 2 * align_up(8 * (size_t)cap)             // acore, abest
          + 2 * align_up(4 * (size_t)cap)             // afrom, idx
-         + align_up(sizeof(PrimSlot) * 2 * 4096) + 512;
+         + align_up(sizeof(PrimSlot) * 2 * (PRIM_MAX_GRID + 1)) + 1024;
 }
 
 template <int DIM>
@@ -1003,6 +1003,9 @@ void mreach_impl(Ctx& c, const double* pts, int64_t n, int k, int engine, int32_
   st.idx = (int32_t*)p;
   p += align_up(4 * (size_t)n);
   PrimSlot* slots = (PrimSlot*)p;
+  p += align_up(sizeof(PrimSlot) * 2 * (PRIM_MAX_GRID + 1));
+  unsigned long long* bar = (unsigned long long*)p;
+  c.zero(bar, 8);
   c.begin(KK_OTHER);
   k_core_sq<DIM><<<grid_for(n, KNN_BLOCK), KNN_BLOCK, 0, c.s>>>(pts, n, k, core_sq);
   c.launched();
@@ -1017,8 +1020,12 @@ void mreach_impl(Ctx& c, const double* pts, int64_t n, int k, int engine, int32_
   int per_sm = 0;
   DMST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PRIM_BLOCK, 0));
   if (per_sm < 1) invalid("k_prim cannot be co-resident");
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>({cdiv(n - 1, PRIM_BLOCK), (int64_t)c.sms * per_sm, 4096}));
-  PrimArgs a{pts, core_sq, n, st, slots, u, v, w};
+  // one slot per thread in the post-barrier reduction: grid <= PRIM_BLOCK
+  int64_t grid = std::max<int64_t>(
+      1, std::min<int64_t>({cdiv(n - 1, 2 * PRIM_BLOCK), (int64_t)c.sms * per_sm, (int64_t)PRIM_MAX_GRID}));
+  if (const char* e = getenv("DMST_PRIM_GRID"))
+    grid = std::max<int64_t>(1, std::min<int64_t>({atoll(e), (int64_t)c.sms * per_sm, (int64_t)PRIM_MAX_GRID}));
+  PrimArgs a{pts, core_sq, n, st, slots, bar, u, v, w};
   void* args[] = {&a};
   c.begin(KK_OTHER);
   DMST_CUDA(cudaLaunchCooperativeKernel(kern, dim3((unsigned)grid), dim3(PRIM_BLOCK), args, 0, c.s));

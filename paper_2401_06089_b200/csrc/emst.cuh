@@ -121,13 +121,30 @@ struct PrimState {
   int64_t cap;
 };
 
-struct PrimSlot {  // one block's candidate of one step
+struct PrimSlot {  // one block's candidate of one step (+ the candidate point, so the
+                   // next step needs no dependent load of its coordinates)
   double bv;
   int32_t key;    // tie-break key: compacted position (numba) or point id (numpy)
   int32_t k;      // compacted position
   int32_t id;     // point id
   int32_t from;
+  double core;
+  double x[EMST_MAX_DIM];
 };
+
+// slots are rewritten every other step by other SMs: read them from L2
+__device__ __forceinline__ PrimSlot ldcg_slot(const PrimSlot* p) {
+  PrimSlot s;
+  s.bv = __ldcg(&p->bv);
+  s.key = __ldcg(&p->key);
+  s.k = __ldcg(&p->k);
+  s.id = __ldcg(&p->id);
+  s.from = __ldcg(&p->from);
+  s.core = __ldcg(&p->core);
+#pragma unroll
+  for (int t = 0; t < EMST_MAX_DIM; ++t) s.x[t] = __ldcg(&p->x[t]);
+  return s;
+}
 
 __device__ __forceinline__ bool slot_less(double b, int32_t key, double bv, int32_t bkey) {
   return b < bv || (b == bv && key < bkey);
@@ -146,134 +163,237 @@ __global__ void k_prim_init(const double* __restrict__ pts, const double* __rest
   st.idx[k] = (int32_t)(k + 1);
 }
 
-constexpr int PRIM_BLOCK = 512;
+constexpr int PRIM_BLOCK = 512, PRIM_U = 4, PRIM_MAX_GRID = 296;
 struct PrimArgs {
   const double* pts;
   const double* core_sq;
   int64_t n;
   PrimState st;
-  PrimSlot* slots;  // [2][gridDim.x]
+  PrimSlot* slots;          // [2][gridDim.x + 1]: block candidates, then the last element
+  unsigned long long* bar;  // grid barrier counter (zeroed before the launch)
   int32_t* out_u;
   int32_t* out_v;
-  double* out_w;    // w_sq until the final sqrt
+  double* out_w;            // w_sq until the final sqrt
 };
 
+template <int DIM>
+struct PrimCand {
+  double bv, core;
+  int32_t key, k, id, from;
+  double x[DIM];
+  __device__ __forceinline__ void reset() {
+    bv = __longlong_as_double(0x7ff0000000000000ll);
+    key = 0x7fffffff;
+    k = -1;
+    id = from = 0;
+    core = 0.0;
+#pragma unroll
+    for (int t = 0; t < DIM; ++t) x[t] = 0.0;
+  }
+  __device__ __forceinline__ void take(const PrimCand& q) {
+    if (slot_less(q.bv, q.key, bv, key)) *this = q;
+  }
+  __device__ __forceinline__ void warp_min() {  // butterfly: every lane ends with the minimum
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      PrimCand q;
+      q.bv = __shfl_xor_sync(kFull, bv, o);
+      q.key = __shfl_xor_sync(kFull, key, o);
+      q.k = __shfl_xor_sync(kFull, k, o);
+      q.id = __shfl_xor_sync(kFull, id, o);
+      q.from = __shfl_xor_sync(kFull, from, o);
+      q.core = __shfl_xor_sync(kFull, core, o);
+#pragma unroll
+      for (int t = 0; t < DIM; ++t) q.x[t] = __shfl_xor_sync(kFull, x[t], o);
+      take(q);
+    }
+  }
+  __device__ __forceinline__ void store(PrimSlot& s) const {
+    s.bv = bv;
+    s.key = key;
+    s.k = k;
+    s.id = id;
+    s.from = from;
+    s.core = core;
+#pragma unroll
+    for (int t = 0; t < DIM; ++t) s.x[t] = x[t];
+  }
+  __device__ __forceinline__ void load(const PrimSlot& s) {
+    bv = s.bv;
+    key = s.key;
+    k = s.k;
+    id = s.id;
+    from = s.from;
+    core = s.core;
+#pragma unroll
+    for (int t = 0; t < DIM; ++t) x[t] = s.x[t];
+  }
+};
+
+__device__ __forceinline__ void bar_arrive(unsigned long long* p) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(p) : "memory");
+}
+__device__ __forceinline__ unsigned long long bar_poll(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // One cooperative launch for all n - 1 steps.  Step: every thread updates
-// best/from of its compacted positions (k = gtid + j * T) against the
-// current point and keeps its lexicographic minimum (best, key); block
-// minimum -> slot; grid barrier; every block reduces all slots to the same
-// winner; the owner thread of the winner's position moves the last element
-// into it (so the next step's reads of that position are its own writes).
+// best/from of its compacted positions (k = gtid + j * T, U loads in flight)
+// against the current point and keeps its lexicographic minimum (best,
+// key); the owner of the last position publishes that element (the
+// swap-with-last source); per-warp minima -> shared memory -> warp 0: block
+// minimum -> slot, release-arrive on the grid counter, acquire-spin, then
+// all slots (loads in flight together) -> the winner, which carries the
+// next current point; one block barrier releases the other warps.  The
+// owner thread of the winner's position moves the published last element
+// into it, so the next step's reads of that position are its own writes.
 template <int DIM, bool NUMPY>
 __global__ void __launch_bounds__(PRIM_BLOCK) k_prim(PrimArgs a) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
-  __shared__ PrimSlot wbest[PRIM_BLOCK / 32];
-  __shared__ PrimSlot win;
-  const int64_t T = (int64_t)gridDim.x * PRIM_BLOCK;
+  constexpr int NW = PRIM_BLOCK / 32;
+  constexpr int SPL = (PRIM_MAX_GRID + 31) / 32;  // slots per lane (upper bound)
+  __shared__ PrimSlot wbest[NW];
+  __shared__ PrimSlot win, last;
+  const uint32_t G = gridDim.x;
+  const int64_t T = (int64_t)G * PRIM_BLOCK;
   const int64_t gtid = (int64_t)blockIdx.x * PRIM_BLOCK + threadIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const PrimState& st = a.st;
+  constexpr int U = DIM <= 4 ? PRIM_U : DIM <= 6 ? 2 : 1;  // loads in flight vs registers
   int32_t cur = 0;
   double cc, curc[DIM];
 #pragma unroll
   for (int t = 0; t < DIM; ++t) curc[t] = a.pts[t];
   cc = a.core_sq[0];
-  const double INF = __longlong_as_double(0x7ff0000000000000ll);
   for (int64_t it = 0; it < a.n - 1; ++it) {
     const int64_t m = a.n - 1 - it;
-    double bv = INF;
-    int32_t bkey = 0x7fffffff, bk = -1, bid = 0, bfrom = 0;
-    for (int64_t k = gtid; k < m; k += T) {
-      double x[DIM];
+    PrimSlot* slots = a.slots + (it & 1) * (G + 1);
+    PrimCand<DIM> best;
+    best.reset();
+    for (int64_t k0 = gtid; k0 < m; k0 += T * U) {
+      double x[U][DIM], ck[U], bb[U];
+      int32_t fr[U], id[U];
 #pragma unroll
-      for (int t = 0; t < DIM; ++t) x[t] = st.acoord[t * st.cap + k];
-      double d = sqdist_prim<DIM, NUMPY>(x, curc);
-      const double ck = st.acore[k];
-      if (ck > d) d = ck;
-      if (cc > d) d = cc;
-      double b = st.abest[k];
-      int32_t fr = st.afrom[k];
-      if (d < b) {
-        b = d;
-        fr = cur;
-        st.abest[k] = b;
-        st.afrom[k] = fr;
+      for (int q = 0; q < U; ++q) {
+        const int64_t k = k0 + q * T;
+        const bool ok = k < m;
+#pragma unroll
+        for (int t = 0; t < DIM; ++t) x[q][t] = ok ? st.acoord[t * st.cap + k] : 0.0;
+        ck[q] = ok ? st.acore[k] : 0.0;
+        bb[q] = ok ? st.abest[k] : -1.0;
+        fr[q] = ok ? st.afrom[k] : 0;
+        id[q] = ok ? st.idx[k] : 0;
       }
-      const int32_t id = st.idx[k];
-      const int32_t key = NUMPY ? id : (int32_t)k;
-      if (slot_less(b, key, bv, bkey)) {
-        bv = b;
-        bkey = key;
-        bk = (int32_t)k;
-        bid = id;
-        bfrom = fr;
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int64_t k = k0 + q * T;
+        if (k < m) {
+          double d = sqdist_prim<DIM, NUMPY>(x[q], curc);
+          if (ck[q] > d) d = ck[q];
+          if (cc > d) d = cc;
+          if (d < bb[q]) {
+            bb[q] = d;
+            fr[q] = cur;
+            st.abest[k] = d;
+            st.afrom[k] = cur;
+          }
+          const int32_t key = NUMPY ? id[q] : (int32_t)k;
+          if (k == m - 1) {  // publish the swap-with-last source (post-update)
+            PrimSlot& l = slots[G];
+            l.bv = bb[q];
+            l.from = fr[q];
+            l.id = id[q];
+            l.core = ck[q];
+#pragma unroll
+            for (int t = 0; t < DIM; ++t) l.x[t] = x[q][t];
+          }
+          if (slot_less(bb[q], key, best.bv, best.key)) {
+            best.bv = bb[q];
+            best.key = key;
+            best.k = (int32_t)k;
+            best.id = id[q];
+            best.from = fr[q];
+            best.core = ck[q];
+#pragma unroll
+            for (int t = 0; t < DIM; ++t) best.x[t] = x[q][t];
+          }
+        }
       }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(kFull, bv, o);
-      const int32_t okey = __shfl_xor_sync(kFull, bkey, o), ok = __shfl_xor_sync(kFull, bk, o),
-                    oid = __shfl_xor_sync(kFull, bid, o), ofr = __shfl_xor_sync(kFull, bfrom, o);
-      if (slot_less(ov, okey, bv, bkey)) {
-        bv = ov;
-        bkey = okey;
-        bk = ok;
-        bid = oid;
-        bfrom = ofr;
-      }
-    }
-    if (lane == 0) wbest[wid] = PrimSlot{bv, bkey, bk, bid, bfrom};
+    best.warp_min();
+    if (lane == 0) best.store(wbest[wid]);
     __syncthreads();
-    PrimSlot* slots = a.slots + (it & 1) * gridDim.x;
     if (wid == 0) {
-      PrimSlot s = lane < PRIM_BLOCK / 32 ? wbest[lane] : PrimSlot{INF, 0x7fffffff, -1, 0, 0};
+      PrimCand<DIM> c;
+      if (lane < NW)
+        c.load(wbest[lane]);
+      else
+        c.reset();
+      c.warp_min();
+      if (lane == 0) {
+        c.store(slots[blockIdx.x]);
+        bar_arrive(a.bar);
+        const unsigned long long target = (unsigned long long)(it + 1) * G;
+        while (bar_poll(a.bar) < target) {
+        }
+      }
+      __syncwarp();
+      // (best, key) of every slot at once (loads in flight together), the
+      // minimum's slot index, then that slot and the published last element
+      double sb[SPL];
+      int32_t sk[SPL];
+#pragma unroll
+      for (int q = 0; q < SPL; ++q) {
+        const uint32_t b = lane + 32u * q;
+        sb[q] = b < G ? __ldcg(&slots[b].bv) : __longlong_as_double(0x7ff0000000000000ll);
+        sk[q] = b < G ? __ldcg(&slots[b].key) : 0x7fffffff;
+      }
+      double bv = sb[0];
+      int32_t bkey = sk[0], bslot = lane;
+#pragma unroll
+      for (int q = 1; q < SPL; ++q)
+        if (slot_less(sb[q], sk[q], bv, bkey)) {
+          bv = sb[q];
+          bkey = sk[q];
+          bslot = lane + 32 * q;
+        }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(kFull, s.bv, o);
-        const int32_t okey = __shfl_xor_sync(kFull, s.key, o), ok = __shfl_xor_sync(kFull, s.k, o),
-                      oid = __shfl_xor_sync(kFull, s.id, o), ofr = __shfl_xor_sync(kFull, s.from, o);
-        if (slot_less(ov, okey, s.bv, s.key)) s = PrimSlot{ov, okey, ok, oid, ofr};
+        const double ov = __shfl_xor_sync(kFull, bv, o);
+        const int32_t ok = __shfl_xor_sync(kFull, bkey, o), os = __shfl_xor_sync(kFull, bslot, o);
+        if (slot_less(ov, ok, bv, bkey)) {
+          bv = ov;
+          bkey = ok;
+          bslot = os;
+        }
       }
-      if (lane == 0) slots[blockIdx.x] = s;
-    }
-    grid.sync();
-    if (wid == 0) {
-      PrimSlot s{INF, 0x7fffffff, -1, 0, 0};
-      for (uint32_t b = lane; b < gridDim.x; b += 32) {
-        const PrimSlot o = slots[b];
-        if (slot_less(o.bv, o.key, s.bv, s.key)) s = o;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(kFull, s.bv, o);
-        const int32_t okey = __shfl_xor_sync(kFull, s.key, o), ok = __shfl_xor_sync(kFull, s.k, o),
-                      oid = __shfl_xor_sync(kFull, s.id, o), ofr = __shfl_xor_sync(kFull, s.from, o);
-        if (slot_less(ov, okey, s.bv, s.key)) s = PrimSlot{ov, okey, ok, oid, ofr};
-      }
-      if (lane == 0) win = s;
+      if (lane == 0) win = ldcg_slot(&slots[bslot]);
+      if (lane == 1) last = ldcg_slot(&slots[G]);
     }
     __syncthreads();
-    const PrimSlot w = win;
+    PrimCand<DIM> w;
+    w.load(win);
     if (gtid == 0) {
       a.out_u[it] = w.from;
       a.out_v[it] = w.id;
       a.out_w[it] = w.bv;
     }
-    if (w.k != m - 1 && gtid == w.k % T) {  // swap-with-last (pointgen.py:141-148)
-      const int64_t l = m - 1, bk = w.k;
-      st.idx[bk] = st.idx[l];
-      st.acore[bk] = st.acore[l];
-      st.abest[bk] = st.abest[l];
-      st.afrom[bk] = st.afrom[l];
+    if (w.k != m - 1 && gtid == (int64_t)w.k % T) {  // swap-with-last (pointgen.py:141-148)
+      const int64_t bk = w.k;
+      const PrimSlot& l = last;
+      st.idx[bk] = l.id;
+      st.acore[bk] = l.core;
+      st.abest[bk] = l.bv;
+      st.afrom[bk] = l.from;
 #pragma unroll
-      for (int t = 0; t < DIM; ++t) st.acoord[t * st.cap + bk] = st.acoord[t * st.cap + l];
+      for (int t = 0; t < DIM; ++t) st.acoord[t * st.cap + bk] = l.x[t];
     }
     cur = w.id;
 #pragma unroll
-    for (int t = 0; t < DIM; ++t) curc[t] = a.pts[(int64_t)cur * DIM + t];
-    cc = a.core_sq[cur];
-    __syncthreads();  // `win` / `wbest` reused by the next step
+    for (int t = 0; t < DIM; ++t) curc[t] = w.x[t];
+    cc = w.core;
+    __syncthreads();  // win / last / wbest read before the next step rewrites them
   }
 }
 

@@ -20,8 +20,10 @@ BS = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 def kind(name: str) -> str:
     rules = [
         ("k_key_reduce", "sort1_hist"), ("k_upsweep", "upsweep_scan"), ("k_chunk_scan", "upsweep_scan"),
+        ("Sort1Loader", "sort1_pass_first"), ("Sort1Emitter", "sort1_pass_final"),
         ("Sort1FirstLoader", "sort1_pass_first"), ("Sort1FinalEmitter", "sort1_pass_final"),
         ("k_downsweep<unsigned long, 0,", "sort2_pass"), ("k_downsweep<unsigned long", "sort1_pass_mid"),
+        ("k_downsweep<unsigned int, 3,", "sort1_pass_mid"),
         ("k_downsweep<unsigned int", "sort2_pass"),
         ("k_fine_hist", "mi_hist"), ("k_fine_scan", "mi_hist"),
         ("k_split<0, EdgeRecSrc", "mi_split_a"), ("k_split<1, AosRecSrc<3>", "mi_split_b"),

@@ -45,7 +45,7 @@ constexpr int S1N_ITEMS = 12;  // narrow (32-bit) keys: bigger tiles in the same
 constexpr int64_t S1_ALIGN = 3 * S1_BLOCK * 8;  // lcm of both tiles: one chunk geometry
 static_assert(S1_ALIGN % (S1_BLOCK * S1_ITEMS) == 0 && S1_ALIGN % (S1_BLOCK * S1N_ITEMS) == 0, "S1_ALIGN");
 // Chain sort: u32 key + 1-word payload.
-constexpr int S2_BLOCK = 512, S2_ITEMS = 16, S2_MINB = 1, S2_BITS = 9;
+constexpr int S2_BLOCK = 256, S2_ITEMS = 16, S2_MINB = 2, S2_BITS = 9;
 constexpr int64_t kDirectMiBytes = 64ll << 20;  // direct scatter-max below this mi64 size
 
 enum KernelKind {

@@ -547,7 +547,7 @@ def read_dendrogram_b200(path, device=None, use_sidecar: bool = True) -> BuildRe
             except (ValueError, OSError):
                 arr = None
             if arr is not None and arr.dtype == np.int32 and arr.shape == (n + nv,):
-                both = torch.from_numpy(np.ascontiguousarray(arr)).to(dev)
+                both = torch.from_numpy(np.array(arr)).to(dev)
                 return BuildResult(orig_of=None, heights=None, edge_parent=both[:n], vertex_parent=both[n:])
     with open(path, "rb") as f:
         data = f.read()

@@ -260,22 +260,80 @@ __global__ void __launch_bounds__(PRIM_BLOCK) k_prim(PrimArgs a) {
   const int64_t gtid = (int64_t)blockIdx.x * PRIM_BLOCK + threadIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const PrimState& st = a.st;
-  constexpr int U = DIM <= 4 ? PRIM_U : DIM <= 6 ? 2 : 1;  // loads in flight vs registers
+  constexpr int U = DIM <= 3 ? PRIM_U : DIM <= 6 ? 2 : 1;  // register-resident positions
   int32_t cur = 0;
   double cc, curc[DIM];
 #pragma unroll
   for (int t = 0; t < DIM; ++t) curc[t] = a.pts[t];
   cc = a.core_sq[0];
+  // the thread's first U positions (k = gtid + q * T) live in registers for
+  // the whole kernel: only the owner ever reads or writes a position, the
+  // swap source is published from registers and the swap target is patched
+  // in registers, so those positions never go back to memory; positions
+  // beyond them are read and written in HBM / L2 as before.
+  double rx[U][DIM], rck[U], rbb[U];
+  int32_t rfr[U], rid[U];
+#pragma unroll
+  for (int q = 0; q < U; ++q) {
+    const int64_t k = gtid + q * T;
+    const bool ok = k < a.n - 1;
+#pragma unroll
+    for (int t = 0; t < DIM; ++t) rx[q][t] = ok ? st.acoord[t * st.cap + k] : 0.0;
+    rck[q] = ok ? st.acore[k] : 0.0;
+    rbb[q] = ok ? st.abest[k] : -1.0;
+    rfr[q] = ok ? st.afrom[k] : 0;
+    rid[q] = ok ? st.idx[k] : 0;
+  }
   for (int64_t it = 0; it < a.n - 1; ++it) {
     const int64_t m = a.n - 1 - it;
     PrimSlot* slots = a.slots + (it & 1) * (G + 1);
     PrimCand<DIM> best;
     best.reset();
-    for (int64_t k0 = gtid; k0 < m; k0 += T * U) {
-      double x[U][DIM], ck[U], bb[U];
-      int32_t fr[U], id[U];
+    auto visit = [&](int64_t k, const double (&x)[DIM], double ck, double& bb, int32_t& fr, int32_t id,
+                     bool in_memory) {
+      double d = sqdist_prim<DIM, NUMPY>(x, curc);
+      if (ck > d) d = ck;
+      if (cc > d) d = cc;
+      if (d < bb) {
+        bb = d;
+        fr = cur;
+        if (in_memory) {
+          st.abest[k] = d;
+          st.afrom[k] = cur;
+        }
+      }
+      const int32_t key = NUMPY ? id : (int32_t)k;
+      if (k == m - 1) {  // publish the swap-with-last source (post-update)
+        PrimSlot& l = slots[G];
+        l.bv = bb;
+        l.from = fr;
+        l.id = id;
+        l.core = ck;
 #pragma unroll
-      for (int q = 0; q < U; ++q) {
+        for (int t = 0; t < DIM; ++t) l.x[t] = x[t];
+      }
+      if (slot_less(bb, key, best.bv, best.key)) {
+        best.bv = bb;
+        best.key = key;
+        best.k = (int32_t)k;
+        best.id = id;
+        best.from = fr;
+        best.core = ck;
+#pragma unroll
+        for (int t = 0; t < DIM; ++t) best.x[t] = x[t];
+      }
+    };
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int64_t k = gtid + q * T;
+      if (k < m) visit(k, rx[q], rck[q], rbb[q], rfr[q], rid[q], false);
+    }
+    constexpr int UM = DIM <= 4 ? 2 : 1;  // memory-resident positions in flight
+    for (int64_t k0 = gtid + U * T; k0 < m; k0 += T * UM) {
+      double x[UM][DIM], ck[UM], bb[UM];
+      int32_t fr[UM], id[UM];
+#pragma unroll
+      for (int q = 0; q < UM; ++q) {
         const int64_t k = k0 + q * T;
         const bool ok = k < m;
 #pragma unroll
@@ -286,39 +344,9 @@ __global__ void __launch_bounds__(PRIM_BLOCK) k_prim(PrimArgs a) {
         id[q] = ok ? st.idx[k] : 0;
       }
 #pragma unroll
-      for (int q = 0; q < U; ++q) {
+      for (int q = 0; q < UM; ++q) {
         const int64_t k = k0 + q * T;
-        if (k < m) {
-          double d = sqdist_prim<DIM, NUMPY>(x[q], curc);
-          if (ck[q] > d) d = ck[q];
-          if (cc > d) d = cc;
-          if (d < bb[q]) {
-            bb[q] = d;
-            fr[q] = cur;
-            st.abest[k] = d;
-            st.afrom[k] = cur;
-          }
-          const int32_t key = NUMPY ? id[q] : (int32_t)k;
-          if (k == m - 1) {  // publish the swap-with-last source (post-update)
-            PrimSlot& l = slots[G];
-            l.bv = bb[q];
-            l.from = fr[q];
-            l.id = id[q];
-            l.core = ck[q];
-#pragma unroll
-            for (int t = 0; t < DIM; ++t) l.x[t] = x[q][t];
-          }
-          if (slot_less(bb[q], key, best.bv, best.key)) {
-            best.bv = bb[q];
-            best.key = key;
-            best.k = (int32_t)k;
-            best.id = id[q];
-            best.from = fr[q];
-            best.core = ck[q];
-#pragma unroll
-            for (int t = 0; t < DIM; ++t) best.x[t] = x[q][t];
-          }
-        }
+        if (k < m) visit(k, x[q], ck[q], bb[q], fr[q], id[q], true);
       }
     }
     best.warp_min();
@@ -382,12 +410,26 @@ __global__ void __launch_bounds__(PRIM_BLOCK) k_prim(PrimArgs a) {
     if (w.k != m - 1 && gtid == (int64_t)w.k % T) {  // swap-with-last (pointgen.py:141-148)
       const int64_t bk = w.k;
       const PrimSlot& l = last;
-      st.idx[bk] = l.id;
-      st.acore[bk] = l.core;
-      st.abest[bk] = l.bv;
-      st.afrom[bk] = l.from;
+      const int64_t q0 = bk / T;
+      if (q0 < U) {
 #pragma unroll
-      for (int t = 0; t < DIM; ++t) st.acoord[t * st.cap + bk] = l.x[t];
+        for (int q = 0; q < U; ++q)
+          if (q == q0) {
+            rid[q] = l.id;
+            rck[q] = l.core;
+            rbb[q] = l.bv;
+            rfr[q] = l.from;
+#pragma unroll
+            for (int t = 0; t < DIM; ++t) rx[q][t] = l.x[t];
+          }
+      } else {
+        st.idx[bk] = l.id;
+        st.acore[bk] = l.core;
+        st.abest[bk] = l.bv;
+        st.afrom[bk] = l.from;
+#pragma unroll
+        for (int t = 0; t < DIM; ++t) st.acoord[t * st.cap + bk] = l.x[t];
+      }
     }
     cur = w.id;
 #pragma unroll

@@ -1,7 +1,8 @@
 """Small builds for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
 every entry point (device build incl. the cooperative tail, host-buffer build,
-validation incl. the duplicate-sort path, dendrogram height) on small trees,
-each checked against the CPU oracle."""
+validation incl. the duplicate-sort path, dendrogram height, the v1 text
+writer / reader / verify, the mutual-reachability MST producer) on small
+inputs, each checked against the CPU oracle."""
 import os
 import sys
 
@@ -46,4 +47,33 @@ for name, (uu, vv) in cases.items():
         except err as exc:
             return str(exc)
     bad += verdict(validate_b200, _tree_format_error()) != verdict(O.weighted_tree, O.TreeFormatError)
+# edge sort key transforms: top-field compaction + narrow 32-bit keys
+rng = np.random.default_rng(5)
+nv, u, v, _ = synth.random_attach(20_000, seed=5)
+for w in (rng.integers(0, 4096, nv - 1).astype(np.float64),
+          rng.choice([-1.0, 1.0], nv - 1) * rng.integers(1, 64, nv - 1) * np.exp2(rng.integers(-3, 3, nv - 1))):
+    r = b.build(nv, u, v, w)
+    e = O.build(nv, u, v, w)
+    bad += not (np.array_equal(r.orig_of.cpu().numpy(), e.orig_of)
+                and np.array_equal(r.edge_parent.cpu().numpy(), e.edge_parent))
+# v1 text format: device writer -> device reader -> verify
+import tempfile  # noqa: E402
+from paper_2401_06089_b200 import read_dendrogram_b200, verify_b200, write_dendrogram_b200  # noqa: E402
+with tempfile.TemporaryDirectory() as d:
+    pa, pb = os.path.join(d, "a"), os.path.join(d, "b")
+    write_dendrogram_b200(pa, r.edge_parent, r.vertex_parent)
+    write_dendrogram_b200(pb, r.edge_parent, r.vertex_parent, sidecar=True)
+    back = read_dendrogram_b200(pa)
+    bad += not bool((back.edge_parent == r.edge_parent).all())
+    bad += verify_b200(pa, pb) != (0, "identical")
+# upstream producer: core distances + both Prim engines
+from paper_2401_06089_b200 import mutual_reachability_mst_b200  # noqa: E402
+for dim, engine in ((3, "numba"), (8, "numpy"), (2, "numba")):
+    x = rng.standard_normal((300, dim))
+    if dim == 2:
+        x = np.round(x * 3)  # ties
+    t = mutual_reachability_mst_b200(x, 3, engine)
+    _, eu, ev, ew = O.mutual_reachability_mst(x, 3, engine)
+    bad += not (np.array_equal(t.u.cpu().numpy(), eu) and np.array_equal(t.v.cpu().numpy(), ev)
+                and np.array_equal(t.w.cpu().numpy(), ew))
 print("sanitize driver done, mismatches:", bad)

@@ -41,9 +41,14 @@ namespace dmst {
 // Radix sort geometry (sub-tile = BLOCK x ITEMS items; MINB CTAs per SM).
 // Edge sort: u64 key + 3-word payload.
 constexpr int S1_BLOCK = 512, S1_ITEMS = 8, S1_MINB = 1;
-constexpr int S1N_ITEMS = 12;  // narrow (32-bit) keys: bigger tiles in the same shared memory
-constexpr int64_t S1_ALIGN = 3 * S1_BLOCK * 8;  // lcm of both tiles: one chunk geometry
-static_assert(S1_ALIGN % (S1_BLOCK * S1_ITEMS) == 0 && S1_ALIGN % (S1_BLOCK * S1N_ITEMS) == 0, "S1_ALIGN");
+// narrow (32-bit) keys: 256-thread CTAs, two per SM, 12-item tiles
+constexpr int S1N_BLOCK = 256, S1N_MINB = 2;
+constexpr int S1N_ITEMS = 12;
+// the fused first upsweep counts before the key width is known: its chunk
+// geometry (S1N_MINB chunks per SM, multiples of S1_ALIGN) is shared by the
+// first pass of either width (the wide one then runs in two waves)
+constexpr int64_t S1_ALIGN = 12288;
+static_assert(S1_ALIGN % (S1_BLOCK * S1_ITEMS) == 0 && S1_ALIGN % (S1N_BLOCK * S1N_ITEMS) == 0, "S1_ALIGN");
 // Chain sort: u32 key + 1-word payload.
 constexpr int S2_BLOCK = 256, S2_ITEMS = 16, S2_MINB = 2, S2_BITS = 9;
 constexpr int64_t kDirectMiBytes = 64ll << 20;  // direct scatter-max below this mi64 size
@@ -356,12 +361,12 @@ SweepGeom sweep_geom(const Ctx& c, int64_t n, int T, int minb, int64_t align = 0
 // upsweep already produced them), chunk scan, downsweep.
 template <typename K, int PW, int BLOCK, int ITEMS, int MINB, int BITS, class Loader, class Emitter>
 int64_t radix_pass(Ctx& c, int kind, int64_t n, int shift, Loader ld, Emitter em, bool counts_ready = false,
-                   int64_t align = 0) {
+                   int64_t align = 0, int geom_minb = 0) {
   using S = DownSmem<K, PW, BLOCK, ITEMS, Loader, Emitter, BITS>;
   constexpr int T = S::T;
   auto kern = k_downsweep<K, PW, BLOCK, ITEMS, MINB, Loader, Emitter, BITS>;
   smem_attr(kern, (int)S::bytes());
-  const SweepGeom g = sweep_geom(c, n, T, MINB, align);
+  const SweepGeom g = sweep_geom(c, n, T, geom_minb ? geom_minb : MINB, align);
   SweepArgs a{};
   a.n = n;
   a.shift = shift;
@@ -390,7 +395,7 @@ int64_t radix_pass(Ctx& c, int kind, int64_t n, int shift, Loader ld, Emitter em
 template <typename K, int PW, int BLOCK, int ITEMS, int MINB, int BITS, class FirstLoader, class FinalEmitter>
 int64_t run_sort(Ctx& c, const int (&kinds)[3], int64_t n, const std::vector<int>& shifts,
               K* const (&bufK)[2], uint32_t* const (&bufP)[2], FirstLoader first, FinalEmitter final_em,
-              int ready_shift = -1, int64_t align = 0) {
+              int ready_shift = -1, int64_t align = 0, int first_minb = 0) {
   const int P = (int)shifts.size();
   if (P == 0) {
     c.begin(KK_OTHER);
@@ -405,9 +410,11 @@ int64_t run_sort(Ctx& c, const int (&kinds)[3], int64_t n, const std::vector<int
     ArrayLoader<K, PW> ldr{bufK[in], bufP[in]};
     const bool ready = p == 0 && shifts[0] == ready_shift;
     if (P == 1)
-      G = radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[2], n, shifts[p], first, final_em, ready, align);
+      G = radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[2], n, shifts[p], first, final_em, ready, align,
+                                                      first_minb);
     else if (p == 0)
-      G = radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[0], n, shifts[p], first, mid, ready, align);
+      G = radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[0], n, shifts[p], first, mid, ready, align,
+                                                      first_minb);
     else if (p == P - 1)
       G = radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[2], n, shifts[p], ldr, final_em, false, align);
     else
@@ -455,7 +462,7 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
   c.sync();
   const std::vector<int> guess = active_digits(sao[0], sao[1], 8, 64);
   const int d0 = guess.empty() ? 0 : guess[0];
-  const SweepGeom g = sweep_geom(c, n, S1_BLOCK * S1_ITEMS, S1_MINB, S1_ALIGN);
+  const SweepGeom g = sweep_geom(c, n, S1_BLOCK * S1_ITEMS, S1N_MINB, S1_ALIGN);
   SweepArgs a{};
   a.n = n;
   a.shift = d0;
@@ -516,14 +523,14 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
     Sort1Emitter<uint32_t> em32{em.orig_of, em.heights, em.euv, em.ru, em.rv, em.inv,
                                 lo ? kand & ((1ull << lo) - 1) : 0ull, (uint32_t)lo};
     em32.base |= lo + 32 < 64 ? kand & ~((1ull << (lo + 32)) - 1) : 0ull;
-    run_sort<uint32_t, 3, S1_BLOCK, S1N_ITEMS, S1_MINB, 8>(
+    run_sort<uint32_t, 3, S1N_BLOCK, S1N_ITEMS, S1N_MINB, 8>(
         c, {KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL}, n, s32, bufK, bufP,
         Sort1Loader<uint32_t>{w, u, v, code, (uint32_t)lo}, em32, ready >= 0 ? 0 : -1, S1_ALIGN);
   } else {
     uint64_t* const bufK[2] = {(uint64_t*)R, (uint64_t*)(R + 8 * n)};
     run_sort<uint64_t, 3, S1_BLOCK, S1_ITEMS, S1_MINB, 8>(c, {KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL}, n,
                                                        shifts, bufK, bufP, Sort1FirstLoader{w, u, v, code}, em,
-                                                       ready, S1_ALIGN);
+                                                       ready, S1_ALIGN, S1N_MINB);
   }
   if (nz) {
     c.begin(KK_OTHER);

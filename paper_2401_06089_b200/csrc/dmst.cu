@@ -50,7 +50,7 @@ constexpr int S1N_ITEMS = 12;
 constexpr int64_t S1_ALIGN = 12288;
 static_assert(S1_ALIGN % (S1_BLOCK * S1_ITEMS) == 0 && S1_ALIGN % (S1N_BLOCK * S1N_ITEMS) == 0, "S1_ALIGN");
 // Chain sort: u32 key + 1-word payload.
-constexpr int S2_BLOCK = 256, S2_ITEMS = 16, S2_MINB = 2, S2_BITS = 9;
+constexpr int S2_BLOCK = 256, S2_ITEMS = 20, S2_MINB = 2, S2_BITS = 9;
 constexpr int64_t kDirectMiBytes = 64ll << 20;  // direct scatter-max below this mi64 size
 
 enum KernelKind {

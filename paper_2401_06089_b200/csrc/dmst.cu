@@ -50,7 +50,12 @@ constexpr int S1N_ITEMS = 12;
 constexpr int64_t S1_ALIGN = 12288;
 static_assert(S1_ALIGN % (S1_BLOCK * S1_ITEMS) == 0 && S1_ALIGN % (S1N_BLOCK * S1N_ITEMS) == 0, "S1_ALIGN");
 // Chain sort: u32 key + 1-word payload.
-constexpr int S2_BLOCK = 256, S2_ITEMS = 20, S2_MINB = 2, S2_BITS = 9;
+constexpr int S2_BLOCK = 512, S2_ITEMS = 16, S2_MINB = 1, S2_BITS = 9;
+// large trees: 256-thread CTAs, two per SM, 20-item tiles (2.36 -> 2.25 ms at
+// 128M); small trees, often several per GPU on concurrent streams, keep the
+// fewer, larger chunks of one CTA per SM (config 5: 129 -> 124 ms)
+constexpr int S2L_BLOCK = 256, S2L_ITEMS = 20, S2L_MINB = 2;
+constexpr int64_t kS2LargeEdges = 32ll << 20;
 constexpr int64_t kDirectMiBytes = 64ll << 20;  // direct scatter-max below this mi64 size
 
 enum KernelKind {
@@ -854,8 +859,12 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     ArrayEmitter<uint64_t, 0> fin{bufK[lastb], nullptr};
     std::vector<int> shifts64(shifts);
     for (int& x : shifts64) x += 32;
-    run_sort<uint64_t, 0, S2_BLOCK, S2_ITEMS, S2_MINB, S2_BITS>(c, {KK_SORT2_PASS, KK_SORT2_PASS, KK_SORT2_PASS}, n,
-                                                             shifts64, bufK, bufP, Sort2FirstLoader{keys}, fin);
+    if (n >= kS2LargeEdges)
+      run_sort<uint64_t, 0, S2L_BLOCK, S2L_ITEMS, S2L_MINB, S2_BITS>(
+          c, {KK_SORT2_PASS, KK_SORT2_PASS, KK_SORT2_PASS}, n, shifts64, bufK, bufP, Sort2FirstLoader{keys}, fin);
+    else
+      run_sort<uint64_t, 0, S2_BLOCK, S2_ITEMS, S2_MINB, S2_BITS>(c, {KK_SORT2_PASS, KK_SORT2_PASS, KK_SORT2_PASS}, n,
+                                                               shifts64, bufK, bufP, Sort2FirstLoader{keys}, fin);
     if (st && st->want_chains) {
       uint32_t* cnt = w.small + SM_MISC + 60;
       c.zero(cnt, 4);

@@ -1036,11 +1036,9 @@ void mreach_impl(Ctx& c, const double* pts, int64_t n, int k, int engine, int32_
   int per_sm = 0;
   DMST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PRIM_BLOCK, 0));
   if (per_sm < 1) invalid("k_prim cannot be co-resident");
-  // one slot per thread in the post-barrier reduction: grid <= PRIM_BLOCK
-  int64_t grid = std::max<int64_t>(
+  // at most PRIM_MAX_GRID blocks: warp 0 reduces all block slots after the barrier
+  const int64_t grid = std::max<int64_t>(
       1, std::min<int64_t>({cdiv(n - 1, 2 * PRIM_BLOCK), (int64_t)c.sms * per_sm, (int64_t)PRIM_MAX_GRID}));
-  if (const char* e = getenv("DMST_PRIM_GRID"))
-    grid = std::max<int64_t>(1, std::min<int64_t>({atoll(e), (int64_t)c.sms * per_sm, (int64_t)PRIM_MAX_GRID}));
   PrimArgs a{pts, core_sq, n, st, slots, bar, u, v, w};
   void* args[] = {&a};
   c.begin(KK_OTHER);

@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(256) k_upsweep(SweepArgs a, Loader ld, KeyRed 
   const int64_t plen = (a.chunk / kUpSplit + 1023) & ~int64_t(1023);
   const int64_t begin = cbeg + part * plen;
   const int64_t end = min(min(a.n, cbeg + a.chunk), begin + plen);
-  constexpr int U = 8;
+  constexpr int U = KEYRED ? 16 : 8;  // the fused pass over w is load-latency-bound at 8
   uint64_t ka = ~0ull, ko = 0ull;
   uint32_t tw = 0;
   bool nz = false;

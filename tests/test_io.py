@@ -159,3 +159,67 @@ def test_device_sidecar_roundtrip():
         os.utime(sidecar_path(path), (1, 1))
         back = read_dendrogram_b200(path)
         assert int(back.edge_parent[5]) == -1
+
+
+@pytest.mark.parametrize("t", GOLDEN[:6], ids=[t["name"] for t in GOLDEN[:6]])
+def test_oracle_verify_matches_reference_cli(t, capsys):
+    """O.verify_text (the checker of verify_b200) against the reference's own
+    `dendromst verify` (cli.py:138-155) on the same file pairs."""
+    if _reference_writer() is None:
+        pytest.skip("reference package not importable here")
+    import argparse
+    from dendromst.cli import _cmd_verify
+    with tempfile.TemporaryDirectory() as d:
+        for name, a, b in _variants(t):
+            pa, pb = os.path.join(d, "a"), os.path.join(d, "b")
+            _write(pa, a)
+            _write(pb, b)
+            capsys.readouterr()
+            rc = _cmd_verify(argparse.Namespace(a=pa, b=pb))
+            line = capsys.readouterr().out.strip()
+            assert (rc, line) == O.verify_text(a, b), name
+
+
+def test_reader_messages_match_reference(tmp_path):
+    """The reader's header / line / count errors, as read_dendrogram
+    (dendro_io.py:41-75) words them (checked on the reference itself)."""
+    if _reference_writer() is None:
+        pytest.skip("reference package not importable here")
+    from dendromst.dendro_io import DendrogramFormatError, read_dendrogram
+    cases = {
+        "header": b"#dendrogram v2 n=1 nv=2\n",
+        "line": b"#dendrogram v1 n=1 nv=2\nE 0 -1\nX 1 0\n",
+        "count": b"#dendrogram v1 n=1 nv=2\nE 0 -1\nV 0 0\n",
+    }
+    expect = {"header": "bad header: '#dendrogram v2 n=1 nv=2'", "line": "bad line: 'X 1 0'",
+              "count": "expected 1 edge and 2 vertex lines, got 1 and 1"}
+    for name, data in cases.items():
+        p = tmp_path / name
+        p.write_bytes(data)
+        with pytest.raises(DendrogramFormatError) as ei:
+            read_dendrogram(str(p))
+        assert str(ei.value) == expect[name], name
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+def test_device_reader_messages(tmp_path):
+    """read_dendrogram_b200 raises the reference's exact messages (the strings
+    test_reader_messages_match_reference pins on the reference)."""
+    from paper_2401_06089_b200 import read_dendrogram_b200
+    from paper_2401_06089_b200.api import _format_error
+    cases = {
+        "header": (b"#dendrogram v2 n=1 nv=2\n", "bad header: '#dendrogram v2 n=1 nv=2'"),
+        "line": (b"#dendrogram v1 n=1 nv=2\nE 0 -1\nX 1 0\n", "bad line: 'X 1 0'"),
+        "count": (b"#dendrogram v1 n=1 nv=2\nE 0 -1\nV 0 0\n", "expected 1 edge and 2 vertex lines, got 1 and 1"),
+    }
+    for name, (data, msg) in cases.items():
+        p = tmp_path / name
+        p.write_bytes(data)
+        with pytest.raises(_format_error()) as ei:
+            read_dendrogram_b200(str(p))
+        assert str(ei.value) == msg, name
+    p = tmp_path / "ok"
+    p.write_bytes(b"#dendrogram v1 n=1 nv=2\n# comment\n\nE 0 -1\nV 0 0\nV 1 0\n")
+    r = read_dendrogram_b200(str(p))
+    assert r.edge_parent.tolist() == [-1] and r.vertex_parent.tolist() == [0, 0]

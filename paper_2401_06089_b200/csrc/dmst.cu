@@ -1033,8 +1033,13 @@ void mreach_impl(Ctx& c, const double* pts, int64_t n, int k, int engine, int32_
   c.launched();
   const bool numpy = engine == 2 || (engine == 0 && n < 4096);  // "auto" (pointgen.py:170-171)
   const void* kern = numpy ? (const void*)k_prim<DIM, true> : (const void*)k_prim<DIM, false>;
+  constexpr size_t psm = prim_smem_bytes<DIM>();
+  if (numpy)
+    smem_attr(k_prim<DIM, true>, (int)psm);
+  else
+    smem_attr(k_prim<DIM, false>, (int)psm);
   int per_sm = 0;
-  DMST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PRIM_BLOCK, 0));
+  DMST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PRIM_BLOCK, psm));
   if (per_sm < 1) invalid("k_prim cannot be co-resident");
   // at most PRIM_MAX_GRID blocks: warp 0 reduces all block slots after the barrier
   const int64_t grid = std::max<int64_t>(
@@ -1042,7 +1047,7 @@ void mreach_impl(Ctx& c, const double* pts, int64_t n, int k, int engine, int32_
   PrimArgs a{pts, core_sq, n, st, slots, bar, u, v, w};
   void* args[] = {&a};
   c.begin(KK_OTHER);
-  DMST_CUDA(cudaLaunchCooperativeKernel(kern, dim3((unsigned)grid), dim3(PRIM_BLOCK), args, 0, c.s));
+  DMST_CUDA(cudaLaunchCooperativeKernel(kern, dim3((unsigned)grid), dim3(PRIM_BLOCK), args, psm, c.s));
   c.launched();
   c.begin(KK_OTHER);
   k_sqrt_inplace<<<grid_for(n - 1, EW_BLOCK), EW_BLOCK, 0, c.s>>>(w, n - 1);

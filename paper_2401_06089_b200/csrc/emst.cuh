@@ -164,6 +164,16 @@ __global__ void k_prim_init(const double* __restrict__ pts, const double* __rest
 }
 
 constexpr int PRIM_BLOCK = 512, PRIM_U = 4, PRIM_MAX_GRID = 296;
+// positions per thread staged in shared memory after the register-resident
+// ones: ~200 KB per CTA (8 B per coordinate + core + best, 4 B from + id)
+template <int DIM>
+__host__ __device__ constexpr int prim_smem_slots() {
+  return (200 * 1024) / (PRIM_BLOCK * (8 * DIM + 24));
+}
+template <int DIM>
+__host__ __device__ constexpr size_t prim_smem_bytes() {
+  return (size_t)prim_smem_slots<DIM>() * PRIM_BLOCK * (8 * DIM + 24);
+}
 struct PrimArgs {
   const double* pts;
   const double* core_sq;
@@ -284,6 +294,26 @@ __global__ void __launch_bounds__(PRIM_BLOCK) k_prim(PrimArgs a) {
     rfr[q] = ok ? st.afrom[k] : 0;
     rid[q] = ok ? st.idx[k] : 0;
   }
+  // the next S positions live in this CTA's shared memory (owner-only
+  // slots, SoA per position index j: no bank conflicts, no barriers)
+  constexpr int S = prim_smem_slots<DIM>();
+  extern __shared__ __align__(16) unsigned char prim_sm[];
+  double* sx = reinterpret_cast<double*>(prim_sm);          // [DIM][S][BLOCK]
+  double* sck = sx + DIM * S * PRIM_BLOCK;                   // [S][BLOCK]
+  double* sbb = sck + S * PRIM_BLOCK;                        // [S][BLOCK]
+  int32_t* sfr = reinterpret_cast<int32_t*>(sbb + S * PRIM_BLOCK);
+  int32_t* sid = sfr + S * PRIM_BLOCK;
+  const int tid = threadIdx.x;
+  for (int j = 0; j < S; ++j) {
+    const int64_t k = gtid + (int64_t)(U + j) * T;
+    const bool ok = k < a.n - 1;
+#pragma unroll
+    for (int t = 0; t < DIM; ++t) sx[(t * S + j) * PRIM_BLOCK + tid] = ok ? st.acoord[t * st.cap + k] : 0.0;
+    sck[j * PRIM_BLOCK + tid] = ok ? st.acore[k] : 0.0;
+    sbb[j * PRIM_BLOCK + tid] = ok ? st.abest[k] : -1.0;
+    sfr[j * PRIM_BLOCK + tid] = ok ? st.afrom[k] : 0;
+    sid[j * PRIM_BLOCK + tid] = ok ? st.idx[k] : 0;
+  }
   for (int64_t it = 0; it < a.n - 1; ++it) {
     const int64_t m = a.n - 1 - it;
     PrimSlot* slots = a.slots + (it & 1) * (G + 1);
@@ -328,8 +358,23 @@ __global__ void __launch_bounds__(PRIM_BLOCK) k_prim(PrimArgs a) {
       const int64_t k = gtid + q * T;
       if (k < m) visit(k, rx[q], rck[q], rbb[q], rfr[q], rid[q], false);
     }
+    for (int j = 0; j < S; ++j) {
+      const int64_t k = gtid + (int64_t)(U + j) * T;
+      if (k >= m) break;  // positions grow with j
+      double x[DIM];
+#pragma unroll
+      for (int t = 0; t < DIM; ++t) x[t] = sx[(t * S + j) * PRIM_BLOCK + tid];
+      double bb = sbb[j * PRIM_BLOCK + tid];
+      int32_t fr = sfr[j * PRIM_BLOCK + tid];
+      const double bb0 = bb;
+      visit(k, x, sck[j * PRIM_BLOCK + tid], bb, fr, sid[j * PRIM_BLOCK + tid], false);
+      if (bb != bb0) {
+        sbb[j * PRIM_BLOCK + tid] = bb;
+        sfr[j * PRIM_BLOCK + tid] = fr;
+      }
+    }
     constexpr int UM = DIM <= 4 ? 2 : 1;  // memory-resident positions in flight
-    for (int64_t k0 = gtid + U * T; k0 < m; k0 += T * UM) {
+    for (int64_t k0 = gtid + (int64_t)(U + S) * T; k0 < m; k0 += T * UM) {
       double x[UM][DIM], ck[UM], bb[UM];
       int32_t fr[UM], id[UM];
 #pragma unroll
@@ -411,7 +456,15 @@ __global__ void __launch_bounds__(PRIM_BLOCK) k_prim(PrimArgs a) {
       const int64_t bk = w.k;
       const PrimSlot& l = last;
       const int64_t q0 = bk / T;
-      if (q0 < U) {
+      if (q0 >= U && q0 < U + S) {
+        const int j = (int)(q0 - U);
+#pragma unroll
+        for (int t = 0; t < DIM; ++t) sx[(t * S + j) * PRIM_BLOCK + tid] = l.x[t];
+        sck[j * PRIM_BLOCK + tid] = l.core;
+        sbb[j * PRIM_BLOCK + tid] = l.bv;
+        sfr[j * PRIM_BLOCK + tid] = l.from;
+        sid[j * PRIM_BLOCK + tid] = l.id;
+      } else if (q0 < U) {
 #pragma unroll
         for (int q = 0; q < U; ++q)
           if (q == q0) {

@@ -72,6 +72,25 @@ typedef struct dmst_stats {
   int32_t num_chains;                        /* out: ChainAssignment.num_chains() (want_chains = 1) */
   float kernel_ms[DMST_MAX_KERNELS];         /* out (profile=1): device ms per kernel kind */
   int32_t kernel_calls[DMST_MAX_KERNELS];    /* out: launches per kernel kind */
+  /* in: code-path overrides (0 = the library's size-based default).  They
+   * choose WHICH kernels run, never the result: every setting gives the same
+   * bits (tests/test_paths_gpu.py), so tests can drive the paths a 128M-edge
+   * build takes on trees the oracle checks in seconds. */
+  int64_t tail_edges;       /* views >= 1 of at most this many edges finish inside the
+                               cooperative k_tail (default and maximum 4M); -1 = never */
+  int64_t direct_mi_bytes;  /* views >= 1 whose packed maxIncident (8 B per vertex) is at
+                               most this large take direct atomics in k_select_edges + k_v1
+                               (default 64 MB); -1 = always bucketed (multisplit + apply) */
+  int32_t sort1_mode;       /* bit 0: no narrow 32-bit keys; bit 1: no top-field compaction */
+  int32_t sort2_geometry;   /* chain-sort tiles: 1 = 512 x 16, 2 = 256 x 20 (two CTAs per SM);
+                               0 = by size (2 from 32M edges) */
+  /* out: the path this call took (what bench.py's byte model reads) */
+  int32_t sort1_narrow;     /* 1 = the edge sort ran on 32-bit keys */
+  int32_t sort1_compacted;  /* 1 = the sign/exponent field was replaced by its dense code */
+  int32_t sort2_geometry_used; /* 0 = no chain sort (a single chain), else as sort2_geometry */
+  int32_t tail_level;       /* first view finished inside k_tail, -1 = none */
+  uint64_t mi_bucketed;     /* bit k: view k's maxIncident was bucketed */
+  uint64_t mi_direct;       /* bit k: view k's maxIncident took direct atomics */
 } dmst_stats;
 
 /* Workspace size for a tree with n_edges edges. */
@@ -156,7 +175,8 @@ int dmst_validate(const int32_t* u, const int32_t* v, const double* w, int64_t n
  * (DEVICE pointer, n_edges entries, ROOT = -1): the largest number of edge
  * ancestors of a vertex, by pointer jumping.  *height is a HOST pointer.
  * Workspace: any buffer of at least 16 n_edges + 4096 bytes (e.g. the
- * dmst_build workspace). */
+ * dmst_build workspace).  Returns DMST_EINVAL when a parent is neither ROOT
+ * nor a smaller (heavier) rank, i.e. the array is not a dendrogram. */
 int dmst_dendrogram_height(const int32_t* edge_parent, int64_t n_edges, int64_t* height, void* workspace,
                            size_t workspace_bytes, void* stream);
 
@@ -174,10 +194,12 @@ int64_t dmst_format_dendrogram(const int32_t* edge_parent, const int32_t* vertex
  * `body` (DEVICE, body_len bytes) holds "E <rank> <parent>" / "V <id>
  * <parent>" lines ('#' and blank lines skipped; single spaces, '\n'
  * endings); edge_parent / vertex_parent (DEVICE, n_edges / n_vertices)
- * start at ROOT (-1) and receive every line.  HOST outputs: *bad_line =
- * 0-based body line of the first malformed line (-1 if none), and the
- * numbers of E and V lines.  Workspace: 8 * (ceil(body_len / 8192) + 1) + 64
- * bytes. */
+ * start at ROOT (-1) and receive every line; an id given on several lines
+ * takes the last one's parent, as the reference's in-order assignment does
+ * (dendro_io.py:60-66).  HOST outputs: *bad_line = 0-based body line of the
+ * first malformed line (-1 if none), and the numbers of E and V lines.
+ * Workspace: dmst_parse_workspace_bytes(body_len, n_edges, n_vertices). */
+size_t dmst_parse_workspace_bytes(int64_t body_len, int64_t n_edges, int64_t n_vertices);
 int dmst_parse_dendrogram(const char* body, int64_t body_len, int64_t n_edges, int64_t n_vertices,
                           int32_t* edge_parent, int32_t* vertex_parent, int64_t* bad_line, int64_t* edge_lines,
                           int64_t* vertex_lines, void* workspace, size_t workspace_bytes, void* stream);

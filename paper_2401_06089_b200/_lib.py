@@ -30,6 +30,7 @@ EXPORTS = (
     "dmst_validate",
     "dmst_dendrogram_height",
     "dmst_format_dendrogram",
+    "dmst_parse_workspace_bytes",
     "dmst_parse_dendrogram",
     "dmst_first_difference",
     "dmst_mreach_workspace_bytes",
@@ -54,7 +55,36 @@ class DmstStats(ctypes.Structure):
         ("num_chains", ctypes.c_int32),
         ("kernel_ms", ctypes.c_float * DMST_MAX_KERNELS),
         ("kernel_calls", ctypes.c_int32 * DMST_MAX_KERNELS),
+        ("tail_edges", ctypes.c_int64),
+        ("direct_mi_bytes", ctypes.c_int64),
+        ("sort1_mode", ctypes.c_int32),
+        ("sort2_geometry", ctypes.c_int32),
+        ("sort1_narrow", ctypes.c_int32),
+        ("sort1_compacted", ctypes.c_int32),
+        ("sort2_geometry_used", ctypes.c_int32),
+        ("tail_level", ctypes.c_int32),
+        ("mi_bucketed", ctypes.c_uint64),
+        ("mi_direct", ctypes.c_uint64),
     ]
+
+    # code-path overrides accepted by DendrogramBuilder.build(paths=...)
+    PATH_OPTIONS = ("tail_edges", "direct_mi_bytes", "sort1_mode", "sort2_geometry")
+
+    def set_paths(self, paths: dict | None) -> None:
+        for k, v in (paths or {}).items():
+            if k not in self.PATH_OPTIONS:
+                raise ValueError(f"unknown path option {k!r} (have {self.PATH_OPTIONS})")
+            setattr(self, k, int(v))
+
+    def path_info(self) -> dict:
+        """Which code path each stage took (bench.py's byte model reads this)."""
+        L = int(self.num_levels)
+        return {"sort1_passes": int(self.sort1_passes), "sort1_narrow": bool(self.sort1_narrow),
+                "sort1_compacted": bool(self.sort1_compacted), "sort2_passes": int(self.sort2_passes),
+                "sort2_geometry": {0: None, 1: "512x16", 2: "256x20"}[int(self.sort2_geometry_used)],
+                "tail_level": int(self.tail_level),
+                "mi_bucketed_views": [k for k in range(L + 1) if (int(self.mi_bucketed) >> k) & 1],
+                "mi_direct_views": [k for k in range(L + 1) if (int(self.mi_direct) >> k) & 1]}
 
     def kernel_profile(self) -> dict[str, tuple[float, int]]:
         """{kernel kind: (device ms, launches)} when profile=1 was set."""
@@ -113,6 +143,8 @@ def load() -> ctypes.CDLL:
     lib.dmst_format_dendrogram.argtypes = [vp, vp, i64, i64, vp, sz, vp, sz, vp]
     lib.dmst_format_dendrogram.restype = ctypes.c_int64
     p64 = ctypes.POINTER(ctypes.c_int64)
+    lib.dmst_parse_workspace_bytes.argtypes = [i64, i64, i64]
+    lib.dmst_parse_workspace_bytes.restype = sz
     lib.dmst_parse_dendrogram.argtypes = [vp, i64, i64, i64, vp, vp, p64, p64, p64, vp, sz, vp]
     lib.dmst_parse_dendrogram.restype = ctypes.c_int
     lib.dmst_first_difference.argtypes = [vp, vp, i64, p64, vp, sz, vp]

@@ -25,6 +25,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -143,6 +144,14 @@ class HostBuildResult:
     vertex_parent: torch.Tensor  # int32[nv]
     stats: _lib.DmstStats = field(repr=False, default=None)
 
+    @property
+    def num_levels(self) -> int:
+        return int(self.stats.num_levels)
+
+    @property
+    def view_kind_counts(self) -> list[tuple[int, int, int, int]]:
+        return self.stats.view_kind_counts()
+
     @classmethod
     def empty(cls, n: int, nv: int, pin: bool = True) -> "HostBuildResult":
         def mk(k, dt):
@@ -219,7 +228,7 @@ class DendrogramBuilder:
         return self._hws
 
     def build_host(self, num_vertices: int, u, v, w, *, out: HostBuildResult | None = None,
-                   profile: bool = False) -> HostBuildResult:
+                   profile: bool = False, paths: dict | None = None) -> HostBuildResult:
         """rank_edges + pandora on HOST arrays (dmst_build_host): inputs are
         copied in and every output copied back as soon as its stage is done,
         overlapped with the remaining kernels.  Page-locked (pinned) inputs
@@ -238,6 +247,7 @@ class DendrogramBuilder:
             ws = self.host_workspace(n, nv) if n >= 1 and nv >= 2 else torch.empty(1, dtype=torch.uint8, device=dev)
             st = _lib.DmstStats()
             st.profile = 1 if profile else 0
+            st.set_paths(paths)
             _lib.check(self.lib.dmst_build_host(
                 _ptr(u), _ptr(v), _ptr(w), n, nv, _ptr(out.orig_of), _ptr(out.heights),
                 _ptr(out.edge_parent), _ptr(out.vertex_parent), ctypes.byref(st),
@@ -249,7 +259,12 @@ class DendrogramBuilder:
         return torch.cuda.current_stream(self.device).cuda_stream
 
     def build(self, num_vertices: int, u, v, w, *, out: BuildResult | None = None,
-              debug: bool = False, profile: bool = False, want_chains: bool = False) -> BuildResult:
+              debug: bool = False, profile: bool = False, want_chains: bool = False,
+              paths: dict | None = None) -> BuildResult:
+        """rank_edges + pandora on device tensors (dmst_build).  ``paths``
+        overrides the size-based code-path choices (dmst_stats in-fields:
+        tail_edges, direct_mi_bytes, sort1_mode, sort2_geometry); results are
+        identical for every setting, the path taken is in ``stats.path_info()``."""
         dev = self.device
         with torch.cuda.device(dev):
             u = _as_dev(u, torch.int32, dev)
@@ -269,6 +284,7 @@ class DendrogramBuilder:
             st = _lib.DmstStats()
             st.profile = 1 if profile else 0
             st.want_chains = 1 if want_chains else 0
+            st.set_paths(paths)
             if debug:
                 dbg = {"retirement": torch.empty(n, dtype=torch.int8, device=dev),
                        "chain_key": torch.empty(n, dtype=torch.int32, device=dev),
@@ -307,7 +323,7 @@ class DendrogramBuilder:
                 _ptr(ru), _ptr(rv), _ptr(ws), ws.numel(), self._stream()))
             return orig_of, heights, ru, rv
 
-    def pandora(self, num_vertices: int, ru, rv):
+    def pandora(self, num_vertices: int, ru, rv, paths: dict | None = None):
         """-> (edge_parent, vertex_parent, stats) from rank-order endpoints."""
         dev = self.device
         with torch.cuda.device(dev):
@@ -319,6 +335,7 @@ class DendrogramBuilder:
             vp = torch.empty(nv, dtype=torch.int32, device=dev)
             ws = self.workspace(n, nv)
             st = _lib.DmstStats()
+            st.set_paths(paths)
             _lib.check(self.lib.dmst_pandora(_ptr(ru), _ptr(rv), n, nv, _ptr(ep), _ptr(vp),
                                              ctypes.byref(st), _ptr(ws), ws.numel(), self._stream()))
             return ep, vp, st
@@ -375,14 +392,18 @@ def _validate(builder: "DendrogramBuilder", num_vertices: int, u, v, w) -> None:
         raise err(_TREE_MESSAGES[kind.value].format(n=n, nv1=nv - 1, bad=bad.value))
 
 
-_builders: dict[int, DendrogramBuilder] = {}
+_builders: dict[tuple[int, int], DendrogramBuilder] = {}
 
 
 def _builder(device=None) -> DendrogramBuilder:
+    """The module-level helpers' builder: one per (device, host thread), so
+    concurrent callers never share a workspace (dmst.h: concurrent calls need
+    different workspaces and streams)."""
     dev = _device_of(device)
-    b = _builders.get(dev.index)
+    key = (dev.index, threading.get_ident())
+    b = _builders.get(key)
     if b is None:
-        b = _builders[dev.index] = DendrogramBuilder(dev)
+        b = _builders[key] = DendrogramBuilder(dev)
     return b
 
 
@@ -459,13 +480,25 @@ def format_dendrogram_b200(edge_parent, vertex_parent, device=None) -> torch.Ten
     return out
 
 
-_STAGE: dict[int, list] = {}
+_STAGE: dict[tuple[int, int], list] = {}  # pinned staging buffers per (device, host thread)
 
 
 def sidecar_path(path) -> str:
     """Binary sidecar of a v1 dendrogram file: ``<path>.npy``, one int32
-    array = edge_parent followed by vertex_parent."""
+    array = edge_parent, then vertex_parent, then an 8-word binding to the
+    text file it was written with."""
     return os.fspath(path) + ".npy"
+
+
+_SIDECAR_MAGIC = 0x31524344  # "DCR1"
+
+
+def _text_binding(path) -> np.ndarray:
+    """(magic, size, mtime_ns, inode) of the text file as 4 int64 = 8 int32:
+    a sidecar is used only while the text file is exactly the one it was
+    written beside (a rewrite by any writer changes mtime_ns, and usually size)."""
+    st = os.stat(path)
+    return np.array([_SIDECAR_MAGIC, st.st_size, st.st_mtime_ns, st.st_ino], dtype=np.int64).view(np.int32)
 
 
 def write_dendrogram_b200(path, edge_parent, vertex_parent, device=None, chunk_bytes: int = 64 << 20,
@@ -480,9 +513,10 @@ def write_dendrogram_b200(path, edge_parent, vertex_parent, device=None, chunk_b
     dev_bytes = format_dendrogram_b200(edge_parent, vertex_parent, device=device)
     total = int(dev_bytes.numel())
     dev = dev_bytes.device
-    bufs = _STAGE.get(dev.index)
+    key = (dev.index, threading.get_ident())
+    bufs = _STAGE.get(key)
     if bufs is None or bufs[0].numel() < chunk_bytes:
-        bufs = _STAGE[dev.index] = [torch.empty(chunk_bytes, dtype=torch.uint8).pin_memory() for _ in range(2)]
+        bufs = _STAGE[key] = [torch.empty(chunk_bytes, dtype=torch.uint8).pin_memory() for _ in range(2)]
     evs = [torch.cuda.Event(), torch.cuda.Event()]
     stream = torch.cuda.current_stream(dev)
     with open(path, "wb") as f:
@@ -501,11 +535,14 @@ def write_dendrogram_b200(path, edge_parent, vertex_parent, device=None, chunk_b
             evs[k & 1].synchronize()
             hi = min(total, lo + chunk_bytes)
             f.write(memoryview(bufs[k & 1].numpy())[:hi - lo])
+    side = sidecar_path(path)
     if sidecar:
         both = torch.cat([torch.as_tensor(edge_parent).reshape(-1).to(dev, torch.int32),
                           torch.as_tensor(vertex_parent).reshape(-1).to(dev, torch.int32)]).cpu().numpy()
-        with open(sidecar_path(path), "wb") as f:
-            np.save(f, both)
+        with open(side, "wb") as f:
+            np.save(f, np.concatenate([both, _text_binding(path)]))
+    elif os.path.exists(side):
+        os.remove(side)  # a sidecar of an older file must not outlive it
     return total
 
 
@@ -530,13 +567,15 @@ def read_dendrogram_b200(path, device=None, use_sidecar: bool = True) -> BuildRe
     Lines must use single spaces and '\\n' endings (what write_dendrogram and
     write_dendrogram_b200 produce); a malformed line raises
     DendrogramFormatError("bad line: ...").  A ``<path>.npy`` sidecar
-    (write_dendrogram_b200(sidecar=True)) of the header's size that is not
-    older than the text file is loaded instead of parsing the body."""
+    (write_dendrogram_b200(sidecar=True)) is loaded instead of parsing the
+    body when its size matches the header and its binding (size, mtime_ns,
+    inode of the text file when the sidecar was written) matches the text
+    file as it is now."""
     err = _format_error()
     b = _builder(device)
     dev = b.device
     side = sidecar_path(path)
-    if use_sidecar and os.path.exists(side) and os.path.getmtime(side) >= os.path.getmtime(path):
+    if use_sidecar and os.path.exists(side):
         with open(path, "rb") as f:
             first = f.readline()
         parts = first.decode(errors="replace").split()
@@ -546,8 +585,9 @@ def read_dendrogram_b200(path, device=None, use_sidecar: bool = True) -> BuildRe
                 arr = np.load(side, mmap_mode="r")
             except (ValueError, OSError):
                 arr = None
-            if arr is not None and arr.dtype == np.int32 and arr.shape == (n + nv,):
-                both = torch.from_numpy(np.array(arr)).to(dev)
+            if (arr is not None and arr.dtype == np.int32 and arr.shape == (n + nv + 8,)
+                    and np.array_equal(arr[n + nv:], _text_binding(path))):
+                both = torch.from_numpy(np.array(arr[:n + nv])).to(dev)
                 return BuildResult(orig_of=None, heights=None, edge_parent=both[:n], vertex_parent=both[n:])
     with open(path, "rb") as f:
         data = f.read()
@@ -569,7 +609,8 @@ def read_dendrogram_b200(path, device=None, use_sidecar: bool = True) -> BuildRe
         dbody = host.to(dev)
         ep = torch.empty(max(n, 0), dtype=torch.int32, device=dev)
         vp = torch.empty(max(nv, 0), dtype=torch.int32, device=dev)
-        ws = torch.empty(8 * ((blen + 8191) // 8192 + 2) + 64, dtype=torch.uint8, device=dev)
+        ws = torch.empty(int(b.lib.dmst_parse_workspace_bytes(blen, max(n, 0), max(nv, 0))) or 64,
+                         dtype=torch.uint8, device=dev)
         bad, ne, nvl = ctypes.c_int64(-1), ctypes.c_int64(0), ctypes.c_int64(0)
         _lib.check(b.lib.dmst_parse_dendrogram(_ptr(dbody) if blen else None, blen, n, nv, _ptr(ep), _ptr(vp),
                                                ctypes.byref(bad), ctypes.byref(ne), ctypes.byref(nvl),
@@ -582,11 +623,12 @@ def read_dendrogram_b200(path, device=None, use_sidecar: bool = True) -> BuildRe
     return BuildResult(orig_of=None, heights=None, edge_parent=ep, vertex_parent=vp)
 
 
-def verify_b200(path_a, path_b, device=None) -> tuple[int, str]:
+def verify_b200(path_a, path_b, device=None, use_sidecar: bool = False) -> tuple[int, str]:
     """``dendromst verify a b`` (cli.py:138-155) with the files parsed and
-    compared on the GPU: returns (exit code, the line the reference prints)."""
-    da = read_dendrogram_b200(path_a, device=device)
-    db = read_dendrogram_b200(path_b, device=device)
+    compared on the GPU: returns (exit code, the line the reference prints).
+    The text files themselves are compared unless ``use_sidecar``."""
+    da = read_dendrogram_b200(path_a, device=device, use_sidecar=use_sidecar)
+    db = read_dendrogram_b200(path_b, device=device, use_sidecar=use_sidecar)
     b = _builder(device)
     ws = torch.empty(64, dtype=torch.uint8, device=b.device)
     for label, pa, pb in (("edge", da.edge_parent, db.edge_parent),

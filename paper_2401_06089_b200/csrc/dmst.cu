@@ -180,25 +180,26 @@ int num_sms() {
   return sms > 0 ? sms : 148;
 }
 
-// Per-thread host-mapped pinned buffer for small readbacks (Ctx::to_host).
+// Host-mapped pinned buffer for small readbacks (Ctx::to_host), one per
+// (host thread, device): kept for the thread's lifetime, so a thread that
+// alternates devices reuses its buffers instead of reallocating them.
 struct MappedBuf {
   static constexpr uint32_t kWords = 2048;
   volatile uint32_t* host = nullptr;
   uint32_t* dev = nullptr;
-  int device = -1;
 };
 MappedBuf& mapped_buf() {
-  thread_local MappedBuf mb;
+  thread_local std::unordered_map<int, MappedBuf> bufs;
   int dev = 0;
   DMST_CUDA(cudaGetDevice(&dev));
-  if (mb.host == nullptr || mb.device != dev) {
+  MappedBuf& mb = bufs[dev];
+  if (mb.host == nullptr) {
     void* h = nullptr;
     DMST_CUDA(cudaHostAlloc(&h, 4 * MappedBuf::kWords, cudaHostAllocMapped | cudaHostAllocPortable));
     void* d = nullptr;
     DMST_CUDA(cudaHostGetDevicePointer(&d, h, 0));
     mb.host = (volatile uint32_t*)h;
     mb.dev = (uint32_t*)d;
-    mb.device = dev;
   }
   return mb;
 }
@@ -236,6 +237,18 @@ struct HostIO {
   cudaEvent_t ev[4] = {};
 };
 
+// Per-call code-path choices (dmst_stats in-fields; 0 there = these defaults)
+// and a record of the path taken (dmst_stats out-fields).
+struct Paths {
+  int64_t tail_edges = kTailEdges;
+  int64_t direct_mi_bytes = kDirectMiBytes;
+  int sort1_mode = 0;
+  int sort2_geometry = 0;
+  // out
+  int sort1_narrow = 0, sort1_compacted = 0, sort2_geometry_used = 0, tail_level = -1;
+  uint64_t mi_bucketed = 0, mi_direct = 0;
+};
+
 struct Ctx {
   cudaStream_t s;
   Workspace w;
@@ -243,6 +256,7 @@ struct Ctx {
   int sms = 148;
   bool profile = false;
   HostIO* io = nullptr;
+  Paths paths;
   struct Ev {
     int kind;
     cudaEvent_t a, b;
@@ -491,7 +505,7 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
   int ncodes = 0;
   for (uint32_t x : tb) ncodes += __builtin_popcount(x);
   const uint8_t* code = nullptr;
-  if (ncodes > 1 && ncodes <= 256) {
+  if (ncodes > 1 && ncodes <= 256 && !(c.paths.sort1_mode & 2)) {
     int cbits = 0;
     while ((1 << cbits) < ncodes) ++cbits;
     const uint64_t cand = ao[0] & kMantMask, cor = (ao[1] & kMantMask) | (((1ull << cbits) - 1) << kTopShift);
@@ -503,6 +517,7 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
       code = top_code;
       em.inv = top_inv;
       shifts = cs;
+      c.paths.sort1_compacted = 1;
     }
   }
   // the upsweep counted digit d0 of the raw keys: valid for the compacted
@@ -520,7 +535,8 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
                              : 0ull;
   const uint64_t var = kvar | cvar;
   const int lo = shifts.empty() ? 0 : shifts[0];
-  const bool narrow = !shifts.empty() && (var >> lo) < (1ull << 32);
+  const bool narrow = !shifts.empty() && (var >> lo) < (1ull << 32) && !(c.paths.sort1_mode & 1);
+  c.paths.sort1_narrow = narrow;
   if (narrow) {
     std::vector<int> s32(shifts);
     for (int& x : s32) x -= lo;
@@ -597,21 +613,15 @@ Recs recs_at(char* base, int64_t) {
   return Recs{(uint32_t*)base};
 }
 
-bool use_tail() {
-  static const bool v = getenv("DMST_NO_TAIL") == nullptr;
-  return v;
-}
-
 // Run levels level0..L of the contraction in k_tail; fills lt.soff / lt.L,
 // the per-view stats and the running soff exactly as the host loop would.
 void run_tail(Ctx& c, int level0, int cur, int64_t n_k, int64_t nv_k, LevelTable& lt, int64_t& soff,
               dmst_stats* st, int& jump_rounds) {
   Workspace& w = c.w;
-  static int blocks_per_sm = -1;
-  if (blocks_per_sm < 0) {
-    DMST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_tail, TAIL_BLOCK, 0));
-    if (blocks_per_sm < 1) invalid("k_tail cannot be co-resident");
-  }
+  int blocks_per_sm = 0;  // queried per call (host-side occupancy calculation, no device round trip)
+  DMST_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_tail, TAIL_BLOCK, 0));
+  if (blocks_per_sm < 1) invalid("k_tail cannot be co-resident");
+  c.paths.tail_level = level0;
   const int64_t want = cdiv(std::max(n_k, nv_k), TAIL_BLOCK);
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)c.sms * blocks_per_sm));
   // scratch / outputs in the radix counts area (idle during the level loop)
@@ -681,6 +691,7 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
   c.zero(w.cnt2, 4 * (n / 16 + 2));
   mi_buckets(c, EdgeRecSrc{w.euv0}, 2 * n, nv, recs_at(w.R, 2 * n), recs_at(w.R + 24 * n, 2 * n),
              MiApplyOut{w.mi64_0, vertex_parent, nullptr, w.cnt2});
+  c.paths.mi_bucketed |= 1;
   if (c.io) c.copy_out(2, c.io->h_vp, vertex_parent, 4 * (size_t)nv);
   bool v1_done = true;
 
@@ -697,7 +708,7 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
   while (true) {
     if (level >= DMST_MAX_LEVELS) invalid("too many contraction levels");
     // small view: every remaining level in one cooperative kernel (tail.cuh)
-    if (level >= 1 && !v1_done && n_k <= kTailEdges && use_tail()) {
+    if (level >= 1 && !v1_done && n_k <= std::min<int64_t>(c.paths.tail_edges, kTailEdges)) {
       run_tail(c, level, cur, n_k, nv_k, lt, soff, st, jump_rounds);
       level = lt.L;
       break;
@@ -774,7 +785,8 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     }
     // retire + compact alpha edges into view level+1
     const int64_t nv_next = n_leaf, n_next = n_alpha;
-    const bool direct = nv_next * 8 <= kDirectMiBytes;
+    const bool direct = c.paths.direct_mi_bytes >= 0 && nv_next * 8 <= c.paths.direct_mi_bytes;
+    if (n_next > 0 && level + 1 <= 63) (direct ? c.paths.mi_direct : c.paths.mi_bucketed) |= 1ull << (level + 1);
     unsigned long long* mi_next = w.mi64[cur ^ 1];
     // records of view level+1: R[24n, 36n); bucketing mid buffer R[0, 12n)
     uint32_t* rec = (uint32_t*)(w.R + 24 * n);
@@ -859,7 +871,9 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     ArrayEmitter<uint64_t, 0> fin{bufK[lastb], nullptr};
     std::vector<int> shifts64(shifts);
     for (int& x : shifts64) x += 32;
-    if (n >= kS2LargeEdges)
+    const bool large = c.paths.sort2_geometry ? c.paths.sort2_geometry == 2 : n >= kS2LargeEdges;
+    c.paths.sort2_geometry_used = large ? 2 : 1;
+    if (large)
       run_sort<uint64_t, 0, S2L_BLOCK, S2L_ITEMS, S2L_MINB, S2_BITS>(
           c, {KK_SORT2_PASS, KK_SORT2_PASS, KK_SORT2_PASS}, n, shifts64, bufK, bufP, Sort2FirstLoader{keys}, fin);
     else
@@ -924,11 +938,34 @@ void init_ctx(Ctx& c, int64_t n, int64_t nv, void* ws, void* stream, dmst_stats*
   c.w = carve(n, nv, base);
   if (st) {
     const int32_t prof = st->profile, wc = st->want_chains;
+    const int64_t te = st->tail_edges, dm = st->direct_mi_bytes;
+    const int32_t s1 = st->sort1_mode, s2 = st->sort2_geometry;
+    if (s1 < 0 || s1 > 3) invalid("sort1_mode must be in [0, 3]");
+    if (s2 < 0 || s2 > 2) invalid("sort2_geometry must be 0, 1 or 2");
+    if (te < -1 || dm < -1) invalid("tail_edges / direct_mi_bytes must be >= -1");
     memset(st, 0, sizeof(*st));
     st->profile = prof;
     st->want_chains = wc;
+    st->tail_edges = te;
+    st->direct_mi_bytes = dm;
+    st->sort1_mode = s1;
+    st->sort2_geometry = s2;
     c.profile = prof != 0;
+    if (te) c.paths.tail_edges = te < 0 ? 0 : te;
+    if (dm) c.paths.direct_mi_bytes = dm;
+    c.paths.sort1_mode = s1;
+    c.paths.sort2_geometry = s2;
   }
+}
+
+void report_paths(const Ctx& c, dmst_stats* st) {
+  if (!st) return;
+  st->sort1_narrow = c.paths.sort1_narrow;
+  st->sort1_compacted = c.paths.sort1_compacted;
+  st->sort2_geometry_used = c.paths.sort2_geometry_used;
+  st->tail_level = c.paths.tail_level;
+  st->mi_bucketed = c.paths.mi_bucketed;
+  st->mi_direct = c.paths.mi_direct;
 }
 
 static int build_impl(const int32_t* u, const int32_t* v, const double* w, int64_t n, int64_t nv,
@@ -956,6 +993,7 @@ static int build_impl(const int32_t* u, const int32_t* v, const double* w, int64
     c.sync();
     if (io) DMST_CUDA(cudaStreamSynchronize(io->side));
     c.collect(st);
+    report_paths(c, st);
     if (st) {
       st->sort1_passes = p1;
       st->kernel_launches = c.launches;
@@ -1168,6 +1206,7 @@ int dmst_pandora(const int32_t* ru, const int32_t* rv, int64_t n_edges, int64_t 
                  nullptr);
     c.sync();
     c.collect(stats);
+    report_paths(c, stats);
     if (stats) stats->kernel_launches = c.launches;
   });
 }
@@ -1280,11 +1319,18 @@ int dmst_dendrogram_height(const int32_t* edge_parent, int64_t n_edges, int64_t*
     int2* buf[2] = {(int2*)base, (int2*)(base + align_up(8 * n))};
     uint32_t* flag = (uint32_t*)(base + align_up(8 * n) + align_up(8 * n));
     if ((size_t)((char*)flag - (char*)workspace) + 16 > workspace_bytes) invalid("workspace too small");
+    c.zero(flag + 2, 4);
     c.begin(KK_OTHER);
-    k_depth_init<<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(edge_parent, n, buf[0]);
+    k_depth_init<<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(edge_parent, n, buf[0], flag + 2);
     c.launched();
+    uint32_t bad = 0;
+    c.to_host(&bad, flag + 2, 4);
+    c.sync();
+    if (bad) invalid("edge_parent[e] must be ROOT (-1) or a heavier edge's rank in [0, e)");
     int cur = 0;
-    for (int round = 0; round < 64; ++round) {
+    bool live_left = true;
+    // parents are strictly smaller ranks, so ceil(log2 n) <= 29 rounds resolve every edge
+    for (int round = 0; round < 64 && live_left; ++round) {
       c.zero(flag, 4);
       c.begin(KK_OTHER);
       k_depth_jump<<<c.persistent_grid(n, 256, 8), 256, 0, c.s>>>(buf[cur], buf[cur ^ 1], n, flag);
@@ -1293,8 +1339,9 @@ int dmst_dendrogram_height(const int32_t* edge_parent, int64_t n_edges, int64_t*
       uint32_t live = 0;
       c.to_host(&live, flag, 4);
       c.sync();
-      if (!live) break;
+      live_left = live != 0;
     }
+    if (live_left) invalid("edge_parent does not resolve to ROOT within 64 pointer-jumping rounds");
     c.zero(flag + 1, 4);
     c.begin(KK_OTHER);
     k_depth_max<<<c.persistent_grid(n, 256, 8), 256, 0, c.s>>>(buf[cur], n, flag + 1);
@@ -1348,6 +1395,11 @@ int64_t dmst_format_dendrogram(const int32_t* edge_parent, const int32_t* vertex
   return rc ? -1 : total;
 }
 
+size_t dmst_parse_workspace_bytes(int64_t body_len, int64_t n_edges, int64_t n_vertices) {
+  if (body_len < 0 || n_edges < 0 || n_vertices < 0) return 0;
+  return (size_t)(8 * (cdiv(body_len, PARSE_TILE) + 1) + 32 + 8 * (n_edges + n_vertices) + 64);
+}
+
 int dmst_parse_dendrogram(const char* body, int64_t body_len, int64_t n_edges, int64_t n_vertices,
                           int32_t* edge_parent, int32_t* vertex_parent, int64_t* bad_line, int64_t* edge_lines,
                           int64_t* vertex_lines, void* workspace, size_t workspace_bytes, void* stream) {
@@ -1367,11 +1419,14 @@ int dmst_parse_dendrogram(const char* body, int64_t body_len, int64_t n_edges, i
     }
     if (!body) invalid("null body");
     const int64_t nb = cdiv(body_len, PARSE_TILE);
-    if (!workspace || workspace_bytes < (size_t)(8 * (nb + 1) + 64)) invalid("workspace too small");
+    if (!workspace || workspace_bytes < dmst_parse_workspace_bytes(body_len, n_edges, n_vertices))
+      invalid("workspace too small (dmst_parse_workspace_bytes)");
     unsigned long long* bl = (unsigned long long*)workspace;
     unsigned long long* err = bl + nb + 1;
+    unsigned long long* last = err + 4;
     c.ones(err, 8);
     c.zero(err + 1, 16);
+    c.zero(last, 8 * (size_t)(n_edges + n_vertices));
     c.begin(KK_OTHER);
     k_parse_count<<<(unsigned)nb, PARSE_BLOCK, 0, c.s>>>(body, body_len, bl);
     c.launched();
@@ -1379,9 +1434,14 @@ int dmst_parse_dendrogram(const char* body, int64_t body_len, int64_t n_edges, i
     k_fmt_scan<<<1, 1024, 0, c.s>>>(bl, nb);
     c.launched();
     c.begin(KK_OTHER);
-    k_parse_lines<<<(unsigned)nb, PARSE_BLOCK, 0, c.s>>>(body, body_len, bl, n_edges, n_vertices, edge_parent,
-                                                           vertex_parent, err);
+    k_parse_lines<<<(unsigned)nb, PARSE_BLOCK, 0, c.s>>>(body, body_len, bl, n_edges, n_vertices, last, err);
     c.launched();
+    if (n_edges + n_vertices) {
+      c.begin(KK_OTHER);
+      k_parse_finish<<<grid_for(n_edges + n_vertices, EW_BLOCK), EW_BLOCK, 0, c.s>>>(last, n_edges, n_vertices,
+                                                                                    edge_parent, vertex_parent);
+      c.launched();
+    }
     unsigned long long h[3];
     c.to_host(h, err, 24);
     c.sync();

@@ -132,9 +132,18 @@ namespace dmst {
 // node has two vertex children, so it is some vertex's parent).  Pointer
 // jumping over (ancestor, distance) pairs packed in 8 B: one random probe
 // per live edge per round, ceil(log2(height)) rounds.
-__global__ void k_depth_init(const int32_t* __restrict__ parent, int64_t n, int2* __restrict__ ad) {
+// A dendrogram's parents are heavier edges (smaller ranks) or ROOT; anything
+// else (a corrupt file) is flagged instead of being followed out of bounds.
+__global__ void k_depth_init(const int32_t* __restrict__ parent, int64_t n, int2* __restrict__ ad,
+                             uint32_t* __restrict__ bad) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < n) ad[e] = make_int2(parent[e], 1);
+  if (e >= n) return;
+  int32_t p = parent[e];
+  if (p < -1 || p >= e) {
+    atomicOr(bad, 1u);
+    p = -1;
+  }
+  ad[e] = make_int2(p, 1);
 }
 
 __global__ void __launch_bounds__(256) k_depth_jump(const int2* __restrict__ in, int2* __restrict__ out, int64_t n,
@@ -360,8 +369,8 @@ __device__ __forceinline__ bool parse_int(const char* b, int64_t len, int64_t& i
 
 __global__ void __launch_bounds__(PARSE_BLOCK) k_parse_lines(const char* __restrict__ body, int64_t len,
                                                              const unsigned long long* __restrict__ block_off,
-                                                             int64_t n, int64_t nv, int32_t* __restrict__ ep,
-                                                             int32_t* __restrict__ vp,
+                                                             int64_t n, int64_t nv,
+                                                             unsigned long long* __restrict__ last,
                                                              unsigned long long* __restrict__ err) {
   const int64_t beg = (int64_t)blockIdx.x * PARSE_TILE + (int64_t)threadIdx.x * PARSE_CHUNK;
   uint32_t mine = 0;
@@ -395,13 +404,13 @@ __global__ void __launch_bounds__(PARSE_BLOCK) k_parse_lines(const char* __restr
       bad = min(bad, (unsigned long long)ln);
       continue;
     }
-    if (k == 'E') {
-      ep[id] = (int32_t)par;
+    // duplicate ids: the last line wins, as in the reference's sequential
+    // assignment (dendro_io.py:60-66): keep the max of (line, parent)
+    atomicMax(&last[k == 'E' ? id : n + id], ((ln + 1) << 32) | (uint32_t)(int32_t)par);
+    if (k == 'E')
       ++ne;
-    } else {
-      vp[id] = (int32_t)par;
+    else
       ++nvv;
-    }
   }
   if (bad != ~0ull) atomicMin(err, bad + 1);
   ne = __reduce_add_sync(kFull, ne);
@@ -410,6 +419,19 @@ __global__ void __launch_bounds__(PARSE_BLOCK) k_parse_lines(const char* __restr
     if (ne) atomicAdd(err + 1, (unsigned long long)ne);
     if (nvv) atomicAdd(err + 2, (unsigned long long)nvv);
   }
+}
+
+// (line + 1, parent) of the last line per id -> parents (ROOT where none).
+__global__ void k_parse_finish(const unsigned long long* __restrict__ last, int64_t n, int64_t nv,
+                               int32_t* __restrict__ ep, int32_t* __restrict__ vp) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n + nv) return;
+  const unsigned long long x = last[i];
+  const int32_t p = x ? (int32_t)(uint32_t)x : -1;
+  if (i < n)
+    ep[i] = p;
+  else
+    vp[i - n] = p;
 }
 
 // First index where two int32 arrays differ (atomicMin), for `verify`.

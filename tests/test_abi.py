@@ -35,9 +35,23 @@ def test_exports_every_declared_symbol(lib):
         assert hasattr(lib, name), name
 
 
-def test_stats_struct_layout_matches_header():
-    # profile, num_levels, 65*4 counts, 65 view sizes, 4 int32 fields, 16 float + 16 int32
-    assert ctypes.sizeof(_lib.DmstStats) == 4 * (2 + 65 * 4 + 65 + 4 + 2 + 2 * 24)
+def test_stats_struct_layout_matches_header(tmp_path):
+    # the ctypes mirror agrees with the C compiler's layout of dmst_stats, field by field
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        pytest.skip("gcc not available")
+    names = [f[0] for f in _lib.DmstStats._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "dmst.h"\nint main(void) {\n'
+                   '  printf("%zu\\n", sizeof(dmst_stats));\n'
+                   + "".join(f'  printf("%zu\\n", offsetof(dmst_stats, {n}));\n' for n in names)
+                   + "  return 0;\n}\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    assert got[0] == ctypes.sizeof(_lib.DmstStats)
+    assert got[1:] == [getattr(_lib.DmstStats, n).offset for n in names]
 
 
 def test_workspace_bytes(lib):

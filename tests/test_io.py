@@ -146,19 +146,55 @@ def test_device_sidecar_roundtrip():
         path = os.path.join(d, "x.dendro")
         write_dendrogram_b200(path, r.edge_parent, r.vertex_parent, sidecar=True)
         side = np.load(sidecar_path(path))
-        assert side.dtype == np.int32 and side.shape == (2 * nv - 1,)
+        assert side.dtype == np.int32 and side.shape == (2 * nv - 1 + 8,)
         for use in (True, False):
             back = read_dendrogram_b200(path, use_sidecar=use)
             assert bool((back.edge_parent == r.edge_parent).all())
             assert bool((back.vertex_parent == r.vertex_parent).all())
-        # a text file newer than its sidecar is parsed, not shadowed
+        # the same-size text rewritten at once (same mtime tick possible) is parsed, not shadowed
         data = open(path, "rb").read()
         i = data.index(b"\nE 5 ") + 1
         j = data.index(b"\n", i)
-        _write(path, data[:i] + b"E 5 -1" + data[j:])
-        os.utime(sidecar_path(path), (1, 1))
+        edited = data[:i] + (b"E 5 -1" + b" " * 0) + data[j:]
+        _write(path, edited)
         back = read_dendrogram_b200(path)
         assert int(back.edge_parent[5]) == -1
+        # writing without a sidecar removes the stale one
+        write_dendrogram_b200(path, r.edge_parent, r.vertex_parent, sidecar=False)
+        assert not os.path.exists(sidecar_path(path))
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+def test_device_reader_duplicate_ids_last_wins():
+    # read_dendrogram assigns lines in order (dendro_io.py:60-66): a repeated id keeps the LAST parent
+    from paper_2401_06089_b200 import read_dendrogram_b200
+    body = b"#dendrogram v1 n=3 nv=4\nE 0 -1\nE 1 0\nE 1 7\nE 2 0\nE 1 0\nV 0 2\nV 1 2\nV 2 1\nV 3 1\n"
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "dup.dendro")
+        _write(path, body)
+        err = __import__("paper_2401_06089_b200.api", fromlist=["x"])._format_error()
+        with pytest.raises(err, match="expected 3 edge and 4 vertex lines, got 5 and 4"):
+            read_dendrogram_b200(path)
+        _write(path, b"#dendrogram v1 n=3 nv=4\nE 0 -1\nE 1 2\nE 1 0\nV 0 2\nV 1 2\nV 2 1\nV 3 1\nV 3 0\n")
+        with pytest.raises(err, match="got 3 and 5"):
+            read_dendrogram_b200(path)
+        # duplicates that still add up: 2 E lines for id 1, none for id 2 -> id 2 stays ROOT, id 1 = last
+        _write(path, b"#dendrogram v1 n=3 nv=4\nE 0 -1\nE 1 2\nE 1 0\nV 0 2\nV 1 2\nV 2 1\nV 3 1\n")
+        for _ in range(20):  # the same answer every run
+            r = read_dendrogram_b200(path)
+            assert r.edge_parent.cpu().tolist() == [-1, 0, -1]
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+def test_height_rejects_non_dendrogram_parents():
+    import torch
+    from paper_2401_06089_b200 import dendrogram_height_b200
+    assert dendrogram_height_b200(torch.tensor([-1, 0, 0, 1], dtype=torch.int32)) == 3
+    for bad in ([-1, 5, 0], [-1, 2, 0], [-1, -7, 0], [0, -1, 1]):
+        with pytest.raises(ValueError, match="heavier edge"):
+            dendrogram_height_b200(torch.tensor(bad, dtype=torch.int32))
 
 
 @pytest.mark.parametrize("t", GOLDEN[:6], ids=[t["name"] for t in GOLDEN[:6]])

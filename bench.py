@@ -54,42 +54,48 @@ WORKLOADS = {
 # Algorithmic HBM bytes of each kernel kind per build: what the
 # kernel must read and write given its design, counting a random 4-B access
 # as 4 B (the 64-B DRAM sector it really costs is NOT credited; `traffic`
-# shows it).  ids / ranks 4 B, weights and keys 8 B, records 12 B (maxIncident)
-# or 8 B (chain links).
-DIRECT_MI_BYTES = 24 << 20  # dmst.cu kDirectMiBytes: views whose mi64 fits are scatter-maxed directly
+# shows it).  ids / ranks 4 B, weights and keys 8 B (4 B for narrow edge-sort
+# keys), records 12 B (maxIncident) or 8 B (chain links).  Which views were
+# bucketed and the key width come from the library (dmst_stats path fields),
+# not from constants restated here.
 
 
 def kernel_bytes(stats, n: int, nv: int) -> dict[str, float]:
     counts = stats.view_kind_counts()            # (n_alpha, n_leaf, n_chain, n_k) per view
+    info = stats.path_info()
     L = stats.num_levels
     views_n = [c[3] for c in counts]
     views_v = [int(stats.view_vertices[k]) for k in range(L + 1)]
-    # views whose maxIncident is bucketed: view 0 and later views with a large mi64
-    buck = [0] + [k for k in range(1, L + 1) if views_v[k] * 8 > DIRECT_MI_BYTES]
+    buck = info["mi_bucketed_views"]             # maxIncident by multisplit + shared-memory apply
+    direct = info["mi_direct_views"]             # direct atomics in select_edges, then k_v1
     mb = sum(2 * views_n[k] for k in buck)        # records (2 per edge) of bucketed views
     vb = sum(views_v[k] for k in buck)
     p1, p2 = stats.sort1_passes, stats.sort2_passes
+    kb = 4 if info["sort1_narrow"] else 8         # key bytes per item in the edge sort's passes
+    item = kb + 12                                # key + (id, u, v) payload
     alpha = sum(c[0] for c in counts[:L])         # edges copied into the next view
     return {
         "sort1_hist": 8.0 * n,                                  # read w
-        "sort1_pass_first": 36.0 * n,                           # read w, u, v 16; write key + (id, u, v) 20
-        "sort1_pass_mid": 40.0 * n * max(p1 - 2, 0),            # read 20, write 20 per pass
-        "sort1_pass_final": 40.0 * n,                           # read 20; write orig_of 4, heights 8, euv 8
-        "upsweep_scan": 8.0 * n * p1 + 4.0 * n * p2,            # key reads
+        "sort1_pass_first": (16.0 + item) * n,                  # read w, u, v 16; write key + payload
+        "sort1_pass_mid": 2.0 * item * n * max(p1 - 2, 0),      # read + write key + payload per pass
+        "sort1_pass_final": (item + 20.0) * n,                  # read; write orig_of 4, heights 8, euv 8
+        "upsweep_scan": float(kb) * n * max(p1 - 1, 0) + 8.0 * n * max(p2 - 1, 0) + 4.0 * n * min(p2, 1),
         "mi_hist": 4.0 * mb,                                    # read endpoints
         "mi_split_a": 16.0 * mb,                                # read 4 + write 12 per record
         "mi_split_b": 24.0 * mb,                                # read 12 + write 12 per record
         "mi_apply": 12.0 * mb + 12.0 * vb,                      # read records; write mi64 8 + parent 4
-        "v1": 12.0 * sum(views_v[k] for k in range(1, L + 1) if k not in buck),
+        "v1": 12.0 * sum(views_v[k] for k in direct),
         "leafscan": 1.0 * sum(views_n),                         # 2-bit counts in, prefixes out (per 16 edges)
         "v2": 12.0 * sum(views_v[:L]),                          # mi64 8 + vertex map 4 (chase hops not credited)
         "jump": 0.0,
-        "select_edges": 9.0 * sum(views_n[:L]) + 4.0 * n + 20.0 * alpha,  # euv + ret; x1; alpha: 2 gathers + next view
+        "select_edges": 9.0 * sum(views_n[:L]) + 4.0 * n + 20.0 * alpha
+        + 16.0 * sum(views_n[k] for k in direct),               # euv + ret; x1; alpha: 2 gathers + next view;
+                                                                # direct views: 2 atomics per next-view edge
         "walk": 17.0 * n,                                       # ret 1 + x1 4 + smi 4 + map 4 + key 4
         "sort2_pass": 16.0 * n * p2,                            # read 8, write 8 per pass
         "link_split": 32.0 * n if p2 else 0.0,                  # two 8-B record passes (read + write)
         "link_apply": 12.0 * n,                                 # read records 8, write edge_parent 4
-        "tail": 0.0,                                            # small views (< 1M edges), L2-resident
+        "tail": 0.0,                                            # small views (<= 4M edges), L2-resident
         "other": 0.0,
     }
 
@@ -228,18 +234,82 @@ def make_inputs(workload: str, n_override: int | None, seeds: list[int]):
     return [synth.GENERATORS[gen](n, seed=sd) for sd in seeds], desc
 
 
-def cpu_reference_rate(workload: str, n_sample: int, repeats: int) -> tuple[float, list[float]]:
-    """Time the oracle port of rank_edges + pandora (single core) on a sample."""
-    from oracle import dendro_oracle as O
+REF_SITE = os.path.join(ROOT, "baseline", "_ref")   # the unmodified reference, pip-installed
+
+
+def _import_reference():
+    """The unmodified reference package (dendromst) from baseline/_ref, or None."""
+    if os.path.isdir(os.path.join(REF_SITE, "dendromst")) and REF_SITE not in sys.path:
+        sys.path.insert(0, REF_SITE)
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join("/tmp", "dmst_numba_cache"))
+    try:
+        import dendromst  # type: ignore
+        from dendromst import tree_core  # noqa: F401  (numba import check)
+        return dendromst
+    except Exception:
+        return None
+
+
+def cpu_worker(args) -> None:
+    """Subprocess body: time the reference CPU path exactly as `dendromst
+    build` scopes it (cli.py:82-85: perf_counter around rank_edges + pandora)
+    on `--n` edges of the workload's shape, `--repeats` times, 1 core.  The
+    WeightedTree is built untimed (the inputs are trees by construction; the
+    reference's own weighted_tree validation is outside its timed scope too),
+    and numba's JIT is warmed on a tiny tree first.  Uses the unmodified
+    reference from baseline/_ref when it is installed ("reference"), else the
+    oracle port (numpy + C union-find, "port")."""
     from paper_2401_06089_b200 import synth
-    gen, _, _ = WORKLOADS[workload]
-    nv, u, v, w = synth.GENERATORS[gen](n_sample, seed=0)
+    gen, _, _ = WORKLOADS[args.workload]
+    nv, u, v, w = synth.GENERATORS[gen](args.n, seed=0)
+    n = int(u.shape[0])
+    R = _import_reference()
     times = []
-    for _ in range(repeats):
-        t0 = time.perf_counter()
-        O.build(nv, u, v, w)
-        times.append(time.perf_counter() - t0)
-    return n_sample / statistics.median(times), times
+    if R is not None:
+        def mk(nv_, u_, v_, w_):
+            k = int(u_.shape[0])
+            return R.WeightedTree(int(nv_), np.asarray(u_, np.int64), np.asarray(v_, np.int64),
+                                  np.asarray(w_, np.float64), np.arange(k, dtype=np.int64))
+        small = synth.random_attach(2000, seed=1)
+        R.pandora(R.rank_edges(mk(*small)))
+        tree = mk(nv, u, v, w)
+        del u, v, w
+        for _ in range(args.repeats):
+            t0 = time.perf_counter()
+            ranked = R.rank_edges(tree)
+            R.pandora(ranked)
+            times.append(time.perf_counter() - t0)
+            del ranked
+        try:
+            from importlib.metadata import version
+            ver = version("dendromst")
+        except Exception:
+            ver = "?"
+        kind, what = "reference", f"unmodified reference dendromst {ver} (baseline/_ref)"
+    else:
+        from oracle import dendro_oracle as O
+        for _ in range(args.repeats):
+            t0 = time.perf_counter()
+            O.build(nv, u, v, w)
+            times.append(time.perf_counter() - t0)
+        kind, what = "port", "oracle port of the reference (numpy + C union-find; reference not installed)"
+    print(json.dumps({"kind": kind, "what": what, "n": n, "times": times}), flush=True)
+
+
+def cpu_reference(workload: str, n: int, repeats: int) -> dict:
+    """Run cpu_worker in a fresh process (the 128M reference needs ~26 GB of
+    host memory, released when it exits)."""
+    cmd = [sys.executable, os.path.abspath(__file__), "--cpu-worker", "--workload", workload, "--n", str(n),
+           "--repeats", str(repeats)]
+    out = subprocess.run(cmd, capture_output=True, text=True, check=True).stdout
+    return json.loads(out.strip().splitlines()[-1])
+
+
+def reference_sample(n_full: int, steps: int, budget_s: float) -> int:
+    """Edges per step for the reference arm: the whole K-step run ~ budget_s
+    at the reference's ~0.7e6 edges/s (1 core), between 1M and the full n."""
+    per = int(budget_s * 0.7e6 / max(steps, 1))
+    return int(min(n_full, max(1_000_000, per // 1_000_000 * 1_000_000)))
 
 
 def run_reference(args) -> None:
@@ -247,33 +317,58 @@ def run_reference(args) -> None:
     if rank != 0:
         return
     _, n_full, desc = WORKLOADS[args.workload]
-    n_sample = min(args.ref_sample, args.n or n_full)
-    O_warm = max(args.warmup, 0)
-    from oracle import dendro_oracle as O
-    from paper_2401_06089_b200 import synth
-    gen, _, _ = WORKLOADS[args.workload]
-    nv, u, v, w = synth.GENERATORS[gen](n_sample, seed=0)
-    for _ in range(O_warm):
-        O.build(nv, u, v, w)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        O.build(nv, u, v, w)
-        times.append(time.perf_counter() - t0)
+    n_full = args.n or n_full
+    n_sample = args.ref_sample or reference_sample(n_full, args.steps, args.ref_budget)
+    r = cpu_reference(args.workload, n_sample, args.steps)
+    times = r["times"]
     mean = sum(times) / len(times)
-    value = n_sample / mean
-    sample = (f"{n_sample} edges of the {args.workload} shape per step (bounded sample of the "
-              f"n={n_full} workload); oracle port of rank_edges+pandora, numpy + C union-find")
+    value = r["n"] / mean
+    sample = (f"{r['n']} edges of the {args.workload} shape per step (a bounded sample of the n={n_full} "
+              f"workload, sized so K={args.steps} steps take ~{args.ref_budget:.0f} s); {r['what']}; "
+              f"rank_edges + pandora timed as cli.py:82-85 scopes it; numba JIT warmed on a 2k-edge tree")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * mean,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64+int64",
         "data": "synthetic",
-        "config": {"workload": desc, "n_edges_sample": n_sample, "parallelism": "single core"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample,
-                         "host_cpus": os.cpu_count()},
+        "config": {"workload": desc, "n_edges": n_full, "n_edges_sample_per_step": r["n"],
+                   "parallelism": "single core (the reference is single-threaded: numpy + numba without prange)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": r["kind"], "sample": sample,
+                         "host_cpus": os.cpu_count(), "times_s": times},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+DIGEST_CASE = {"config4": "config4_tied", "config4u": "config4_uniform", "random16M": "random16M",
+               "config3-path": "path16M", "config3-caterpillar": "caterpillar16M", "config2": "config2"}
+
+
+def reference_parity(workload: str, seeds: list[int], outs) -> dict | None:
+    """Compare this run's outputs with the digests of the UNMODIFIED
+    reference's outputs on the same inputs (tests/golden/ref_digests/, made by
+    tests/golden/make_digests.py): sha256 of int32 orig_of / edge_parent /
+    vertex_parent and float64 heights.  Outside the timed region."""
+    import hashlib
+    ddir = os.path.join(ROOT, "tests", "golden", "ref_digests")
+    checked = exact = 0
+    for sd, o in zip(seeds, outs):
+        case = f"config5_{sd}" if workload == "config5" else (DIGEST_CASE.get(workload) if sd == 0 else None)
+        path = os.path.join(ddir, f"{case}.json") if case else None
+        if not path or not os.path.exists(path):
+            continue
+        d = json.load(open(path))
+        ok = True
+        for key, t, dt in (("orig_of", o.orig_of, np.int32), ("heights", o.heights, np.float64),
+                           ("edge_parent", o.edge_parent, np.int32), ("vertex_parent", o.vertex_parent, np.int32)):
+            a = np.ascontiguousarray(t.cpu().numpy().astype(dt, copy=False))
+            ok &= hashlib.sha256(a.tobytes()).hexdigest() == d[key]
+        checked += 1
+        exact += int(ok)
+    if not checked:
+        return None
+    return {"trees_checked": checked, "bit_exact": exact,
+            "against": "sha256 of the unmodified reference's rank_edges + pandora outputs on the same inputs "
+                       "(tests/golden/ref_digests)"}
 
 
 def run_b200(args) -> None:
@@ -293,6 +388,7 @@ def run_b200(args) -> None:
     if ws > 1:
         torch.distributed.barrier()
 
+    paths = json.loads(args.paths) if args.paths else None  # code-path overrides (experiments; same results)
     seeds = replica_plan(args.workload, ws, rank)
     trees, desc = make_inputs(args.workload, args.n, seeds)
     n_max = max(int(t[1].shape[0]) for t in trees)
@@ -332,7 +428,7 @@ def run_b200(args) -> None:
                 s_.wait_event(start_evt)
             for t in range(i, len(trees), n_streams):
                 nv, du, dv, dw = inputs[t]
-                res = b.build(nv, du, dv, dw, out=outs[t], profile=profile)
+                res = b.build(nv, du, dv, dw, out=outs[t], profile=profile, paths=paths)
                 last_res[0] = res
                 with lock:
                     counters["launches"] += int(res.stats.kernel_launches)
@@ -388,6 +484,13 @@ def run_b200(args) -> None:
     n_last = int(dev_trees[-1][1].shape[0])
     S = sum(c[3] for c in counts[1:])
 
+    parity = reference_parity(args.workload, seeds, outs) if not args.n else None
+    chk = reduce_sum([float(parity["trees_checked"]) if parity else 0.0,
+                      float(parity["bit_exact"]) if parity else 0.0], device=dev)  # every rank joins
+    parity = {"trees_checked": int(chk[0]), "bit_exact": int(chk[1]),
+              "against": "sha256 of the unmodified reference's rank_edges + pandora outputs on the same inputs "
+                         "(tests/golden/ref_digests)"} if chk[0] else None
+
     # ---------------- end-to-end through the public API (host buffers) ----------------
     # DendrogramBuilder.build_host (C ABI dmst_build_host): pinned host
     # inputs copied in, every output copied back to pinned host buffers as
@@ -422,7 +525,7 @@ def run_b200(args) -> None:
                     nv, hu, hv, hw = host_in[t]
                     n_t = int(hu.shape[0])
                     o = e2e_outs[i]
-                    b.build_host(nv, hu, hv, hw, out=HostBuildResult(
+                    b.build_host(nv, hu, hv, hw, paths=paths, out=HostBuildResult(
                         o.orig_of[:n_t], o.heights[:n_t], o.edge_parent[:n_t], o.vertex_parent[:nv]))
                 done = torch.cuda.Event()
                 done.record(s_)
@@ -503,12 +606,14 @@ def run_b200(args) -> None:
         pipe_ach = B / (ms_step * 1e-3) / 1e9
         cpu = None
         if ws == 1 and not args.no_cpu_baseline:
-            n_s = min(args.cpu_sample, n_last)
-            rate, times = cpu_reference_rate(args.workload, n_s, 1)
-            cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
-                   "sample": f"oracle port (numpy + C union-find, 1 core) of rank_edges+pandora on "
-                             f"{n_s} edges of the {args.workload} shape, {times[0]:.1f}s",
-                   "host_cpus": os.cpu_count()}
+            n_s = min(args.cpu_sample or n_last, n_last)
+            r = cpu_reference(args.workload, n_s, args.cpu_repeats)
+            cpu = {"value": r["n"] / statistics.median(r["times"]), "unit": UNIT, "cores": 1, "kind": r["kind"],
+                   "sample": (f"{'the full workload' if r['n'] == n_last else 'a bounded sample'}: {r['n']} edges "
+                              f"of the {args.workload} shape, median of {len(r['times'])} run(s) "
+                              f"({', '.join(f'{t:.1f}' for t in r['times'])} s); {r['what']}; rank_edges + pandora "
+                              f"timed as cli.py:82-85 scopes it, 1 core"),
+                   "host_cpus": os.cpu_count(), "host_affinity": len(os.sched_getaffinity(0))}
         n_tree = n_last
         line = {
             "metric": METRIC, "value": edges_total / (ms_step * 1e-3), "unit": UNIT, "n_gpus": ws,
@@ -522,8 +627,7 @@ def run_b200(args) -> None:
                        "l2": "inputs (16 B/edge = %.1f GB) and working set larger than the 126 MB L2"
                              % (16 * n_tree / 1e9) if n_tree > 10_000_000 else "working set per tree vs 126 MB L2",
                        "parallelism": f"replicas x{ws}", "levels": stats.num_levels,
-                       "sort1_passes": stats.sort1_passes, "sort2_passes": stats.sort2_passes,
-                       "S_over_n": S / n_tree},
+                       "paths": stats.path_info(), "S_over_n": S / n_tree},
             "e2e": {"value": edges_total / (e2e_ms * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
                     "api": "DendrogramBuilder.build_host -> dmst_build_host (pinned host buffers)",
@@ -544,6 +648,7 @@ def run_b200(args) -> None:
                                     "frac": round(v["achieved_GBs"] / peak, 4)}
                                 for k, v in sorted(kroof.items(), key=lambda kv: -kv[1]["ms_per_build"])},
             "cpu_baseline": cpu,
+            "parity": parity,
             "clocks": clk.summary(),
             "gpu_launches": launches,
         }
@@ -560,17 +665,26 @@ def main() -> None:
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="config4")
     ap.add_argument("--n", type=int, default=None, help="override the workload's edge count")
-    ap.add_argument("--cpu-sample", type=int, default=8_000_000)
+    ap.add_argument("--cpu-sample", type=int, default=0,
+                    help="edges for cpu_baseline (0 = the full workload tree; 128M takes ~4 min)")
+    ap.add_argument("--cpu-repeats", type=int, default=1)
     ap.add_argument("--streams", type=int, default=8, help="concurrent trees per GPU (multi-tree workloads)")
-    ap.add_argument("--ref-sample", type=int, default=2_000_000)
+    ap.add_argument("--ref-sample", type=int, default=0,
+                    help="reference arm: edges per step (0 = sized by --ref-budget)")
+    ap.add_argument("--ref-budget", type=float, default=150.0, help="reference arm: seconds for all K steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--paths", default="", help="JSON dmst_stats path overrides, e.g. '{\"sort2_geometry\": 4}'")
+    ap.add_argument("--cpu-worker", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--repeats", type=int, default=1, help=argparse.SUPPRESS)
     ap.add_argument("--e2e-depth", type=int, default=2, help="builds in flight in the e2e leg")
     ap.add_argument("--e2e-steps", type=int, default=12,
                     help="builds timed in the e2e leg (a stream of builds: pipeline fill and drain included)")
     args = ap.parse_args()
     if args.warmup < 0 or args.steps < 1:
         raise SystemExit("bad steps/warmup")
-    if args.impl == "reference":
+    if args.cpu_worker:
+        cpu_worker(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_b200(args)

@@ -17,6 +17,7 @@ DMST_EINVAL = 22
 DMST_ECUDA = -1
 DMST_MAX_LEVELS = 64
 DMST_MAX_KERNELS = 24
+SORT2_GEOMETRIES = {0: None, 1: "512x16", 2: "256x20", 3: "512x16-or", 4: "256x18-or"}
 
 # every symbol include/dmst.h declares
 EXPORTS = (
@@ -81,7 +82,7 @@ class DmstStats(ctypes.Structure):
         L = int(self.num_levels)
         return {"sort1_passes": int(self.sort1_passes), "sort1_narrow": bool(self.sort1_narrow),
                 "sort1_compacted": bool(self.sort1_compacted), "sort2_passes": int(self.sort2_passes),
-                "sort2_geometry": {0: None, 1: "512x16", 2: "256x20"}[int(self.sort2_geometry_used)],
+                "sort2_geometry": SORT2_GEOMETRIES[int(self.sort2_geometry_used)],
                 "tail_level": int(self.tail_level),
                 "mi_bucketed_views": [k for k in range(L + 1) if (int(self.mi_bucketed) >> k) & 1],
                 "mi_direct_views": [k for k in range(L + 1) if (int(self.mi_direct) >> k) & 1]}

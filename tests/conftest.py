@@ -84,3 +84,24 @@ def has_gpu() -> bool:
         return torch.cuda.is_available()
     except Exception:
         return False
+
+
+REF_SITE = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_package():
+    """The unmodified reference package `dendromst`, pip-installed into
+    baseline/_ref (`pip install --no-deps --target baseline/_ref`
+    of /root/reference/pkg; it travels to the GPU box with the repo
+    snapshot), or None when it is not installed."""
+    if not os.path.isdir(os.path.join(REF_SITE, "dendromst")):
+        return None
+    if REF_SITE not in sys.path:
+        sys.path.insert(0, REF_SITE)
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/dmst_numba_cache")
+    try:
+        import dendromst  # noqa: F401
+        import dendromst.cli  # noqa: F401
+        return dendromst
+    except Exception:
+        return None

@@ -42,6 +42,9 @@ PATHS = {
     "wide_sort_large_s2": {"sort1_mode": 3, "sort2_geometry": 2},
     # narrow keys without compaction; 512 x 16 chain-sort tiles; no tail, bucketed
     "nocompact_bucketed": {"sort1_mode": 2, "sort2_geometry": 1, "direct_mi_bytes": -1, "tail_edges": -1},
+    # atomic-or warp ranking: wide edge-sort keys, both chain-sort geometries
+    "or_rank_512": {"sort1_mode": 7, "sort2_geometry": 3},
+    "or_rank_256": {"sort1_mode": 4, "sort2_geometry": 4, "tail_edges": -1},
 }
 
 SEEN_KINDS: dict[str, int] = {}   # kernel kind -> launches inside checked builds
@@ -104,7 +107,8 @@ def _assert_path_taken(res, paths):
     if p.get("sort1_mode", 0) & 2:
         assert not info["sort1_compacted"]
     if p.get("sort2_geometry") and info["sort2_passes"]:
-        assert info["sort2_geometry"] == {1: "512x16", 2: "256x20"}[p["sort2_geometry"]]
+        from paper_2401_06089_b200._lib import SORT2_GEOMETRIES
+        assert info["sort2_geometry"] == SORT2_GEOMETRIES[p["sort2_geometry"]]
 
 
 GOLDEN = list(golden_trees())
@@ -168,9 +172,9 @@ def test_deep_in_trees_all_paths(builder, paths):
 def test_rejects_bad_path_options(builder):
     nv, u, v, w = synth.random_attach(100, seed=1)
     with pytest.raises(ValueError):
-        builder.build(nv, u, v, w, paths={"sort2_geometry": 3})
+        builder.build(nv, u, v, w, paths={"sort2_geometry": 5})
     with pytest.raises(ValueError):
-        builder.build(nv, u, v, w, paths={"sort1_mode": 4})
+        builder.build(nv, u, v, w, paths={"sort1_mode": 8})
     with pytest.raises(ValueError):
         builder.build(nv, u, v, w, paths={"no_such_option": 1})
 

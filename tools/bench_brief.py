@@ -12,5 +12,5 @@ for f in sys.argv[1:]:
     print(f"{f}: {d['ms_per_step']:.3f} ms/step, {d['value']:.3e} {d['unit']}, frac "
           f"{d.get('pipeline_roofline', {}).get('frac', 0):.3f}, e2e {d.get('e2e', {}).get('value', 0):.3e} "
           f"(serial {d.get('e2e', {}).get('serial', {}).get('value', 0):.3e}), "
-          f"sort1 {c.get('sort1_passes')} sort2 {c.get('sort2_passes')} L {c.get('levels')}")
+          f"paths {c.get('paths')} L {c.get('levels')} parity {d.get('parity')}")
     print("   ", {k: round(v, 3) for k, v in d.get("kernel_ms_per_step", {}).items()})

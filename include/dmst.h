@@ -81,11 +81,9 @@ typedef struct dmst_stats {
   int64_t direct_mi_bytes;  /* views >= 1 whose packed maxIncident (8 B per vertex) is at
                                most this large take direct atomics in k_select_edges + k_v1
                                (default 64 MB); -1 = always bucketed (multisplit + apply) */
-  int32_t sort1_mode;       /* bit 0: no narrow 32-bit keys; bit 1: no top-field compaction;
-                               bit 2: atomic-or warp ranking in wide-key passes */
-  int32_t sort2_geometry;   /* chain-sort tiles and warp ranking: 1 = 512 x 16 vote, 2 = 256 x 20
-                               vote (two CTAs per SM), 3 = 512 x 16 atomic-or, 4 = 256 x 18
-                               atomic-or; 0 = by size (2 from 32M edges) */
+  int32_t sort1_mode;       /* bit 0: no narrow 32-bit keys; bit 1: no top-field compaction */
+  int32_t sort2_geometry;   /* chain-sort tiles: 1 = 512 x 16, 2 = 256 x 20 (two CTAs per SM);
+                               0 = by size (2 from 32M edges) */
   /* out: the path this call took (what bench.py's byte model reads) */
   int32_t sort1_narrow;     /* 1 = the edge sort ran on 32-bit keys */
   int32_t sort1_compacted;  /* 1 = the sign/exponent field was replaced by its dense code */

@@ -17,7 +17,7 @@ DMST_EINVAL = 22
 DMST_ECUDA = -1
 DMST_MAX_LEVELS = 64
 DMST_MAX_KERNELS = 24
-SORT2_GEOMETRIES = {0: None, 1: "512x16", 2: "256x20", 3: "512x16-or", 4: "256x18-or"}
+SORT2_GEOMETRIES = {0: None, 1: "512x16", 2: "256x20"}
 
 # every symbol include/dmst.h declares
 EXPORTS = (

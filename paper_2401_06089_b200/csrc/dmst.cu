@@ -56,9 +56,6 @@ constexpr int S2_BLOCK = 512, S2_ITEMS = 16, S2_MINB = 1, S2_BITS = 9;
 // fewer, larger chunks of one CTA per SM (config 5: 129 -> 124 ms)
 constexpr int S2L_BLOCK = 256, S2L_ITEMS = 20, S2L_MINB = 2;
 constexpr int64_t kS2LargeEdges = 32ll << 20;
-// atomic-or ranking (RANK_OR) needs a peer-mask word per digit and warp: two
-// 256-thread CTAs per SM fit with 18-item tiles
-constexpr int S2O_ITEMS = 18;
 constexpr int64_t kDirectMiBytes = 64ll << 20;  // direct scatter-max below this mi64 size
 
 enum KernelKind {
@@ -381,12 +378,12 @@ SweepGeom sweep_geom(const Ctx& c, int64_t n, int T, int minb, int64_t align = 0
 
 // One radix pass: upsweep (per-chunk digit counts; skipped when a fused
 // upsweep already produced them), chunk scan, downsweep.
-template <typename K, int PW, int BLOCK, int ITEMS, int MINB, int BITS, int RANK, class Loader, class Emitter>
+template <typename K, int PW, int BLOCK, int ITEMS, int MINB, int BITS, class Loader, class Emitter>
 int64_t radix_pass(Ctx& c, int kind, int64_t n, int shift, Loader ld, Emitter em, bool counts_ready = false,
                    int64_t align = 0, int geom_minb = 0) {
-  using S = DownSmem<K, PW, BLOCK, ITEMS, Loader, Emitter, BITS, RANK>;
+  using S = DownSmem<K, PW, BLOCK, ITEMS, Loader, Emitter, BITS>;
   constexpr int T = S::T;
-  auto kern = k_downsweep<K, PW, BLOCK, ITEMS, MINB, Loader, Emitter, BITS, RANK>;
+  auto kern = k_downsweep<K, PW, BLOCK, ITEMS, MINB, Loader, Emitter, BITS>;
   smem_attr(kern, (int)S::bytes());
   const SweepGeom g = sweep_geom(c, n, T, geom_minb ? geom_minb : MINB, align);
   SweepArgs a{};
@@ -414,8 +411,7 @@ int64_t radix_pass(Ctx& c, int kind, int64_t n, int shift, Loader ld, Emitter em
 // Multi-pass driver over the non-constant digits (bit offsets `shifts`).
 // Ping-pong buffers: keys bufK[2], AoS payload bufP[2] (PW words per item);
 // first/last passes use the given loader/emitter.
-template <typename K, int PW, int BLOCK, int ITEMS, int MINB, int BITS, int RANK, class FirstLoader,
-          class FinalEmitter>
+template <typename K, int PW, int BLOCK, int ITEMS, int MINB, int BITS, class FirstLoader, class FinalEmitter>
 int64_t run_sort(Ctx& c, const int (&kinds)[3], int64_t n, const std::vector<int>& shifts,
               K* const (&bufK)[2], uint32_t* const (&bufP)[2], FirstLoader first, FinalEmitter final_em,
               int ready_shift = -1, int64_t align = 0, int first_minb = 0) {
@@ -433,15 +429,15 @@ int64_t run_sort(Ctx& c, const int (&kinds)[3], int64_t n, const std::vector<int
     ArrayLoader<K, PW> ldr{bufK[in], bufP[in]};
     const bool ready = p == 0 && shifts[0] == ready_shift;
     if (P == 1)
-      G = radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS, RANK>(c, kinds[2], n, shifts[p], first, final_em, ready, align,
+      G = radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[2], n, shifts[p], first, final_em, ready, align,
                                                       first_minb);
     else if (p == 0)
-      G = radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS, RANK>(c, kinds[0], n, shifts[p], first, mid, ready, align,
+      G = radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[0], n, shifts[p], first, mid, ready, align,
                                                       first_minb);
     else if (p == P - 1)
-      G = radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS, RANK>(c, kinds[2], n, shifts[p], ldr, final_em, false, align);
+      G = radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[2], n, shifts[p], ldr, final_em, false, align);
     else
-      G = radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS, RANK>(c, kinds[1], n, shifts[p], ldr, mid, false, align);
+      G = radix_pass<K, PW, BLOCK, ITEMS, MINB, BITS>(c, kinds[1], n, shifts[p], ldr, mid, false, align);
   }
   return G;
 }
@@ -548,19 +544,14 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
     Sort1Emitter<uint32_t> em32{em.orig_of, em.heights, em.euv, em.ru, em.rv, em.inv,
                                 lo ? kand & ((1ull << lo) - 1) : 0ull, (uint32_t)lo};
     em32.base |= lo + 32 < 64 ? kand & ~((1ull << (lo + 32)) - 1) : 0ull;
-    run_sort<uint32_t, 3, S1N_BLOCK, S1N_ITEMS, S1N_MINB, 8, RANK_VOTE>(
+    run_sort<uint32_t, 3, S1N_BLOCK, S1N_ITEMS, S1N_MINB, 8>(
         c, {KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL}, n, s32, bufK, bufP,
         Sort1Loader<uint32_t>{w, u, v, code, (uint32_t)lo}, em32, ready >= 0 ? 0 : -1, S1_ALIGN);
   } else {
     uint64_t* const bufK[2] = {(uint64_t*)R, (uint64_t*)(R + 8 * n)};
-    if (c.paths.sort1_mode & 4)
-      run_sort<uint64_t, 3, S1_BLOCK, S1_ITEMS, S1_MINB, 8, RANK_OR>(
-          c, {KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL}, n, shifts, bufK, bufP, Sort1FirstLoader{w, u, v, code},
-          em, ready, S1_ALIGN, S1N_MINB);
-    else
-      run_sort<uint64_t, 3, S1_BLOCK, S1_ITEMS, S1_MINB, 8, RANK_VOTE>(
-          c, {KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL}, n, shifts, bufK, bufP, Sort1FirstLoader{w, u, v, code},
-          em, ready, S1_ALIGN, S1N_MINB);
+    run_sort<uint64_t, 3, S1_BLOCK, S1_ITEMS, S1_MINB, 8>(c, {KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL}, n,
+                                                       shifts, bufK, bufP, Sort1FirstLoader{w, u, v, code}, em,
+                                                       ready, S1_ALIGN, S1N_MINB);
   }
   if (nz) {
     c.begin(KK_OTHER);
@@ -881,26 +872,15 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     ArrayEmitter<uint64_t, 0> fin{bufK[lastb], nullptr};
     std::vector<int> shifts64(shifts);
     for (int& x : shifts64) x += 32;
-    const int geom = c.paths.sort2_geometry ? c.paths.sort2_geometry : (n >= kS2LargeEdges ? 2 : 1);
-    c.paths.sort2_geometry_used = geom;
+    const bool large = c.paths.sort2_geometry ? c.paths.sort2_geometry == 2 : n >= kS2LargeEdges;
+    c.paths.sort2_geometry_used = large ? 2 : 1;
     const int kinds2[3] = {KK_SORT2_PASS, KK_SORT2_PASS, KK_SORT2_PASS};
-    switch (geom) {
-      case 2:
-        run_sort<uint64_t, 0, S2L_BLOCK, S2L_ITEMS, S2L_MINB, S2_BITS, RANK_VOTE>(c, kinds2, n, shifts64, bufK, bufP,
-                                                                                 Sort2FirstLoader{keys}, fin);
-        break;
-      case 3:
-        run_sort<uint64_t, 0, S2_BLOCK, S2_ITEMS, S2_MINB, S2_BITS, RANK_OR>(c, kinds2, n, shifts64, bufK, bufP,
-                                                                            Sort2FirstLoader{keys}, fin);
-        break;
-      case 4:
-        run_sort<uint64_t, 0, S2L_BLOCK, S2O_ITEMS, S2L_MINB, S2_BITS, RANK_OR>(c, kinds2, n, shifts64, bufK, bufP,
-                                                                               Sort2FirstLoader{keys}, fin);
-        break;
-      default:
-        run_sort<uint64_t, 0, S2_BLOCK, S2_ITEMS, S2_MINB, S2_BITS, RANK_VOTE>(c, kinds2, n, shifts64, bufK, bufP,
-                                                                              Sort2FirstLoader{keys}, fin);
-    }
+    if (large)
+      run_sort<uint64_t, 0, S2L_BLOCK, S2L_ITEMS, S2L_MINB, S2_BITS>(c, kinds2, n, shifts64, bufK, bufP,
+                                                                    Sort2FirstLoader{keys}, fin);
+    else
+      run_sort<uint64_t, 0, S2_BLOCK, S2_ITEMS, S2_MINB, S2_BITS>(c, kinds2, n, shifts64, bufK, bufP,
+                                                                 Sort2FirstLoader{keys}, fin);
     if (st && st->want_chains) {
       uint32_t* cnt = w.small + SM_MISC + 60;
       c.zero(cnt, 4);
@@ -962,8 +942,8 @@ void init_ctx(Ctx& c, int64_t n, int64_t nv, void* ws, void* stream, dmst_stats*
     const int32_t prof = st->profile, wc = st->want_chains;
     const int64_t te = st->tail_edges, dm = st->direct_mi_bytes;
     const int32_t s1 = st->sort1_mode, s2 = st->sort2_geometry;
-    if (s1 < 0 || s1 > 7) invalid("sort1_mode must be in [0, 7]");
-    if (s2 < 0 || s2 > 4) invalid("sort2_geometry must be in [0, 4]");
+    if (s1 < 0 || s1 > 3) invalid("sort1_mode must be in [0, 3]");
+    if (s2 < 0 || s2 > 2) invalid("sort2_geometry must be 0, 1 or 2");
     if (te < -1 || dm < -1) invalid("tail_edges / direct_mi_bytes must be >= -1");
     memset(st, 0, sizeof(*st));
     st->profile = prof;
@@ -1314,7 +1294,7 @@ int dmst_validate(const int32_t* u, const int32_t* v, const double* w, int64_t n
     uint32_t* const bufP[2] = {nullptr, nullptr};
     const int lastb = ((int)shifts.size() - 1) % 2;
     ArrayEmitter<uint64_t, 0> fin{bufK[lastb], nullptr};
-    run_sort<uint64_t, 0, S1_BLOCK, S1_ITEMS, S1_MINB, 8, RANK_VOTE>(c, {KK_OTHER, KK_OTHER, KK_OTHER}, n, shifts, bufK, bufP,
+    run_sort<uint64_t, 0, S1_BLOCK, S1_ITEMS, S1_MINB, 8>(c, {KK_OTHER, KK_OTHER, KK_OTHER}, n, shifts, bufK, bufP,
                                                          DupKeyLoader{u, v}, fin);
     c.begin(KK_OTHER);
     k_adjacent_equal<<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>((const unsigned long long*)fin.keys, n, r + 5);

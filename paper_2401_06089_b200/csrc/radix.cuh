@@ -388,20 +388,12 @@ __global__ void __launch_bounds__(kScanThreads) k_chunk_scan(uint32_t* counts, u
 }
 
 // ------------------------------------------------------------- downsweep
-// Warp ranking methods: RANK_VOTE picks __match_any_sync or BITS ballots per
-// pass (k_chunk_scan); RANK_OR builds each item's peer mask with one shared
-// atomicOr of its lane bit into a per-warp digit mask (constant cost, no
-// ballots; needs R more words per warp).
-constexpr int RANK_VOTE = 0, RANK_OR = 1;
-
-template <typename K, int PW, int BLOCK, int ITEMS, class Loader, class Emitter, int BITS = kRadixBits,
-          int RANK = RANK_VOTE>
+template <typename K, int PW, int BLOCK, int ITEMS, class Loader, class Emitter, int BITS = kRadixBits>
 struct DownSmem {
   static constexpr int R = 1 << BITS;
   static constexpr int T = BLOCK * ITEMS;
   static constexpr int NW = BLOCK / 32;
   static constexpr int NS = Loader::NS;
-  static constexpr int kRank = RANK;
   __host__ __device__ static constexpr size_t stream_bytes(int s) {
     return ((size_t)T * Loader::sb(s) + 127) & ~size_t(127);
   }
@@ -422,7 +414,6 @@ struct DownSmem {
   __host__ __device__ static constexpr size_t off_misc() { return 2 * stage_bytes(); }
   struct Misc {
     uint32_t whist[NW][R];
-    uint32_t wmask[RANK == RANK_OR ? NW : 1][RANK == RANK_OR ? R : 1];  // RANK_OR peer masks (zero between uses)
     uint32_t run[R];     // running global offset per digit
     uint32_t lstart[R + 1];
     uint32_t gofs[R];
@@ -462,30 +453,6 @@ __device__ __forceinline__ uint32_t warp_rank(uint32_t* whist, uint32_t d, bool 
   return old + below;
 }
 
-// RANK_OR: every valid lane ORs its bit into the warp's mask word of its
-// digit; after a warp barrier each lane reads its peers, the lowest peer
-// advances the counter and clears the mask for the next item.
-template <bool FULL>
-__device__ __forceinline__ uint32_t warp_rank_or(uint32_t* whist, uint32_t* wmask, uint32_t d, bool valid,
-                                                 uint32_t lane, uint32_t lt) {
-  const bool act = FULL || valid;
-  if (act) atomicOr(&wmask[d], 1u << lane);
-  __syncwarp();
-  uint32_t peers = 0, old = 0;
-  if (act) {
-    peers = wmask[d];
-    old = whist[d];
-  }
-  const uint32_t below = __popc(peers & lt);
-  __syncwarp();  // every peer has read the mask and the counter
-  if (act && below == 0) {
-    whist[d] = old + __popc(peers);
-    wmask[d] = 0;
-  }
-  __syncwarp();
-  return old + below;
-}
-
 // Rank, scatter (in place, into stage buffer `buf`) and write out one sub-tile.
 template <bool FULL, typename K, int PW, int BLOCK, int ITEMS, int BITS, class S, class Emitter>
 __device__ __forceinline__ void down_subtile(const SweepArgs& a, const Emitter& em, typename S::Misc& m,
@@ -501,10 +468,7 @@ __device__ __forceinline__ void down_subtile(const SweepArgs& a, const Emitter& 
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) {
     const bool valid = FULL || lbase + i * 32 < cnt_items;
-    if constexpr (S::kRank == RANK_OR)
-      rk[i] = warp_rank_or<FULL>(m.whist[warp], m.wmask[warp], digit_of<BITS>(k[i], a.shift), valid, lane, lt);
-    else
-      rk[i] = warp_rank<FULL, BITS>(m.whist[warp], digit_of<BITS>(k[i], a.shift), valid, lane, lt, m.ballot);
+    rk[i] = warp_rank<FULL, BITS>(m.whist[warp], digit_of<BITS>(k[i], a.shift), valid, lane, lt, m.ballot);
   }
   __syncthreads();  // (also: every thread has finished reading `buf`)
 
@@ -570,12 +534,11 @@ __device__ __forceinline__ void down_subtile(const SweepArgs& a, const Emitter& 
   __syncthreads();
 }
 
-template <typename K, int PW, int BLOCK, int ITEMS, int MINB, class Loader, class Emitter, int BITS = kRadixBits,
-          int RANK = RANK_VOTE>
+template <typename K, int PW, int BLOCK, int ITEMS, int MINB, class Loader, class Emitter, int BITS = kRadixBits>
 __global__ void __launch_bounds__(BLOCK, MINB)
 k_downsweep(SweepArgs a, Loader ld, Emitter em) {
   static_assert(BLOCK % 32 == 0 && ((1 << BITS) % BLOCK == 0 || BLOCK % (1 << BITS) == 0), "digit ownership");
-  using S = DownSmem<K, PW, BLOCK, ITEMS, Loader, Emitter, BITS, RANK>;
+  using S = DownSmem<K, PW, BLOCK, ITEMS, Loader, Emitter, BITS>;
   constexpr int T = S::T, NW = S::NW, NS = S::NS, R = S::R;
   extern __shared__ __align__(128) unsigned char smem[];
   typename S::Misc& m = *reinterpret_cast<typename S::Misc*>(smem + S::off_misc());
@@ -591,10 +554,6 @@ k_downsweep(SweepArgs a, Loader ld, Emitter em) {
     m.run[b] = a.counts[(uint64_t)b * a.GS + blockIdx.x];
 #pragma unroll
     for (int w = 0; w < NW; ++w) m.whist[w][b] = 0;
-    if constexpr (RANK == RANK_OR) {
-#pragma unroll
-      for (int w = 0; w < NW; ++w) m.wmask[w][b] = 0;
-    }
   }
   if (tid == 0) {
     mbar_init(&m.bar[0], 1);

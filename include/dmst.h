@@ -91,6 +91,9 @@ typedef struct dmst_stats {
   int32_t tail_level;       /* first view finished inside k_tail, -1 = none */
   uint64_t mi_bucketed;     /* bit k: view k's maxIncident was bucketed */
   uint64_t mi_direct;       /* bit k: view k's maxIncident took direct atomics */
+  /* in: kernel-variant switches for A/B measurement (0 = the default kernels;
+   * same bits either way).  None defined at present. */
+  int32_t variant;
 } dmst_stats;
 
 /* Workspace size for a tree with n_edges edges. */

@@ -66,10 +66,11 @@ class DmstStats(ctypes.Structure):
         ("tail_level", ctypes.c_int32),
         ("mi_bucketed", ctypes.c_uint64),
         ("mi_direct", ctypes.c_uint64),
+        ("variant", ctypes.c_int32),
     ]
 
     # code-path overrides accepted by DendrogramBuilder.build(paths=...)
-    PATH_OPTIONS = ("tail_edges", "direct_mi_bytes", "sort1_mode", "sort2_geometry")
+    PATH_OPTIONS = ("tail_edges", "direct_mi_bytes", "sort1_mode", "sort2_geometry", "variant")
 
     def set_paths(self, paths: dict | None) -> None:
         for k, v in (paths or {}).items():

@@ -10,6 +10,8 @@
 // one CTA per fine bucket reduces its records in shared memory and writes
 // the bucket's slice of mi64 (and V1's outputs) with coalesced stores.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 #include "radix.cuh"  // TMA bulk-copy / mbarrier helpers
 
@@ -89,6 +91,12 @@ struct AosRecSrc {
   __device__ __forceinline__ uint32_t vertex(int64_t i) const { return __ldg(r + RW * i); }
 };
 
+template <class Src>
+__device__ __forceinline__ const int2* edge_ptr(const Src& src) {
+  if constexpr (std::is_same<Src, EdgeRecSrc>::value) return src.euv;
+  else return nullptr;
+}
+
 // counts[f] += number of records whose vertex is in fine bucket f, for
 // f in [flo, flo + 16384) (windowed: very large views run several windows).
 constexpr int FH_WINDOW = 16384;
@@ -99,18 +107,53 @@ __global__ void __launch_bounds__(256) k_fine_hist(Src src, int64_t m, uint32_t 
   extern __shared__ uint32_t h[];  // [W]
   for (int i = threadIdx.x; i < W; i += 256) h[i] = 0;
   __syncthreads();
-  constexpr int U = 8;
-  const int64_t stride = (int64_t)gridDim.x * 256 * U;
-  for (int64_t b = (int64_t)blockIdx.x * 256 * U + threadIdx.x; b < m; b += stride) {
-    uint32_t f[U];
+  bool vec = false;
+  if constexpr (std::is_same<Src, EdgeRecSrc>::value) vec = aligned16(src.euv);
+  if (vec) {
+    // two edges (four records) per 16-B load, four loads in flight per thread
+    constexpr int U = 4;
+    const int64_t ne = m >> 1, np = ne >> 1;  // edges, edge pairs
+    const int4* pairs = reinterpret_cast<const int4*>(edge_ptr(src));
+    const int64_t stride = (int64_t)gridDim.x * 256 * U;
+    for (int64_t b = (int64_t)blockIdx.x * 256 * U + threadIdx.x; b < np; b += stride) {
+      int4 e[U];
 #pragma unroll
-    for (int q = 0; q < U; ++q) {
-      const int64_t i = b + q * 256;
-      f[q] = i < m ? (src.vertex(i) >> FB_BITS) - flo : 0xffffffffu;
+      for (int q = 0; q < U; ++q) {
+        const int64_t i = b + q * 256;
+        e[q] = i < np ? ld_stream(pairs + i) : make_int4(-1, -1, -1, -1);
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const uint32_t f0 = ((uint32_t)e[q].x >> FB_BITS) - flo, f1 = ((uint32_t)e[q].y >> FB_BITS) - flo;
+        const uint32_t f2 = ((uint32_t)e[q].z >> FB_BITS) - flo, f3 = ((uint32_t)e[q].w >> FB_BITS) - flo;
+        if (e[q].x >= 0) {
+          if (f0 < (uint32_t)W) atomicAdd(&h[f0], 1u);
+          if (f1 < (uint32_t)W) atomicAdd(&h[f1], 1u);
+          if (f2 < (uint32_t)W) atomicAdd(&h[f2], 1u);
+          if (f3 < (uint32_t)W) atomicAdd(&h[f3], 1u);
+        }
+      }
     }
+    if ((ne & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd edge count: the last edge
+      const int2 e = edge_ptr(src)[ne - 1];
+      const uint32_t f0 = ((uint32_t)e.x >> FB_BITS) - flo, f1 = ((uint32_t)e.y >> FB_BITS) - flo;
+      if (f0 < (uint32_t)W) atomicAdd(&h[f0], 1u);
+      if (f1 < (uint32_t)W) atomicAdd(&h[f1], 1u);
+    }
+  } else {
+    constexpr int U = 8;
+    const int64_t stride = (int64_t)gridDim.x * 256 * U;
+    for (int64_t b = (int64_t)blockIdx.x * 256 * U + threadIdx.x; b < m; b += stride) {
+      uint32_t f[U];
 #pragma unroll
-    for (int q = 0; q < U; ++q)
-      if (f[q] < (uint32_t)W) atomicAdd(&h[f[q]], 1u);
+      for (int q = 0; q < U; ++q) {
+        const int64_t i = b + q * 256;
+        f[q] = i < m ? (src.vertex(i) >> FB_BITS) - flo : 0xffffffffu;
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q)
+        if (f[q] < (uint32_t)W) atomicAdd(&h[f[q]], 1u);
+    }
   }
   __syncthreads();
   const uint32_t lim = min((uint32_t)W, nf - flo);

@@ -4,7 +4,7 @@
 // symbol each stage replaces (paths under /root/reference/pkg/src/dendromst/):
 //
 //  1. edge sort        rank_edges            tree_core.py:174-190
-//     k_sort1_hist, then per non-constant digit k_upsweep -> k_chunk_scan ->
+//     k_sort1_hist, then per non-constant digit k_upsweep -> row scans ->
 //     k_downsweep (radix.cuh).
 //     Key = order-preserving uint64 of (w + 0.0), descending; payload =
 //     (original id, u, v) so the last pass writes orig_of, heights (decoded
@@ -244,6 +244,7 @@ struct Paths {
   int64_t direct_mi_bytes = kDirectMiBytes;
   int sort1_mode = 0;
   int sort2_geometry = 0;
+  int variant = 0;
   // out
   int sort1_narrow = 0, sort1_compacted = 0, sort2_geometry_used = 0, tail_level = -1;
   uint64_t mi_bucketed = 0, mi_direct = 0;
@@ -400,7 +401,10 @@ int64_t radix_pass(Ctx& c, int kind, int64_t n, int shift, Loader ld, Emitter em
     c.launched();
   }
   c.begin(KK_UPSWEEP);
-  k_chunk_scan<BITS><<<1, kScanThreads, 0, c.s>>>(a.counts, a.GS);
+  k_row_scan<BITS><<<(1u << BITS) / kRowScanWarps, 32 * kRowScanWarps, 0, c.s>>>(a.counts, a.GS);
+  c.launched();
+  c.begin(KK_UPSWEEP);
+  k_row_total_scan<BITS><<<1, 1u << BITS, 0, c.s>>>(a.counts, a.GS);
   c.launched();
   c.begin(kind);
   kern<<<(unsigned)g.G, BLOCK, S::bytes(), c.s>>>(a, ld, em);
@@ -941,7 +945,7 @@ void init_ctx(Ctx& c, int64_t n, int64_t nv, void* ws, void* stream, dmst_stats*
   if (st) {
     const int32_t prof = st->profile, wc = st->want_chains;
     const int64_t te = st->tail_edges, dm = st->direct_mi_bytes;
-    const int32_t s1 = st->sort1_mode, s2 = st->sort2_geometry;
+    const int32_t s1 = st->sort1_mode, s2 = st->sort2_geometry, var = st->variant;
     if (s1 < 0 || s1 > 3) invalid("sort1_mode must be in [0, 3]");
     if (s2 < 0 || s2 > 2) invalid("sort2_geometry must be 0, 1 or 2");
     if (te < -1 || dm < -1) invalid("tail_edges / direct_mi_bytes must be >= -1");
@@ -952,11 +956,13 @@ void init_ctx(Ctx& c, int64_t n, int64_t nv, void* ws, void* stream, dmst_stats*
     st->direct_mi_bytes = dm;
     st->sort1_mode = s1;
     st->sort2_geometry = s2;
+    st->variant = var;
     c.profile = prof != 0;
     if (te) c.paths.tail_edges = te;  // -1: n_k <= -1 never holds
     if (dm) c.paths.direct_mi_bytes = dm;
     c.paths.sort1_mode = s1;
     c.paths.sort2_geometry = s2;
+    c.paths.variant = var;
   }
 }
 

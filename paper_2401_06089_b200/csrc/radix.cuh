@@ -4,9 +4,9 @@
 //   k_upsweep    each CTA counts the digits of its contiguous chunk of the
 //                input (keys only) -> counts[digit][chunk]; for the edge
 //                sort's first pass it also reduces all keys (KEYRED);
-//   k_chunk_scan one CTA: exclusive scan of counts in digit-major order ->
-//                the global output offset of every (digit, chunk), and the
-//                pass's warp-ranking method (match_any or ballots);
+//   k_row_scan + k_row_total_scan: exclusive scan of counts in digit-major
+//                order -> the global output offset of every (digit, chunk),
+//                and the pass's warp-ranking method (match_any or ballots);
 //   k_downsweep  persistent: CTA c walks its chunk in sub-tiles of T items,
 //                keeps a running output offset per digit in shared memory
 //                (no inter-CTA look-back, no spinning), ranks each sub-tile
@@ -319,71 +319,62 @@ __global__ void __launch_bounds__(256) k_upsweep(SweepArgs a, Loader ld, KeyRed 
   }
 }
 
-// Exclusive scan of counts[R][GS] in place, digit-major => the global
-// output offset of every (digit, chunk).  Thread t owns rows t*BPT.. (vector
-// loads).  Also picks the pass's warp-ranking method: with digit
-// frequencies p_d, a warp of 32 items holds E = sum_d 1 - (1 - p_d)^32
-// distinct digits on average; __match_any_sync is cheaper below ~kBallotE,
-// ballots above (counts[R * GS] = 1 => ballots).
+// Exclusive scan of counts[R][GS] digit-major => the global output offset of
+// every (digit, chunk), in two small kernels instead of one serial CTA:
+//   k_row_scan        one warp per digit row: the row becomes its exclusive
+//                     in-row offsets, the row total goes to rowsum[r];
+//   k_row_total_scan  one CTA: exclusive scan of the R row totals -> rowstart
+//                     (the downsweep adds rowstart[d] to its row entry), and
+//                     the pass's warp-ranking method: with digit frequencies
+//                     p_d, a warp of 32 items holds E = sum_d 1 - (1 - p_d)^32
+//                     distinct digits on average; __match_any_sync is cheaper
+//                     below ~kBallotE, ballots above (ballot word = 1).
+// Layout behind the R * GS counts: [ballot word, pad x3, rowsum[R], rowstart[R]].
 constexpr float kBallotE = 12.0f;
-constexpr int kScanThreads = 1024;
+constexpr int kRowScanWarps = 8;
+__host__ __device__ constexpr uint64_t scan_ballot_off(int R, uint32_t GS) { return (uint64_t)R * GS; }
+__host__ __device__ constexpr uint64_t scan_rowsum_off(int R, uint32_t GS) { return (uint64_t)R * GS + 4; }
+__host__ __device__ constexpr uint64_t scan_rowstart_off(int R, uint32_t GS) { return (uint64_t)R * GS + 4 + R; }
+
 template <int BITS>
-__global__ void __launch_bounds__(kScanThreads) k_chunk_scan(uint32_t* counts, uint32_t GS) {
-  // one warp per digit row at a time (coalesced, lanes stride the chunks):
-  // row totals, a block scan over the R totals, then each row rewritten as
-  // exclusive offsets with a warp scan
-  constexpr int R = 1 << BITS, NWS = kScanThreads / 32;
-  __shared__ uint32_t rowsum[R];
-  __shared__ uint32_t scratch[kScanThreads / 32 + 1];
-  __shared__ float fscr[kScanThreads / 32];
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int r = warp; r < R; r += NWS) {
-    const uint32_t* row = counts + (uint64_t)r * GS;
-    uint32_t t = 0;
-    for (uint32_t q = lane; q < GS; q += 32) t += row[q];
-    t = __reduce_add_sync(kFull, t);
-    if (lane == 0) rowsum[r] = t;
+__global__ void __launch_bounds__(32 * kRowScanWarps) k_row_scan(uint32_t* counts, uint32_t GS) {
+  constexpr int R = 1 << BITS;
+  const uint32_t lane = threadIdx.x & 31;
+  const int r = blockIdx.x * kRowScanWarps + (threadIdx.x >> 5);
+  if (r >= R) return;
+  uint32_t* row = counts + (uint64_t)r * GS;
+  uint32_t base = 0;
+  for (uint32_t q0 = 0; q0 < GS; q0 += 64) {  // two loads in flight per lane
+    const uint32_t qa = q0 + lane, qb = q0 + 32 + lane;
+    const uint32_t xa = qa < GS ? row[qa] : 0u, xb = qb < GS ? row[qb] : 0u;
+    const uint32_t ia = warp_incl_sum(xa), ib = warp_incl_sum(xb);
+    const uint32_t ta = __shfl_sync(kFull, ia, 31);
+    if (qa < GS) row[qa] = base + ia - xa;
+    if (qb < GS) row[qb] = base + ta + ib - xb;
+    base += ta + __shfl_sync(kFull, ib, 31);
   }
-  __syncthreads();
-  constexpr int RPT = (R + kScanThreads - 1) / kScanThreads;  // rows per thread in the block scan
-  uint32_t v[RPT], sum = 0;
-#pragma unroll
-  for (int q = 0; q < RPT; ++q) {
-    const int r = threadIdx.x * RPT + q;
-    v[q] = r < R ? rowsum[r] : 0u;
-    sum += v[q];
-  }
+  if (lane == 0) counts[scan_rowsum_off(R, GS) + r] = base;
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(1 << BITS) k_row_total_scan(uint32_t* counts, uint32_t GS) {
+  constexpr int R = 1 << BITS;
+  __shared__ uint32_t scratch[R / 32 + 1];
+  __shared__ float fscr[R / 32];
+  const uint32_t r = threadIdx.x;
+  const uint32_t v = counts[scan_rowsum_off(R, GS) + r];
   uint32_t tot;
-  uint32_t run = block_excl_sum<kScanThreads>(sum, scratch, &tot);
-  float e = 0.f;
-#pragma unroll
-  for (int q = 0; q < RPT; ++q) {
-    const int r = threadIdx.x * RPT + q;
-    if (r < R) {
-      e += 1.f - __powf(1.f - (float)v[q] / (float)max(tot, 1u), 32.f);
-      rowsum[r] = run;  // exclusive start of row r
-      run += v[q];
-    }
-  }
+  const uint32_t start = block_excl_sum<R>(v, scratch, &tot);
+  counts[scan_rowstart_off(R, GS) + r] = start;
+  float e = 1.f - __powf(1.f - (float)v / (float)max(tot, 1u), 32.f);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(kFull, e, o);
-  if (lane == 0) fscr[warp] = e;
+  if (lane_id() == 0) fscr[r >> 5] = e;
   __syncthreads();
-  for (int r = warp; r < R; r += NWS) {
-    uint32_t* row = counts + (uint64_t)r * GS;
-    uint32_t base = rowsum[r];
-    for (uint32_t q0 = 0; q0 < GS; q0 += 32) {
-      const uint32_t q = q0 + lane;
-      const uint32_t x = q < GS ? row[q] : 0u;
-      const uint32_t incl = warp_incl_sum(x);
-      if (q < GS) row[q] = base + incl - x;
-      base += __shfl_sync(kFull, incl, 31);
-    }
-  }
-  if (threadIdx.x == 0) {
+  if (r == 0) {
     float E = 0.f;
-    for (int w = 0; w < NWS; ++w) E += fscr[w];
-    counts[(uint64_t)R * GS] = E > kBallotE ? 1u : 0u;
+    for (int w = 0; w < R / 32; ++w) E += fscr[w];
+    counts[scan_ballot_off(R, GS)] = E > kBallotE ? 1u : 0u;
   }
 }
 
@@ -428,7 +419,7 @@ struct DownSmem {
 // Stable rank of item i within its warp's items of equal digit.  Peers come
 // from __match_any_sync (cost grows with the number of distinct digits in
 // the warp) or from BITS ballots (constant cost); `ballot` is chosen per
-// pass from the digit distribution (k_chunk_scan).  All peers read the warp
+// pass from the digit distribution (k_row_total_scan).  All peers read the warp
 // counter (broadcast), the lowest peer advances it.
 template <bool FULL, int BITS>
 __device__ __forceinline__ uint32_t warp_rank(uint32_t* whist, uint32_t d, bool valid, uint32_t lane,
@@ -551,7 +542,7 @@ k_downsweep(SweepArgs a, Loader ld, Emitter em) {
   const bool tma = loader_tma_ok(ld);
 
   for (int b = tid; b < R; b += BLOCK) {
-    m.run[b] = a.counts[(uint64_t)b * a.GS + blockIdx.x];
+    m.run[b] = a.counts[(uint64_t)b * a.GS + blockIdx.x] + a.counts[scan_rowstart_off(R, a.GS) + b];
 #pragma unroll
     for (int w = 0; w < NW; ++w) m.whist[w][b] = 0;
   }
@@ -559,7 +550,7 @@ k_downsweep(SweepArgs a, Loader ld, Emitter em) {
     mbar_init(&m.bar[0], 1);
     mbar_init(&m.bar[1], 1);
     mbar_fence_init();
-    m.ballot = a.counts[(uint64_t)R * a.GS];
+    m.ballot = a.counts[scan_ballot_off(R, a.GS)];
   }
   em.template init<BLOCK, R>(m.est);
   __syncthreads();

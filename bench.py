@@ -74,11 +74,14 @@ def kernel_bytes(stats, n: int, nv: int) -> dict[str, float]:
     kb = 4 if info["sort1_narrow"] else 8         # key bytes per item in the edge sort's passes
     item = kb + 12                                # key + (id, u, v) payload
     alpha = sum(c[0] for c in counts[:L])         # edges copied into the next view
+    local = info.get("sort1_local") == "smem"     # wide keys: 3 global passes + shared-memory finish
+    mids = 2 if local else max(p1 - 2, 0)
     return {
         "sort1_hist": 8.0 * n,                                  # read w
         "sort1_pass_first": (16.0 + item) * n,                  # read w, u, v 16; write key + payload
-        "sort1_pass_mid": 2.0 * item * n * max(p1 - 2, 0),      # read + write key + payload per pass
-        "sort1_pass_final": (item + 20.0) * n,                  # read; write orig_of 4, heights 8, euv 8
+        "sort1_pass_mid": 2.0 * item * n * mids,                # read + write key + payload per pass
+        "sort1_pass_final": 0.0 if local else (item + 20.0) * n,  # read; write orig_of 4, heights 8, euv 8
+        "sort1_local": (item + 20.0) * n if local else 0.0,     # read; write orig_of 4, heights 8, euv 8
         "upsweep_scan": float(kb) * n * max(p1 - 1, 0) + 8.0 * n * max(p2 - 1, 0) + 4.0 * n * min(p2, 1),
         "mi_hist": 4.0 * mb,                                    # read endpoints
         "mi_split_a": 16.0 * mb,                                # read 4 + write 12 per record

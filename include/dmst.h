@@ -89,10 +89,13 @@ typedef struct dmst_stats {
   int32_t sort1_compacted;  /* 1 = the sign/exponent field was replaced by its dense code */
   int32_t sort2_geometry_used; /* 0 = no chain sort (a single chain), else as sort2_geometry */
   int32_t tail_level;       /* first view finished inside k_tail, -1 = none */
+  int32_t sort1_local;      /* 1 = wide keys: top three digits sorted globally, the rest per
+                               window in shared memory; 2 = a window overflowed, full LSD ran */
   uint64_t mi_bucketed;     /* bit k: view k's maxIncident was bucketed */
   uint64_t mi_direct;       /* bit k: view k's maxIncident took direct atomics */
   /* in: kernel-variant switches for A/B measurement (0 = the default kernels;
-   * same bits either way).  None defined at present. */
+   * same bits either way).  8 = wide edge-sort keys never finish in shared
+   * memory (full LSD sort). */
   int32_t variant;
 } dmst_stats;
 

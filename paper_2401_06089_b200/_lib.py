@@ -64,6 +64,7 @@ class DmstStats(ctypes.Structure):
         ("sort1_compacted", ctypes.c_int32),
         ("sort2_geometry_used", ctypes.c_int32),
         ("tail_level", ctypes.c_int32),
+        ("sort1_local", ctypes.c_int32),
         ("mi_bucketed", ctypes.c_uint64),
         ("mi_direct", ctypes.c_uint64),
         ("variant", ctypes.c_int32),
@@ -82,7 +83,9 @@ class DmstStats(ctypes.Structure):
         """Which code path each stage took (bench.py's byte model reads this)."""
         L = int(self.num_levels)
         return {"sort1_passes": int(self.sort1_passes), "sort1_narrow": bool(self.sort1_narrow),
-                "sort1_compacted": bool(self.sort1_compacted), "sort2_passes": int(self.sort2_passes),
+                "sort1_compacted": bool(self.sort1_compacted),
+                "sort1_local": {0: None, 1: "smem", 2: "fallback"}[int(self.sort1_local)],
+                "sort2_passes": int(self.sort2_passes),
                 "sort2_geometry": SORT2_GEOMETRIES[int(self.sort2_geometry_used)],
                 "tail_level": int(self.tail_level),
                 "mi_bucketed_views": [k for k in range(L + 1) if (int(self.mi_bucketed) >> k) & 1],

@@ -61,13 +61,13 @@ constexpr int64_t kDirectMiBytes = 64ll << 20;  // direct scatter-max below this
 enum KernelKind {
   KK_SORT1_HIST, KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL, KK_MI_HIST, KK_MI_SPLIT_A, KK_MI_SPLIT_B,
   KK_MI_APPLY, KK_V1, KK_LEAFSCAN, KK_V2, KK_JUMP, KK_SELECT_EDGES, KK_WALK, KK_SORT2_PASS, KK_LINK_SPLIT,
-  KK_LINK_APPLY, KK_UPSWEEP, KK_TAIL, KK_OTHER, KK_COUNT
+  KK_LINK_APPLY, KK_UPSWEEP, KK_TAIL, KK_SORT1_LOCAL, KK_OTHER, KK_COUNT
 };
 static_assert(KK_COUNT <= DMST_MAX_KERNELS, "kernel kinds");
 const char* const kKernelNames[KK_COUNT] = {
     "sort1_hist", "sort1_pass_first", "sort1_pass_mid", "sort1_pass_final", "mi_hist", "mi_split_a",
     "mi_split_b", "mi_apply", "v1", "leafscan", "v2", "jump", "select_edges", "walk", "sort2_pass",
-    "link_split", "link_apply", "upsweep_scan", "tail", "other"};
+    "link_split", "link_apply", "upsweep_scan", "tail", "sort1_local", "other"};
 
 namespace {
 
@@ -129,7 +129,7 @@ constexpr int SM_HIST1 = 0, SM_GBASE1 = SM_HIST1 + 8 * kRadix, SM_HIST2 = SM_GBA
               SM_GBASE2 = SM_HIST2 + 4 * kRadix, SM_VHIST = SM_GBASE2 + 4 * kRadix,
               SM_VBASE = SM_VHIST + kRadix, SM_TILECTR = SM_VBASE + kRadix, SM_MISC = SM_TILECTR + 64;
 constexpr int MISC_NEGZERO = 0, MISC_ACTIVE0 = 1, MISC_ACTIVE1 = 2, MISC_ACTIVE2 = 3, MISC_COUNTS = 4 /*2*/,
-              MISC_NONRUL = 6, MISC_LSCTR = 13;
+              MISC_NONRUL = 6, MISC_LSCTR = 13, MISC_LOCALOVF = 16;
 
 Workspace carve(int64_t n, int64_t nv, char* base) {
   Workspace w{};
@@ -247,6 +247,7 @@ struct Paths {
   int variant = 0;
   // out
   int sort1_narrow = 0, sort1_compacted = 0, sort2_geometry_used = 0, tail_level = -1;
+  int sort1_local = 0;  // 1 = wide keys finished in shared memory, 2 = tried, fell back to full LSD
   uint64_t mi_bucketed = 0, mi_direct = 0;
 };
 
@@ -484,6 +485,9 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
   c.to_host(&tmin, top_min, 4);
   c.sync();
   const std::vector<int> guess = active_digits(sao[0], sao[1], 8, 64);
+  // the digit the fused upsweep counts: the first pass's (wide keys with >= 5
+  // active digits take the shared-memory finish, local_sort.cuh, whose first
+  // global digit is unaligned and counted by its own upsweep)
   const int d0 = guess.empty() ? 0 : guess[0];
   const SweepGeom g = sweep_geom(c, n, S1_BLOCK * S1_ITEMS, S1N_MINB, S1_ALIGN);
   SweepArgs a{};
@@ -526,7 +530,9 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
   }
   // the upsweep counted digit d0 of the raw keys: valid for the compacted
   // keys only below the top field
-  const int ready = !shifts.empty() && shifts[0] == d0 && (!code || d0 + 8 <= kTopShift) ? d0 : -1;
+  const bool local = shifts.size() >= 5 && !(c.paths.variant & 8);
+  const int first_shift = shifts.empty() ? -1 : local ? -2 : shifts[0];  // local: unaligned digits, own upsweep
+  const int ready = first_shift >= 0 && first_shift == d0 && (!code || d0 + 8 <= kTopShift) ? d0 : -1;
   if (passes_out) *passes_out = (int)shifts.size();
   char* R = c.w.R;
   uint32_t* vb = (uint32_t*)(R + 16 * n);
@@ -553,9 +559,37 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
         Sort1Loader<uint32_t>{w, u, v, code, (uint32_t)lo}, em32, ready >= 0 ? 0 : -1, S1_ALIGN);
   } else {
     uint64_t* const bufK[2] = {(uint64_t*)R, (uint64_t*)(R + 8 * n)};
-    run_sort<uint64_t, 3, S1_BLOCK, S1_ITEMS, S1_MINB, 8>(c, {KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL}, n,
-                                                       shifts, bufK, bufP, Sort1FirstLoader{w, u, v, code}, em,
-                                                       ready, S1_ALIGN, S1N_MINB);
+    bool done = false;
+    if (local && !narrow) {
+      // top three active digits as global LSD passes, the rest per window in
+      // shared memory; a window over capacity falls back to the full LSD sort
+      // the three global digits cover the 24 highest VARYING key bits
+      // (unaligned: sign/exponent bits that never vary are not spent on them)
+      const int hb = 63 - __builtin_clzll(var);
+      const int t0 = std::max(hb - 23, 0);
+      const std::vector<int> top3 = {t0, t0 + 8, t0 + 16};
+      ArrayEmitter<uint64_t, 3> tmp{bufK[0], bufP[0]};  // the third pass (p = 2) writes buffer 0
+      run_sort<uint64_t, 3, S1_BLOCK, S1_ITEMS, S1_MINB, 8>(c, {KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_MID}, n,
+                                                         top3, bufK, bufP, Sort1FirstLoader{w, u, v, code}, tmp,
+                                                         ready, S1_ALIGN, S1N_MINB);
+      uint32_t* ovf = c.w.small + SM_MISC + MISC_LOCALOVF;
+      c.zero(ovf, 4);
+      smem_attr(k_local_final<Sort1FinalEmitter>, sizeof(LocalSmem));
+      LocalSortArgs la{bufK[0], bufP[0], n, top3[0], ovf};
+      c.begin(KK_SORT1_LOCAL);
+      k_local_final<Sort1FinalEmitter><<<grid_for(n, kLocalTile), LF_BLOCK, sizeof(LocalSmem), c.s>>>(la, em);
+      c.launched();
+      uint32_t over = 0;
+      c.to_host(&over, ovf, 4);
+      c.sync();
+      done = over == 0;
+      c.paths.sort1_local = done ? 1 : 2;
+      if (passes_out) *passes_out = done ? 3 : (int)shifts.size();
+    }
+    if (!done)
+      run_sort<uint64_t, 3, S1_BLOCK, S1_ITEMS, S1_MINB, 8>(c, {KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL}, n,
+                                                         shifts, bufK, bufP, Sort1FirstLoader{w, u, v, code}, em,
+                                                         local ? -1 : ready, S1_ALIGN, S1N_MINB);
   }
   if (nz) {
     c.begin(KK_OTHER);
@@ -970,6 +1004,7 @@ void report_paths(const Ctx& c, dmst_stats* st) {
   if (!st) return;
   st->sort1_narrow = c.paths.sort1_narrow;
   st->sort1_compacted = c.paths.sort1_compacted;
+  st->sort1_local = c.paths.sort1_local;
   st->sort2_geometry_used = c.paths.sort2_geometry_used;
   st->tail_level = c.paths.tail_level;
   st->mi_bucketed = c.paths.mi_bucketed;

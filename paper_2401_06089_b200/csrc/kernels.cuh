@@ -154,24 +154,30 @@ struct Sort1Emitter {
   const uint16_t* __restrict__ inv;  // top-field compaction: code -> top field (or nullptr)
   uint64_t base;                     // narrow keys: the constant bits outside [lo, lo + 32)
   uint32_t lo;
+  // rank r <- item (key kn, original id, u, v)
+  __device__ __forceinline__ void put(uint32_t r, K kn, uint32_t id, uint32_t eu, uint32_t ev) const {
+    const uint64_t k = base | ((uint64_t)kn << lo);
+    orig_of[r] = (int32_t)id;
+    heights[r] = key_to_double(inv ? ((uint64_t)__ldg(inv + (k >> kTopShift)) << kTopShift) | (k & kMantMask) : k);
+    if (euv) euv[r] = make_int2((int)eu, (int)ev);
+    if (ru) {
+      ru[r] = (int32_t)eu;
+      rv[r] = (int32_t)ev;
+    }
+  }
   template <int BLOCK, class Tile>
   __device__ __forceinline__ void emit(const Tile& t, State&) const {
     for (int s = threadIdx.x; s < t.cnt; s += BLOCK) {
       const K kn = t.skeys[s];
-      const uint32_t r = t.gofs[digit_of<kRadixBits>(kn, t.shift)] + (uint32_t)s;
       const uint32_t* p = t.spay + 3 * s;
-      const uint64_t k = base | ((uint64_t)kn << lo);
-      orig_of[r] = (int32_t)p[0];
-      heights[r] = key_to_double(inv ? ((uint64_t)__ldg(inv + (k >> kTopShift)) << kTopShift) | (k & kMantMask) : k);
-      if (euv) euv[r] = make_int2((int)p[1], (int)p[2]);
-      if (ru) {
-        ru[r] = (int32_t)p[1];
-        rv[r] = (int32_t)p[2];
-      }
+      put(t.gofs[digit_of<kRadixBits>(kn, t.shift)] + (uint32_t)s, kn, p[0], p[1], p[2]);
     }
   }
 };
 using Sort1FinalEmitter = Sort1Emitter<uint64_t>;
+}  // namespace dmst
+#include "local_sort.cuh"
+namespace dmst {
 
 // Compaction tables from the top-field presence bitmap (128 words, 4096
 // bits): code[t] = number of present top fields below t, inv[code] = t.

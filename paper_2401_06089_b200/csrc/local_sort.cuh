@@ -1,0 +1,277 @@
+// Edge sort, wide keys: finish the sort inside shared memory.
+//
+// A 64-bit-key edge sort (uniform float64 weights: 8 active digits) runs only
+// its three TOP active digits as global LSD passes; the items are then
+// ordered by `key >> pshift` (pshift = the lowest of those digits), with the
+// original id order inside every run of equal prefix (stable passes).  Runs
+// are short for spread-out weights (~250 items per run at 128M uniform
+// weights), so one kernel finishes the sort: each CTA takes the runs that
+// START in its 2048-item tile (a window of at most kLocalCap items) and sorts
+// the window by (key, position in window) — the position breaks ties exactly
+// as the original id does — then writes the RankedTree outputs for its window
+// directly (orig_of, heights, rank-order endpoints).  Five global passes
+// over 20-B items become one read, one write and on-chip work.
+//
+// In-window sort: a counting sort on the top (up to 11) bits that vary in
+// the window scatters the keys into ~1-item buckets (shared-memory atomics,
+// order-free), then every item's final slot is its bucket start plus the
+// number of bucket members below it in (key, position) order (one thread per
+// item, no dependent chains).  A window whose largest bucket exceeds kLocalBucketMax
+// (clustered keys) is sorted instead by stable 8-bit LSD passes over its
+// varying bits (ranking as in k_downsweep).  A window longer than kLocalCap
+// (a run of equal top bits that large: heavily tied or clustered weights)
+// sets `overflow`; the host then re-runs the plain LSD sort, which produces
+// the same bits.
+//
+// Replaces `np.argsort(-w, kind="stable")` (tree_core.py:180 of
+// /root/reference/pkg/src/dendromst/) together with radix.cuh.
+#pragma once
+#include "common.cuh"
+#include "radix.cuh"
+
+namespace dmst {
+
+constexpr int LF_BLOCK = 512, LF_ITEMS = 8;
+constexpr int kLocalCap = LF_BLOCK * LF_ITEMS;  // 4096 items per window
+constexpr int kLocalTile = 2048;                // windows start at the first run start of each tile
+constexpr int kLocalBucketBits = 11;            // counting-sort buckets (2048)
+constexpr int kLocalBucketMax = 24;             // larger bucket -> LSD passes for the window
+
+struct LocalSortArgs {
+  const uint64_t* __restrict__ keys;  // [n], sorted by key >> pshift (stable)
+  const uint32_t* __restrict__ pay;   // [3 n] (original id, u, v)
+  int64_t n;
+  int pshift;
+  uint32_t* __restrict__ overflow;    // set to 1 when a window exceeds kLocalCap
+};
+
+struct LocalSmem {
+  uint64_t okey[kLocalCap];
+  uint16_t oidx[kLocalCap];
+  union {
+    struct {
+      uint32_t cnt[1 << kLocalBucketBits];
+      uint32_t cur[1 << kLocalBucketBits];
+    } cs;
+    struct {
+      uint32_t whist[LF_BLOCK / 32][kRadix];
+      uint32_t lstart[kRadix + 1];
+    } lsd;
+  } u;
+  uint32_t scan[LF_BLOCK / 32 + 1];
+  unsigned long long red[2][LF_BLOCK / 32];
+  unsigned long long found[2];
+  uint32_t maxb;
+};
+
+template <class Emitter>
+__global__ void __launch_bounds__(LF_BLOCK) k_local_final(LocalSortArgs a, Emitter em) {
+  constexpr int NW = LF_BLOCK / 32, R = kRadix, NB = 1 << kLocalBucketBits;
+  extern __shared__ __align__(16) unsigned char lsm[];
+  LocalSmem& s = *reinterpret_cast<LocalSmem*>(lsm);
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t lo = (int64_t)blockIdx.x * kLocalTile;
+  const int64_t hi = min(a.n, lo + kLocalTile);
+
+  // ---- window [start, end): the runs starting in [lo, hi).  Half the
+  // threads look for the first run start at or after lo, half after hi.
+  constexpr unsigned long long kNone = ~0ull;
+  if (tid < 2) s.found[tid] = kNone;
+  if (tid == 0) s.maxb = 0;
+  __syncthreads();
+  for (int step = 0;; ++step) {
+    const int half = tid >> 8;
+    const int64_t base = (half ? hi : lo) + (int64_t)step * 256;
+    const int64_t limit = half ? kLocalCap : kLocalTile;
+    const int64_t j = base + (tid & 255);
+    if (s.found[half] == kNone && (int64_t)step * 256 < limit && j < a.n) {
+      const bool st = j == 0 || (ld_stream(a.keys + j) >> a.pshift) != (ld_stream(a.keys + j - 1) >> a.pshift);
+      if (st) atomicMin(&s.found[half], (unsigned long long)j);
+    }
+    __syncthreads();
+    const int64_t nxt = (int64_t)(step + 1) * 256;
+    const bool d0 = s.found[0] != kNone || nxt >= kLocalTile || lo + nxt >= a.n;
+    const bool d1 = s.found[1] != kNone || nxt >= kLocalCap || hi + nxt >= a.n;
+    if (d0 && d1) break;
+  }
+  const int64_t start = s.found[0] == kNone ? -1 : (int64_t)s.found[0];
+  int64_t end = s.found[1] != kNone ? (int64_t)s.found[1] : (hi + kLocalCap >= a.n ? a.n : -1);
+  if (start < 0 || start >= hi) return;  // no run starts in this tile
+  if (end < 0 || end - start > kLocalCap) {
+    if (tid == 0) atomicOr(a.overflow, 1u);
+    return;
+  }
+  const int W = (int)(end - start);
+  const int ipw = (W + NW * 32 - 1) / (NW * 32);  // items per lane actually used (<= LF_ITEMS)
+  const int wbase = warp * ipw * 32 + lane;
+
+  // ---- keys -> registers (blocked by warp); bits varying in the window
+  uint64_t k[LF_ITEMS];
+  uint32_t x[LF_ITEMS];
+  uint64_t ka = ~0ull, ko = 0ull;
+#pragma unroll
+  for (int q = 0; q < LF_ITEMS; ++q) {
+    const int idx = wbase + q * 32;
+    k[q] = ~0ull;
+    x[q] = (uint32_t)idx;
+    if (q < ipw && idx < W) {
+      k[q] = ld_stream(a.keys + start + idx);
+      ka &= k[q];
+      ko |= k[q];
+    }
+  }
+  ka = (unsigned long long)__reduce_and_sync(kFull, (uint32_t)ka) |
+       ((unsigned long long)__reduce_and_sync(kFull, (uint32_t)(ka >> 32)) << 32);
+  ko = (unsigned long long)__reduce_or_sync(kFull, (uint32_t)ko) |
+       ((unsigned long long)__reduce_or_sync(kFull, (uint32_t)(ko >> 32)) << 32);
+  if (lane == 0) {
+    s.red[0][warp] = ka;
+    s.red[1][warp] = ko;
+  }
+  for (int b = tid; b < NB; b += LF_BLOCK) s.u.cs.cnt[b] = 0;
+  __syncthreads();
+  uint64_t va = ~0ull, vo = 0ull;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    va &= s.red[0][w];
+    vo |= s.red[1][w];
+  }
+  const uint64_t var = va ^ vo;
+  const int lob = var ? __ffsll((long long)var) - 1 : 64;
+  const int hib = var ? 63 - __clzll((long long)var) : -1;
+
+  if (var) {
+    // ---- counting sort on the top varying bits
+    const int nb = min(kLocalBucketBits, hib - lob + 1);
+    const int bsh = hib - nb + 1;
+    const uint32_t bmask = (1u << nb) - 1u;
+#pragma unroll
+    for (int q = 0; q < LF_ITEMS; ++q)
+      if (q < ipw && wbase + q * 32 < W) atomicAdd(&s.u.cs.cnt[(uint32_t)(k[q] >> bsh) & bmask], 1u);
+    __syncthreads();
+    constexpr int BPT = NB / LF_BLOCK;  // buckets per thread (consecutive)
+    uint32_t c[BPT], sum = 0, mx = 0;
+#pragma unroll
+    for (int q = 0; q < BPT; ++q) {
+      c[q] = s.u.cs.cnt[tid * BPT + q];
+      sum += c[q];
+      mx = max(mx, c[q]);
+    }
+    mx = __reduce_max_sync(kFull, mx);
+    if (lane == 0 && mx) atomicMax(&s.maxb, mx);
+    uint32_t tot;
+    uint32_t run = block_excl_sum<LF_BLOCK>(sum, s.scan, &tot);
+#pragma unroll
+    for (int q = 0; q < BPT; ++q) {
+      s.u.cs.cnt[tid * BPT + q] = run;  // bucket start
+      s.u.cs.cur[tid * BPT + q] = run;
+      run += c[q];
+    }
+    __syncthreads();
+    if (s.maxb <= (uint32_t)kLocalBucketMax) {
+      // scatter into the buckets (order-free), then every item counts the
+      // bucket members below it in (key, position) order: its final slot
+      uint32_t bk[LF_ITEMS];
+#pragma unroll
+      for (int q = 0; q < LF_ITEMS; ++q) {
+        if (q < ipw && wbase + q * 32 < W) {
+          bk[q] = (uint32_t)(k[q] >> bsh) & bmask;
+          const uint32_t p = atomicAdd(&s.u.cs.cur[bk[q]], 1u);
+          s.okey[p] = k[q];
+          s.oidx[p] = (uint16_t)x[q];
+        }
+      }
+      __syncthreads();
+      uint32_t pos[LF_ITEMS];
+#pragma unroll
+      for (int q = 0; q < LF_ITEMS; ++q) {
+        if (q < ipw && wbase + q * 32 < W) {
+          const int b0 = (int)s.u.cs.cnt[bk[q]], b1 = (int)s.u.cs.cur[bk[q]];
+          uint32_t r = 0;
+          for (int j = b0; j < b1; ++j) {
+            const uint64_t kj = s.okey[j];
+            r += kj < k[q] || (kj == k[q] && s.oidx[j] < x[q]);
+          }
+          pos[q] = (uint32_t)b0 + r;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < LF_ITEMS; ++q) {
+        if (q < ipw && wbase + q * 32 < W) {
+          s.okey[pos[q]] = k[q];
+          s.oidx[pos[q]] = (uint16_t)x[q];
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < LF_ITEMS; ++q) {
+        const int idx = wbase + q * 32;
+        if (q < ipw) {
+          k[q] = s.okey[idx];
+          x[q] = s.oidx[idx];
+        }
+      }
+    } else {
+      // ---- clustered window: stable LSD passes over its varying bits;
+      // padding keys (all ones) stay behind the window's items
+      const uint32_t lt = lanemask_lt();
+      for (int b = tid; b < NW * R; b += LF_BLOCK) (&s.u.lsd.whist[0][0])[b] = 0;
+      __syncthreads();
+      for (int sh = lob; sh <= hib; sh += kRadixBits) {
+        uint32_t rk[LF_ITEMS];
+#pragma unroll
+        for (int q = 0; q < LF_ITEMS; ++q)
+          if (q < ipw)
+            rk[q] = warp_rank<true, kRadixBits>(s.u.lsd.whist[warp], digit_of(k[q], sh), true, lane, lt, true);
+        __syncthreads();
+        uint32_t cc = 0;
+        if (tid < R) {
+#pragma unroll
+          for (int w = 0; w < NW; ++w) {
+            const uint32_t y = s.u.lsd.whist[w][tid];
+            s.u.lsd.whist[w][tid] = cc;
+            cc += y;
+          }
+        }
+        uint32_t t2;
+        const uint32_t ls = block_excl_sum<LF_BLOCK>(tid < R ? cc : 0u, s.scan, &t2);
+        if (tid < R) s.u.lsd.lstart[tid] = ls;
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < LF_ITEMS; ++q) {
+          if (q < ipw) {
+            const uint32_t d = digit_of(k[q], sh);
+            const uint32_t p = s.u.lsd.lstart[d] + s.u.lsd.whist[warp][d] + rk[q];
+            s.okey[p] = k[q];
+            s.oidx[p] = (uint16_t)x[q];
+          }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < LF_ITEMS; ++q) {
+          if (q < ipw) {
+            const int idx = wbase + q * 32;
+            k[q] = s.okey[idx];
+            x[q] = s.oidx[idx];
+          }
+        }
+        for (int b = tid; b < NW * R; b += LF_BLOCK) (&s.u.lsd.whist[0][0])[b] = 0;
+        __syncthreads();
+      }
+    }
+  }
+  // ---- window position idx -> global rank start + idx (payload from the
+  // window's 12-B records, L2-resident)
+  const uint32_t* pw = a.pay + 3 * start;
+#pragma unroll
+  for (int q = 0; q < LF_ITEMS; ++q) {
+    const int idx = wbase + q * 32;
+    if (q < ipw && idx < W) {
+      const uint32_t* p = pw + 3 * x[q];
+      em.put((uint32_t)(start + idx), k[q], __ldg(p), __ldg(p + 1), __ldg(p + 2));
+    }
+  }
+}
+
+}  // namespace dmst

@@ -42,6 +42,8 @@ PATHS = {
     "wide_sort_large_s2": {"sort1_mode": 3, "sort2_geometry": 2},
     # narrow keys without compaction; 512 x 16 chain-sort tiles; no tail, bucketed
     "nocompact_bucketed": {"sort1_mode": 2, "sort2_geometry": 1, "direct_mi_bytes": -1, "tail_edges": -1},
+    # wide keys always sorted by the full LSD (no shared-memory finish)
+    "no_local": {"variant": 8},
 }
 
 SEEN_KINDS: dict[str, int] = {}   # kernel kind -> launches inside checked builds
@@ -104,6 +106,8 @@ def _assert_path_taken(res, paths):
         assert not info["sort1_narrow"]
     if p.get("sort1_mode", 0) & 2:
         assert not info["sort1_compacted"]
+    if p.get("variant", 0) & 8:
+        assert info["sort1_local"] is None
     if p.get("sort2_geometry") and info["sort2_passes"]:
         from paper_2401_06089_b200._lib import SORT2_GEOMETRIES
         assert info["sort2_geometry"] == SORT2_GEOMETRIES[p["sort2_geometry"]]
@@ -167,6 +171,55 @@ def test_deep_in_trees_all_paths(builder, paths):
         _check(builder, nv, u, v, w, _oracle_full(nv, u, v, w), paths)
 
 
+def _local_weights(kind: str, n: int, rng):
+    """Weight sets for the wide-key edge sort that finishes in shared memory
+    (>= 5 active 8-bit digits) and for its fallback (a run of equal top
+    digits longer than one window)."""
+    if kind == "uniform":
+        return rng.random(n)
+    if kind == "spread":          # both signs, 40 binades: long compacted codes, many digits
+        return rng.standard_normal(n) * np.exp2(rng.integers(-20, 20, n))
+    if kind == "clustered":       # 1% of the weights in a band 2^-30 wide: runs of ~1000 items
+        w = rng.random(n)
+        m = rng.random(n) < 0.01
+        w[m] = 0.5 + rng.random(int(m.sum())) * 2.0 ** -30
+        return w
+    if kind == "overflow":        # 30% equal weights among uniform ones: one run >> a window
+        w = rng.random(n)
+        w[rng.random(n) < 0.3] = 0.25
+        return w
+    if kind == "near_cap":        # runs just below / above the 8192-item window
+        w = rng.random(n)
+        for c, size in enumerate((1900, 4000, 4500)):
+            size = min(size, n // 4)
+            idx = rng.choice(n, size, replace=False)
+            w[idx] = 0.125 * (c + 1) + rng.random(size) * 2.0 ** -40
+        return w
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "spread", "clustered", "overflow", "near_cap"])
+@pytest.mark.parametrize("n", [3000, 70_000, 1_000_000])
+def test_wide_key_local_sort(builder, kind, n):
+    # the wide-key edge sort that finishes per window in shared memory
+    # (local_sort.cuh) and its fallback, against the oracle and against the
+    # forced full LSD sort (variant 8): same bits either way
+    rng = np.random.default_rng(n + len(kind))
+    nv, u, v, _ = synth.random_attach(n, seed=n % 97)
+    w = _local_weights(kind, n, rng)
+    exp = _oracle_full(nv, u, v, w)
+    res = _check(builder, nv, u, v, w, exp, "default", debug=False)
+    full = _check(builder, nv, u, v, w, exp, "no_local", debug=False)
+    info, finfo = res.stats.path_info(), full.stats.path_info()
+    assert finfo["sort1_local"] is None
+    if res.stats.sort1_passes >= 5 or info["sort1_local"]:
+        assert info["sort1_local"] in ("smem", "fallback")
+    if kind == "overflow" and n >= 70_000:
+        assert info["sort1_local"] == "fallback"
+    if kind in ("uniform", "spread") and n >= 70_000:
+        assert info["sort1_local"] == "smem"
+
+
 def test_rejects_bad_path_options(builder):
     nv, u, v, w = synth.random_attach(100, seed=1)
     with pytest.raises(ValueError):
@@ -180,7 +233,7 @@ def test_rejects_bad_path_options(builder):
 def test_every_kernel_kind_was_checked():
     # every kernel kind the 128M headline build launches (profiles/launches_r*_summary.csv)
     # has run inside a bit-exact comparison above; "other" (memset-like helpers) aside
-    need = {"sort1_hist", "sort1_pass_first", "sort1_pass_mid", "sort1_pass_final", "mi_hist",
+    need = {"sort1_hist", "sort1_pass_first", "sort1_pass_mid", "sort1_pass_final", "sort1_local", "mi_hist",
             "mi_split_a", "mi_split_b", "mi_apply", "v1", "leafscan", "v2", "jump", "select_edges",
             "walk", "sort2_pass", "link_split", "link_apply", "upsweep_scan", "tail"}
     if not SEEN_KINDS:

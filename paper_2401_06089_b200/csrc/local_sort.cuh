@@ -6,14 +6,15 @@
 // original id order inside every run of equal prefix (stable passes).  Runs
 // are short for spread-out weights (~250 items per run at 128M uniform
 // weights), so one kernel finishes the sort: each CTA takes the runs that
-// START in its 2048-item tile (a window of at most kLocalCap items) and sorts
+// START in its 2048-item tile (the window must end within kLocalCap items of
+// the tile start) and sorts
 // the window by (key, position in window) — the position breaks ties exactly
 // as the original id does — then writes the RankedTree outputs for its window
 // directly (orig_of, heights, rank-order endpoints).  Five global passes
 // over 20-B items become one read, one write and on-chip work.
 //
-// In-window sort: a counting sort on the top (up to 11) bits that vary in
-// the window scatters the keys into ~1-item buckets (shared-memory atomics,
+// In-window sort: a counting sort on (key - window minimum) >> shift (4096
+// buckets over the window's key range) scatters the keys into ~1-item buckets (shared-memory atomics,
 // order-free), then every item's final slot is its bucket start plus the
 // number of bucket members below it in (key, position) order (one thread per
 // item, no dependent chains).  A window whose largest bucket exceeds kLocalBucketMax
@@ -34,7 +35,7 @@ namespace dmst {
 constexpr int LF_BLOCK = 512, LF_ITEMS = 8;
 constexpr int kLocalCap = LF_BLOCK * LF_ITEMS;  // 4096 items per window
 constexpr int kLocalTile = 2048;                // windows start at the first run start of each tile
-constexpr int kLocalBucketBits = 11;            // counting-sort buckets (2048)
+constexpr int kLocalBucketBits = 12;            // counting-sort buckets (4096)
 constexpr int kLocalBucketMax = 24;             // larger bucket -> LSD passes for the window
 
 struct LocalSortArgs {
@@ -59,7 +60,7 @@ struct LocalSmem {
     } lsd;
   } u;
   uint32_t scan[LF_BLOCK / 32 + 1];
-  unsigned long long red[2][LF_BLOCK / 32];
+  unsigned long long red[4][LF_BLOCK / 32];
   unsigned long long found[2];
   uint32_t maxb;
 };
@@ -73,81 +74,103 @@ __global__ void __launch_bounds__(LF_BLOCK) k_local_final(LocalSortArgs a, Emitt
   const int64_t lo = (int64_t)blockIdx.x * kLocalTile;
   const int64_t hi = min(a.n, lo + kLocalTile);
 
-  // ---- window [start, end): the runs starting in [lo, hi).  Half the
-  // threads look for the first run start at or after lo, half after hi.
-  constexpr unsigned long long kNone = ~0ull;
-  if (tid < 2) s.found[tid] = kNone;
+  // ---- window [start, end): the runs starting in [lo, hi), found from the
+  // keys [lo - 1, lo + kLocalCap) staged once in shared memory (the window
+  // must end by lo + kLocalCap; a run start is where key >> pshift changes)
+  const int64_t stage_end = min(a.n, lo + kLocalCap);
+  const int nst = (int)(stage_end - lo);
+  for (int i = tid; i < nst; i += LF_BLOCK) s.okey[i] = ld_stream(a.keys + lo + i);
+  uint64_t before = 0;
+  if (lo > 0) before = ld_stream(a.keys + lo - 1) >> a.pshift;
+  if (tid < 2) s.found[tid] = ~0ull;
   if (tid == 0) s.maxb = 0;
   __syncthreads();
-  for (int step = 0;; ++step) {
-    const int half = tid >> 8;
-    const int64_t base = (half ? hi : lo) + (int64_t)step * 256;
-    const int64_t limit = half ? kLocalCap : kLocalTile;
-    const int64_t j = base + (tid & 255);
-    if (s.found[half] == kNone && (int64_t)step * 256 < limit && j < a.n) {
-      const bool st = j == 0 || (ld_stream(a.keys + j) >> a.pshift) != (ld_stream(a.keys + j - 1) >> a.pshift);
-      if (st) atomicMin(&s.found[half], (unsigned long long)j);
+  {
+    const int tile = (int)(hi - lo);
+    uint32_t f0 = 0xffffffffu, f1 = 0xffffffffu;
+    for (int i = tid; i < nst; i += LF_BLOCK) {
+      const uint64_t pv = i ? s.okey[i - 1] >> a.pshift : before;
+      const bool st = (lo + i == 0) || (s.okey[i] >> a.pshift) != pv;
+      if (st) {
+        if (i < tile) f0 = min(f0, (uint32_t)i);
+        else f1 = min(f1, (uint32_t)i);
+      }
     }
-    __syncthreads();
-    const int64_t nxt = (int64_t)(step + 1) * 256;
-    const bool d0 = s.found[0] != kNone || nxt >= kLocalTile || lo + nxt >= a.n;
-    const bool d1 = s.found[1] != kNone || nxt >= kLocalCap || hi + nxt >= a.n;
-    if (d0 && d1) break;
+    f0 = __reduce_min_sync(kFull, f0);
+    f1 = __reduce_min_sync(kFull, f1);
+    if (lane == 0) {
+      if (f0 != 0xffffffffu) atomicMin(&s.found[0], (unsigned long long)f0);
+      if (f1 != 0xffffffffu) atomicMin(&s.found[1], (unsigned long long)f1);
+    }
   }
-  const int64_t start = s.found[0] == kNone ? -1 : (int64_t)s.found[0];
-  int64_t end = s.found[1] != kNone ? (int64_t)s.found[1] : (hi + kLocalCap >= a.n ? a.n : -1);
-  if (start < 0 || start >= hi) return;  // no run starts in this tile
-  if (end < 0 || end - start > kLocalCap) {
+  __syncthreads();
+  if (s.found[0] == ~0ull) return;  // no run starts in this tile
+  const int64_t start = lo + (int64_t)s.found[0];
+  const int64_t end = s.found[1] != ~0ull ? lo + (int64_t)s.found[1] : (stage_end == a.n ? a.n : -1);
+  if (end < 0) {  // the window runs past the staged keys: over capacity
     if (tid == 0) atomicOr(a.overflow, 1u);
     return;
   }
   const int W = (int)(end - start);
+  const int woff = (int)(start - lo);
   const int ipw = (W + NW * 32 - 1) / (NW * 32);  // items per lane actually used (<= LF_ITEMS)
   const int wbase = warp * ipw * 32 + lane;
 
   // ---- keys -> registers (blocked by warp); bits varying in the window
   uint64_t k[LF_ITEMS];
   uint32_t x[LF_ITEMS];
-  uint64_t ka = ~0ull, ko = 0ull;
+  uint64_t ka = ~0ull, ko = 0ull, kmin = ~0ull, kmax = 0ull;
 #pragma unroll
   for (int q = 0; q < LF_ITEMS; ++q) {
     const int idx = wbase + q * 32;
     k[q] = ~0ull;
     x[q] = (uint32_t)idx;
     if (q < ipw && idx < W) {
-      k[q] = ld_stream(a.keys + start + idx);
+      k[q] = s.okey[woff + idx];
       ka &= k[q];
       ko |= k[q];
+      kmin = min(kmin, k[q]);
+      kmax = max(kmax, k[q]);
     }
   }
-  ka = (unsigned long long)__reduce_and_sync(kFull, (uint32_t)ka) |
-       ((unsigned long long)__reduce_and_sync(kFull, (uint32_t)(ka >> 32)) << 32);
-  ko = (unsigned long long)__reduce_or_sync(kFull, (uint32_t)ko) |
-       ((unsigned long long)__reduce_or_sync(kFull, (uint32_t)(ko >> 32)) << 32);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ka &= __shfl_xor_sync(kFull, ka, o);
+    ko |= __shfl_xor_sync(kFull, ko, o);
+    kmin = min(kmin, __shfl_xor_sync(kFull, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(kFull, kmax, o));
+  }
   if (lane == 0) {
     s.red[0][warp] = ka;
     s.red[1][warp] = ko;
+    s.red[2][warp] = kmin;
+    s.red[3][warp] = kmax;
   }
   for (int b = tid; b < NB; b += LF_BLOCK) s.u.cs.cnt[b] = 0;
   __syncthreads();
-  uint64_t va = ~0ull, vo = 0ull;
+  uint64_t va = ~0ull, vo = 0ull, vmin = ~0ull, vmax = 0ull;
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
     va &= s.red[0][w];
     vo |= s.red[1][w];
+    vmin = min(vmin, (uint64_t)s.red[2][w]);
+    vmax = max(vmax, (uint64_t)s.red[3][w]);
   }
   const uint64_t var = va ^ vo;
   const int lob = var ? __ffsll((long long)var) - 1 : 64;
   const int hib = var ? 63 - __clzll((long long)var) : -1;
 
   if (var) {
-    // ---- counting sort on the top varying bits
-    const int nb = min(kLocalBucketBits, hib - lob + 1);
-    const int bsh = hib - nb + 1;
-    const uint32_t bmask = (1u << nb) - 1u;
+    // ---- counting sort on (key - min) >> bsh: 2^kLocalBucketBits buckets
+    // spread over the window's key range (a monotone map of the key)
+    const uint64_t span = vmax - vmin;
+    const int sbits = 64 - __clzll((long long)span);  // bits of the range (>= 1: var != 0)
+    const int bsh = max(sbits - kLocalBucketBits, 0);
+    const uint32_t bmask = (1u << kLocalBucketBits) - 1u;
+    auto bucket_of = [&](uint64_t kk) { return (uint32_t)((kk - vmin) >> bsh) & bmask; };
 #pragma unroll
     for (int q = 0; q < LF_ITEMS; ++q)
-      if (q < ipw && wbase + q * 32 < W) atomicAdd(&s.u.cs.cnt[(uint32_t)(k[q] >> bsh) & bmask], 1u);
+      if (q < ipw && wbase + q * 32 < W) atomicAdd(&s.u.cs.cnt[bucket_of(k[q])], 1u);
     __syncthreads();
     constexpr int BPT = NB / LF_BLOCK;  // buckets per thread (consecutive)
     uint32_t c[BPT], sum = 0, mx = 0;
@@ -175,7 +198,7 @@ __global__ void __launch_bounds__(LF_BLOCK) k_local_final(LocalSortArgs a, Emitt
 #pragma unroll
       for (int q = 0; q < LF_ITEMS; ++q) {
         if (q < ipw && wbase + q * 32 < W) {
-          bk[q] = (uint32_t)(k[q] >> bsh) & bmask;
+          bk[q] = bucket_of(k[q]);
           const uint32_t p = atomicAdd(&s.u.cs.cur[bk[q]], 1u);
           s.okey[p] = k[q];
           s.oidx[p] = (uint16_t)x[q];

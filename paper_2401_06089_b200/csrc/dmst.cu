@@ -574,11 +574,19 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
                                                          ready, S1_ALIGN, S1N_MINB);
       uint32_t* ovf = c.w.small + SM_MISC + MISC_LOCALOVF;
       c.zero(ovf, 4);
-      smem_attr(k_local_final<Sort1FinalEmitter>, sizeof(LocalSmem));
       LocalSortArgs la{bufK[0], bufP[0], n, top3[0], ovf};
-      c.begin(KK_SORT1_LOCAL);
-      k_local_final<Sort1FinalEmitter><<<grid_for(n, kLocalTile), LF_BLOCK, sizeof(LocalSmem), c.s>>>(la, em);
-      c.launched();
+      auto launch_local = [&](auto geom) {
+        using G = decltype(geom);
+        auto kern = k_local_final<Sort1FinalEmitter, G>;
+        smem_attr(kern, sizeof(LocalSmem<G>));
+        c.begin(KK_SORT1_LOCAL);
+        kern<<<grid_for(n, G::kLocalTile), G::LF_BLOCK, sizeof(LocalSmem<G>), c.s>>>(la, em);
+        c.launched();
+      };
+      if (c.paths.variant & 32)
+        launch_local(LocalGeom<512, 8, 2048, 11>{});
+      else
+        launch_local(LocalGeomDefault{});
       uint32_t over = 0;
       c.to_host(&over, ovf, 4);
       c.sync();

@@ -13,8 +13,8 @@
 // directly (orig_of, heights, rank-order endpoints).  Five global passes
 // over 20-B items become one read, one write and on-chip work.
 //
-// In-window sort: a counting sort on (key - window minimum) >> shift (4096
-// buckets over the window's key range) scatters the keys into ~1-item buckets (shared-memory atomics,
+// In-window sort: a counting sort on (key - window base) >> shift (4096
+// buckets over the key range of the window's runs) scatters the keys into ~1-item buckets (shared-memory atomics,
 // order-free), then every item's final slot is its bucket start plus the
 // number of bucket members below it in (key, position) order (one thread per
 // item, no dependent chains).  A window whose largest bucket exceeds kLocalBucketMax
@@ -32,11 +32,15 @@
 
 namespace dmst {
 
-constexpr int LF_BLOCK = 512, LF_ITEMS = 8;
-constexpr int kLocalCap = LF_BLOCK * LF_ITEMS;  // 4096 items per window
-constexpr int kLocalTile = 2048;                // windows start at the first run start of each tile
-constexpr int kLocalBucketBits = 12;            // counting-sort buckets (4096)
+// Geometry: BLOCK threads x ITEMS items = the window capacity; windows start
+// at the first run start of each TILE-item tile; 2^BBITS counting-sort buckets.
 constexpr int kLocalBucketMax = 24;             // larger bucket -> LSD passes for the window
+template <int BLOCK_, int ITEMS_, int TILE_, int BBITS_>
+struct LocalGeom {
+  static constexpr int LF_BLOCK = BLOCK_, LF_ITEMS = ITEMS_, kLocalTile = TILE_, kLocalBucketBits = BBITS_;
+  static constexpr int kLocalCap = BLOCK_ * ITEMS_;
+};
+using LocalGeomDefault = LocalGeom<512, 8, 2048, 12>;
 
 struct LocalSortArgs {
   const uint64_t* __restrict__ keys;  // [n], sorted by key >> pshift (stable)
@@ -46,7 +50,9 @@ struct LocalSortArgs {
   uint32_t* __restrict__ overflow;    // set to 1 when a window exceeds kLocalCap
 };
 
+template <class G>
 struct LocalSmem {
+  static constexpr int LF_BLOCK = G::LF_BLOCK, kLocalCap = G::kLocalCap, kLocalBucketBits = G::kLocalBucketBits;
   uint64_t okey[kLocalCap];
   uint16_t oidx[kLocalCap];
   union {
@@ -60,37 +66,43 @@ struct LocalSmem {
     } lsd;
   } u;
   uint32_t scan[LF_BLOCK / 32 + 1];
-  unsigned long long red[4][LF_BLOCK / 32];
+  unsigned long long red[2][LF_BLOCK / 32];
   unsigned long long found[2];
   uint32_t maxb;
 };
 
-template <class Emitter>
-__global__ void __launch_bounds__(LF_BLOCK) k_local_final(LocalSortArgs a, Emitter em) {
+template <class Emitter, class G = LocalGeomDefault>
+__global__ void __launch_bounds__(G::LF_BLOCK, 1024 / G::LF_BLOCK) k_local_final(LocalSortArgs a, Emitter em) {
+  constexpr int LF_BLOCK = G::LF_BLOCK, LF_ITEMS = G::LF_ITEMS, kLocalTile = G::kLocalTile;
+  constexpr int kLocalCap = G::kLocalCap, kLocalBucketBits = G::kLocalBucketBits;
   constexpr int NW = LF_BLOCK / 32, R = kRadix, NB = 1 << kLocalBucketBits;
+  static_assert(NB % LF_BLOCK == 0 && LF_BLOCK >= R, "geometry");
   extern __shared__ __align__(16) unsigned char lsm[];
-  LocalSmem& s = *reinterpret_cast<LocalSmem*>(lsm);
+  LocalSmem<G>& s = *reinterpret_cast<LocalSmem<G>*>(lsm);
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t lo = (int64_t)blockIdx.x * kLocalTile;
   const int64_t hi = min(a.n, lo + kLocalTile);
 
   // ---- window [start, end): the runs starting in [lo, hi), found from the
   // keys [lo - 1, lo + kLocalCap) staged once in shared memory (the window
-  // must end by lo + kLocalCap; a run start is where key >> pshift changes)
+  // must end by lo + kLocalCap; a run start is where key >> pshift changes).
+  // Prefixes compare on the high words when pshift >= 32.
   const int64_t stage_end = min(a.n, lo + kLocalCap);
   const int nst = (int)(stage_end - lo);
   for (int i = tid; i < nst; i += LF_BLOCK) s.okey[i] = ld_stream(a.keys + lo + i);
-  uint64_t before = 0;
-  if (lo > 0) before = ld_stream(a.keys + lo - 1) >> a.pshift;
+  const uint64_t before = lo > 0 ? ld_stream(a.keys + lo - 1) : 0ull;
   if (tid < 2) s.found[tid] = ~0ull;
   if (tid == 0) s.maxb = 0;
   __syncthreads();
+  const int psh = a.pshift;
+  auto differ = [&](uint64_t x, uint64_t y) {
+    return psh >= 32 ? ((uint32_t)((x ^ y) >> 32) >> (psh - 32)) != 0u : ((x ^ y) >> psh) != 0ull;
+  };
   {
     const int tile = (int)(hi - lo);
     uint32_t f0 = 0xffffffffu, f1 = 0xffffffffu;
     for (int i = tid; i < nst; i += LF_BLOCK) {
-      const uint64_t pv = i ? s.okey[i - 1] >> a.pshift : before;
-      const bool st = (lo + i == 0) || (s.okey[i] >> a.pshift) != pv;
+      const bool st = (lo + i == 0) || differ(s.okey[i], i ? s.okey[i - 1] : before);
       if (st) {
         if (i < tile) f0 = min(f0, (uint32_t)i);
         else f1 = min(f1, (uint32_t)i);
@@ -103,6 +115,7 @@ __global__ void __launch_bounds__(LF_BLOCK) k_local_final(LocalSortArgs a, Emitt
       if (f1 != 0xffffffffu) atomicMin(&s.found[1], (unsigned long long)f1);
     }
   }
+  for (int b = tid; b < NB; b += LF_BLOCK) s.u.cs.cnt[b] = 0;
   __syncthreads();
   if (s.found[0] == ~0ull) return;  // no run starts in this tile
   const int64_t start = lo + (int64_t)s.found[0];
@@ -116,172 +129,165 @@ __global__ void __launch_bounds__(LF_BLOCK) k_local_final(LocalSortArgs a, Emitt
   const int ipw = (W + NW * 32 - 1) / (NW * 32);  // items per lane actually used (<= LF_ITEMS)
   const int wbase = warp * ipw * 32 + lane;
 
-  // ---- keys -> registers (blocked by warp); bits varying in the window
+  // ---- keys -> registers (blocked by warp).  The window's keys lie in
+  // [first prefix << pshift, (last prefix + 1) << pshift): the counting sort
+  // spreads 2^BBITS buckets over that range (a monotone map of the key).
+  const uint64_t kfirst = s.okey[woff] >> psh << psh;
+  const uint64_t klast = s.okey[woff + W - 1] | ((1ull << psh) - 1ull);
+  const uint64_t span = klast - kfirst;
+  const int sbits = span ? 64 - __clzll((long long)span) : 0;
+  const int s0 = max(sbits - 32, 0);                          // (key - kfirst) >> s0 fits 32 bits
+  const int bsh = max(min(sbits, 32) - kLocalBucketBits, 0);  // then >> bsh: the bucket
   uint64_t k[LF_ITEMS];
-  uint32_t x[LF_ITEMS];
-  uint64_t ka = ~0ull, ko = 0ull, kmin = ~0ull, kmax = 0ull;
+  uint32_t x[LF_ITEMS], bk[LF_ITEMS];
 #pragma unroll
   for (int q = 0; q < LF_ITEMS; ++q) {
     const int idx = wbase + q * 32;
     k[q] = ~0ull;
     x[q] = (uint32_t)idx;
+    bk[q] = 0;
     if (q < ipw && idx < W) {
       k[q] = s.okey[woff + idx];
-      ka &= k[q];
-      ko |= k[q];
-      kmin = min(kmin, k[q]);
-      kmax = max(kmax, k[q]);
+      bk[q] = (uint32_t)((k[q] - kfirst) >> s0) >> bsh;
+      atomicAdd(&s.u.cs.cnt[bk[q]], 1u);
     }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    ka &= __shfl_xor_sync(kFull, ka, o);
-    ko |= __shfl_xor_sync(kFull, ko, o);
-    kmin = min(kmin, __shfl_xor_sync(kFull, kmin, o));
-    kmax = max(kmax, __shfl_xor_sync(kFull, kmax, o));
-  }
-  if (lane == 0) {
-    s.red[0][warp] = ka;
-    s.red[1][warp] = ko;
-    s.red[2][warp] = kmin;
-    s.red[3][warp] = kmax;
-  }
-  for (int b = tid; b < NB; b += LF_BLOCK) s.u.cs.cnt[b] = 0;
   __syncthreads();
-  uint64_t va = ~0ull, vo = 0ull, vmin = ~0ull, vmax = 0ull;
+  constexpr int BPT = NB / LF_BLOCK;  // buckets per thread (consecutive)
+  uint32_t c[BPT], sum = 0, mx = 0;
 #pragma unroll
-  for (int w = 0; w < NW; ++w) {
-    va &= s.red[0][w];
-    vo |= s.red[1][w];
-    vmin = min(vmin, (uint64_t)s.red[2][w]);
-    vmax = max(vmax, (uint64_t)s.red[3][w]);
+  for (int q = 0; q < BPT; ++q) {
+    c[q] = s.u.cs.cnt[tid * BPT + q];
+    sum += c[q];
+    mx = max(mx, c[q]);
   }
-  const uint64_t var = va ^ vo;
-  const int lob = var ? __ffsll((long long)var) - 1 : 64;
-  const int hib = var ? 63 - __clzll((long long)var) : -1;
-
-  if (var) {
-    // ---- counting sort on (key - min) >> bsh: 2^kLocalBucketBits buckets
-    // spread over the window's key range (a monotone map of the key)
-    const uint64_t span = vmax - vmin;
-    const int sbits = 64 - __clzll((long long)span);  // bits of the range (>= 1: var != 0)
-    const int bsh = max(sbits - kLocalBucketBits, 0);
-    const uint32_t bmask = (1u << kLocalBucketBits) - 1u;
-    auto bucket_of = [&](uint64_t kk) { return (uint32_t)((kk - vmin) >> bsh) & bmask; };
+  mx = __reduce_max_sync(kFull, mx);
+  if (lane == 0 && mx > (uint32_t)kLocalBucketMax) atomicMax(&s.maxb, mx);
+  uint32_t tot;
+  uint32_t run = block_excl_sum<LF_BLOCK>(sum, s.scan, &tot);
 #pragma unroll
-    for (int q = 0; q < LF_ITEMS; ++q)
-      if (q < ipw && wbase + q * 32 < W) atomicAdd(&s.u.cs.cnt[bucket_of(k[q])], 1u);
-    __syncthreads();
-    constexpr int BPT = NB / LF_BLOCK;  // buckets per thread (consecutive)
-    uint32_t c[BPT], sum = 0, mx = 0;
+  for (int q = 0; q < BPT; ++q) {
+    s.u.cs.cnt[tid * BPT + q] = run;  // bucket start
+    s.u.cs.cur[tid * BPT + q] = run;
+    run += c[q];
+  }
+  __syncthreads();
+  if (s.maxb == 0) {
+    // ---- scatter into the buckets (order-free), then every item's slot is
+    // its bucket start + the bucket members below it in (key, position) order
 #pragma unroll
-    for (int q = 0; q < BPT; ++q) {
-      c[q] = s.u.cs.cnt[tid * BPT + q];
-      sum += c[q];
-      mx = max(mx, c[q]);
-    }
-    mx = __reduce_max_sync(kFull, mx);
-    if (lane == 0 && mx) atomicMax(&s.maxb, mx);
-    uint32_t tot;
-    uint32_t run = block_excl_sum<LF_BLOCK>(sum, s.scan, &tot);
-#pragma unroll
-    for (int q = 0; q < BPT; ++q) {
-      s.u.cs.cnt[tid * BPT + q] = run;  // bucket start
-      s.u.cs.cur[tid * BPT + q] = run;
-      run += c[q];
+    for (int q = 0; q < LF_ITEMS; ++q) {
+      if (q < ipw && wbase + q * 32 < W) {
+        const uint32_t p = atomicAdd(&s.u.cs.cur[bk[q]], 1u);
+        s.okey[p] = k[q];
+        s.oidx[p] = (uint16_t)x[q];
+      }
     }
     __syncthreads();
-    if (s.maxb <= (uint32_t)kLocalBucketMax) {
-      // scatter into the buckets (order-free), then every item counts the
-      // bucket members below it in (key, position) order: its final slot
-      uint32_t bk[LF_ITEMS];
+    uint32_t pos[LF_ITEMS];
+#pragma unroll
+    for (int q = 0; q < LF_ITEMS; ++q) {
+      if (q < ipw && wbase + q * 32 < W) {
+        const int b0 = (int)s.u.cs.cnt[bk[q]], b1 = (int)s.u.cs.cur[bk[q]];
+        uint32_t r = 0;
+        if (b1 - b0 > 1) {
+          for (int j = b0; j < b1; ++j) {
+            const uint64_t kj = s.okey[j];
+            r += kj < k[q] || (kj == k[q] && s.oidx[j] < x[q]);
+          }
+        }
+        pos[q] = (uint32_t)b0 + r;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < LF_ITEMS; ++q) {
+      if (q < ipw && wbase + q * 32 < W) {
+        s.okey[pos[q]] = k[q];
+        s.oidx[pos[q]] = (uint16_t)x[q];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < LF_ITEMS; ++q) {
+      const int idx = wbase + q * 32;
+      if (q < ipw) {
+        k[q] = s.okey[idx];
+        x[q] = s.oidx[idx];
+      }
+    }
+  } else {
+    // ---- clustered window: stable 8-bit LSD passes over the bits that
+    // vary in it; padding keys (all ones) stay behind the window's items
+    uint64_t ka = ~0ull, ko = 0ull;
+#pragma unroll
+    for (int q = 0; q < LF_ITEMS; ++q) {
+      if (q < ipw && wbase + q * 32 < W) {
+        ka &= k[q];
+        ko |= k[q];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ka &= __shfl_xor_sync(kFull, ka, o);
+      ko |= __shfl_xor_sync(kFull, ko, o);
+    }
+    if (lane == 0) {
+      s.red[0][warp] = ka;
+      s.red[1][warp] = ko;
+    }
+    for (int b = tid; b < NW * R; b += LF_BLOCK) (&s.u.lsd.whist[0][0])[b] = 0;
+    __syncthreads();
+    uint64_t va = ~0ull, vo = 0ull;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      va &= s.red[0][w];
+      vo |= s.red[1][w];
+    }
+    const uint64_t var = va ^ vo;
+    const int lob = var ? __ffsll((long long)var) - 1 : 64;
+    const int hib = var ? 63 - __clzll((long long)var) : -1;
+    const uint32_t lt = lanemask_lt();
+    for (int sh = lob; sh <= hib; sh += kRadixBits) {
+      uint32_t rk[LF_ITEMS];
+#pragma unroll
+      for (int q = 0; q < LF_ITEMS; ++q)
+        if (q < ipw)
+          rk[q] = warp_rank<true, kRadixBits>(s.u.lsd.whist[warp], digit_of(k[q], sh), true, lane, lt, true);
+      __syncthreads();
+      uint32_t cc = 0;
+      if (tid < R) {
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          const uint32_t y = s.u.lsd.whist[w][tid];
+          s.u.lsd.whist[w][tid] = cc;
+          cc += y;
+        }
+      }
+      uint32_t t2;
+      const uint32_t ls = block_excl_sum<LF_BLOCK>(tid < R ? cc : 0u, s.scan, &t2);
+      if (tid < R) s.u.lsd.lstart[tid] = ls;
+      __syncthreads();
 #pragma unroll
       for (int q = 0; q < LF_ITEMS; ++q) {
-        if (q < ipw && wbase + q * 32 < W) {
-          bk[q] = bucket_of(k[q]);
-          const uint32_t p = atomicAdd(&s.u.cs.cur[bk[q]], 1u);
+        if (q < ipw) {
+          const uint32_t d = digit_of(k[q], sh);
+          const uint32_t p = s.u.lsd.lstart[d] + s.u.lsd.whist[warp][d] + rk[q];
           s.okey[p] = k[q];
           s.oidx[p] = (uint16_t)x[q];
         }
       }
       __syncthreads();
-      uint32_t pos[LF_ITEMS];
 #pragma unroll
       for (int q = 0; q < LF_ITEMS; ++q) {
-        if (q < ipw && wbase + q * 32 < W) {
-          const int b0 = (int)s.u.cs.cnt[bk[q]], b1 = (int)s.u.cs.cur[bk[q]];
-          uint32_t r = 0;
-          for (int j = b0; j < b1; ++j) {
-            const uint64_t kj = s.okey[j];
-            r += kj < k[q] || (kj == k[q] && s.oidx[j] < x[q]);
-          }
-          pos[q] = (uint32_t)b0 + r;
-        }
-      }
-      __syncthreads();
-#pragma unroll
-      for (int q = 0; q < LF_ITEMS; ++q) {
-        if (q < ipw && wbase + q * 32 < W) {
-          s.okey[pos[q]] = k[q];
-          s.oidx[pos[q]] = (uint16_t)x[q];
-        }
-      }
-      __syncthreads();
-#pragma unroll
-      for (int q = 0; q < LF_ITEMS; ++q) {
-        const int idx = wbase + q * 32;
         if (q < ipw) {
+          const int idx = wbase + q * 32;
           k[q] = s.okey[idx];
           x[q] = s.oidx[idx];
         }
       }
-    } else {
-      // ---- clustered window: stable LSD passes over its varying bits;
-      // padding keys (all ones) stay behind the window's items
-      const uint32_t lt = lanemask_lt();
       for (int b = tid; b < NW * R; b += LF_BLOCK) (&s.u.lsd.whist[0][0])[b] = 0;
       __syncthreads();
-      for (int sh = lob; sh <= hib; sh += kRadixBits) {
-        uint32_t rk[LF_ITEMS];
-#pragma unroll
-        for (int q = 0; q < LF_ITEMS; ++q)
-          if (q < ipw)
-            rk[q] = warp_rank<true, kRadixBits>(s.u.lsd.whist[warp], digit_of(k[q], sh), true, lane, lt, true);
-        __syncthreads();
-        uint32_t cc = 0;
-        if (tid < R) {
-#pragma unroll
-          for (int w = 0; w < NW; ++w) {
-            const uint32_t y = s.u.lsd.whist[w][tid];
-            s.u.lsd.whist[w][tid] = cc;
-            cc += y;
-          }
-        }
-        uint32_t t2;
-        const uint32_t ls = block_excl_sum<LF_BLOCK>(tid < R ? cc : 0u, s.scan, &t2);
-        if (tid < R) s.u.lsd.lstart[tid] = ls;
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < LF_ITEMS; ++q) {
-          if (q < ipw) {
-            const uint32_t d = digit_of(k[q], sh);
-            const uint32_t p = s.u.lsd.lstart[d] + s.u.lsd.whist[warp][d] + rk[q];
-            s.okey[p] = k[q];
-            s.oidx[p] = (uint16_t)x[q];
-          }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < LF_ITEMS; ++q) {
-          if (q < ipw) {
-            const int idx = wbase + q * 32;
-            k[q] = s.okey[idx];
-            x[q] = s.oidx[idx];
-          }
-        }
-        for (int b = tid; b < NW * R; b += LF_BLOCK) (&s.u.lsd.whist[0][0])[b] = 0;
-        __syncthreads();
-      }
     }
   }
   // ---- window position idx -> global rank start + idx (payload from the

@@ -457,6 +457,15 @@ std::vector<int> active_digits(uint64_t key_and, uint64_t key_or, int bits, int 
   return shifts;
 }
 
+// Varying bits of the (compacted) keys: XOR of AND / OR, with the dense
+// top-field code's bits when compaction applies.
+uint64_t var_of(const unsigned long long (&ao)[2], const uint8_t* code, int ncodes) {
+  if (!code) return ao[0] ^ ao[1];
+  int cbits = 0;
+  while ((1 << cbits) < ncodes) ++cbits;
+  return ((ao[0] ^ ao[1]) & kMantMask) | (((1ull << cbits) - 1) << kTopShift);
+}
+
 // Sort #1 (rank_edges): orig_of, heights, euv (and/or ru, rv).
 void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int64_t n,
                Sort1FinalEmitter em, int* passes_out) {
@@ -485,10 +494,14 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
   c.to_host(&tmin, top_min, 4);
   c.sync();
   const std::vector<int> guess = active_digits(sao[0], sao[1], 8, 64);
-  // the digit the fused upsweep counts: the first pass's (wide keys with >= 5
-  // active digits take the shared-memory finish, local_sort.cuh, whose first
-  // global digit is unaligned and counted by its own upsweep)
-  const int d0 = guess.empty() ? 0 : guess[0];
+  // The digit the fused upsweep counts: the first pass's.  >= 5 active
+  // digits predicts the shared-memory finish (local_sort.cuh), whose first
+  // global digit is the lowest of the 24 highest varying bits: count that
+  const uint64_t gvar = sao[0] ^ sao[1];
+  const bool local_guess = guess.size() >= 5 && !(c.paths.variant & 8);
+  // digit, one bit above the sample's highest varying bit: the full data
+  // often varies one bit higher (rarer, more extreme weights)
+  const int d0 = guess.empty() ? 0 : local_guess ? std::max(63 - __builtin_clzll(gvar) + 1 - 23, 0) : guess[0];
   const SweepGeom g = sweep_geom(c, n, S1_BLOCK * S1_ITEMS, S1N_MINB, S1_ALIGN);
   SweepArgs a{};
   a.n = n;
@@ -531,7 +544,12 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
   // the upsweep counted digit d0 of the raw keys: valid for the compacted
   // keys only below the top field
   const bool local = shifts.size() >= 5 && !(c.paths.variant & 8);
-  const int first_shift = shifts.empty() ? -1 : local ? -2 : shifts[0];  // local: unaligned digits, own upsweep
+  // (local: the three global digits [t0, t0 + 24) must cover the highest
+  // varying bit; t0 = the fused upsweep's digit when it does)
+  const int hb_full = shifts.empty() ? 0 : 63 - __builtin_clzll(var_of(ao, code, ncodes));
+  const int first_shift = shifts.empty() ? -1
+                          : local        ? (local_guess && hb_full <= d0 + 23 ? d0 : std::max(hb_full - 23, 0))
+                                         : shifts[0];
   const int ready = first_shift >= 0 && first_shift == d0 && (!code || d0 + 8 <= kTopShift) ? d0 : -1;
   if (passes_out) *passes_out = (int)shifts.size();
   char* R = c.w.R;
@@ -565,8 +583,7 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
       // shared memory; a window over capacity falls back to the full LSD sort
       // the three global digits cover the 24 highest VARYING key bits
       // (unaligned: sign/exponent bits that never vary are not spent on them)
-      const int hb = 63 - __builtin_clzll(var);
-      const int t0 = std::max(hb - 23, 0);
+      const int t0 = first_shift;
       const std::vector<int> top3 = {t0, t0 + 8, t0 + 16};
       ArrayEmitter<uint64_t, 3> tmp{bufK[0], bufP[0]};  // the third pass (p = 2) writes buffer 0
       run_sort<uint64_t, 3, S1_BLOCK, S1_ITEMS, S1_MINB, 8>(c, {KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_MID}, n,

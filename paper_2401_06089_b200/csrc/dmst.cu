@@ -601,7 +601,7 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
         c.launched();
       };
       if (c.paths.variant & 32)
-        launch_local(LocalGeom<512, 8, 2048, 11>{});
+        launch_local(LocalGeom<512, 8, 2048, 10>{});
       else
         launch_local(LocalGeomDefault{});
       uint32_t over = 0;

@@ -40,7 +40,7 @@ struct LocalGeom {
   static constexpr int LF_BLOCK = BLOCK_, LF_ITEMS = ITEMS_, kLocalTile = TILE_, kLocalBucketBits = BBITS_;
   static constexpr int kLocalCap = BLOCK_ * ITEMS_;
 };
-using LocalGeomDefault = LocalGeom<512, 8, 2048, 12>;
+using LocalGeomDefault = LocalGeom<512, 8, 2048, 11>;
 
 struct LocalSortArgs {
   const uint64_t* __restrict__ keys;  // [n], sorted by key >> pshift (stable)
@@ -99,20 +99,22 @@ __global__ void __launch_bounds__(G::LF_BLOCK, 1024 / G::LF_BLOCK) k_local_final
     return psh >= 32 ? ((uint32_t)((x ^ y) >> 32) >> (psh - 32)) != 0u : ((x ^ y) >> psh) != 0ull;
   };
   {
+    // runs are short: look at the first LF_BLOCK / 2 positions after lo and
+    // after hi (one per thread), the rest of the staged keys only if needed
     const int tile = (int)(hi - lo);
-    uint32_t f0 = 0xffffffffu, f1 = 0xffffffffu;
-    for (int i = tid; i < nst; i += LF_BLOCK) {
-      const bool st = (lo + i == 0) || differ(s.okey[i], i ? s.okey[i - 1] : before);
-      if (st) {
-        if (i < tile) f0 = min(f0, (uint32_t)i);
-        else f1 = min(f1, (uint32_t)i);
-      }
-    }
-    f0 = __reduce_min_sync(kFull, f0);
-    f1 = __reduce_min_sync(kFull, f1);
-    if (lane == 0) {
-      if (f0 != 0xffffffffu) atomicMin(&s.found[0], (unsigned long long)f0);
-      if (f1 != 0xffffffffu) atomicMin(&s.found[1], (unsigned long long)f1);
+    const int half = (int)(tid >= LF_BLOCK / 2);
+    const int hb0 = half ? tile : 0, hb1 = half ? nst : tile;  // positions [hb0, hb1) of this half
+    for (int i0 = hb0;; i0 += LF_BLOCK / 2) {
+      const int i = i0 + (int)(tid % (LF_BLOCK / 2));
+      uint32_t f = 0xffffffffu;
+      if (i < hb1 && ((lo + i == 0) || differ(s.okey[i], i ? s.okey[i - 1] : before))) f = (uint32_t)i;
+      f = __reduce_min_sync(kFull, f);
+      if (lane == 0 && f != 0xffffffffu) atomicMin(&s.found[half], (unsigned long long)f);
+      __syncthreads();
+      const bool more = (s.found[0] == ~0ull && i0 - hb0 + LF_BLOCK / 2 < tile - 0) ||
+                        (s.found[1] == ~0ull && (i0 - hb0) + LF_BLOCK / 2 < nst - tile);
+      __syncthreads();  // every thread has read `found` before the next step may update it
+      if (!more) break;
     }
   }
   for (int b = tid; b < NB; b += LF_BLOCK) s.u.cs.cnt[b] = 0;

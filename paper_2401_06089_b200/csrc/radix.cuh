@@ -429,8 +429,12 @@ __device__ __forceinline__ uint32_t warp_rank(uint32_t* whist, uint32_t d, bool 
     peers = FULL ? kFull : (valid ? __ballot_sync(kFull, valid) : ~__ballot_sync(kFull, valid));
 #pragma unroll
     for (int b = 0; b < BITS; ++b) {
-      const uint32_t bit = (d >> b) & 1u;
-      peers &= __ballot_sync(kFull, bit) ^ (bit - 1u);
+      // s = bit b of d sign-extended (all ones / zero): peers keep the lanes
+      // whose bit b equals ours, ~(ballot ^ s), one LOP3 per bit
+      int32_t sb;
+      asm("bfe.s32 %0, %1, %2, 1;" : "=r"(sb) : "r"(d), "r"(b));
+      const uint32_t m = __ballot_sync(kFull, sb != 0);
+      peers &= ~(m ^ (uint32_t)sb);
     }
   } else {
     peers = __match_any_sync(kFull, FULL ? d : (valid ? d : 0xffffu));

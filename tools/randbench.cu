@@ -55,7 +55,7 @@ int main(int argc, char** argv) {
   cudaEventRecord(a); for (int r = 0; r < 5; ++r) copyk<<<(n / 4 + 255) / 256, 256>>>((int4*)src, (int4*)dst, n / 4); cudaEventRecord(b);
   cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b); ms /= 5;
   printf("copy 512MB: %.3f ms = %.0f GB/s\n", ms, 2.0 * n * 4 / ms / 1e6);
-  uint32_t ranges[] = {32u << 20, 128000000u};
+  uint32_t ranges[] = {2u << 20, 8u << 20, 32u << 20, 128000000u};
   for (uint32_t range : ranges) {
     fill_idx<<<(n + 255) / 256, 256>>>(idx, n, range, 1234);
     auto run = [&](const char* name, auto launch) {

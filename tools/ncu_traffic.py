@@ -19,6 +19,7 @@ BS = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 def kind(name: str) -> str:
     rules = [
+        ("k_local_final", "sort1_local"),
         ("k_key_reduce", "sort1_hist"), ("k_upsweep", "upsweep_scan"), ("k_row_scan", "upsweep_scan"), ("k_row_total_scan", "upsweep_scan"),
         ("Sort1Loader", "sort1_pass_first"), ("Sort1Emitter", "sort1_pass_final"),
         ("Sort1FirstLoader", "sort1_pass_first"), ("Sort1FinalEmitter", "sort1_pass_final"),

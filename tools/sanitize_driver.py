@@ -56,6 +56,19 @@ for w in (rng.integers(0, 4096, nv - 1).astype(np.float64),
     e = O.build(nv, u, v, w)
     bad += not (np.array_equal(r.orig_of.cpu().numpy(), e.orig_of)
                 and np.array_equal(r.edge_parent.cpu().numpy(), e.edge_parent))
+# wide-key edge sort finished in shared memory: uniform, clustered (window LSD
+# passes) and a long tied run (overflow -> full LSD fallback)
+nv, u, v, _ = synth.random_attach(30_000, seed=9)
+wu = rng.random(nv - 1)
+wc = wu.copy()
+wc[rng.random(nv - 1) < 0.05] = 0.5 + rng.random() * 2.0 ** -30
+wo = wu.copy()
+wo[rng.random(nv - 1) < 0.3] = 0.25
+for w in (wu, wc, wo):
+    r = b.build(nv, u, v, w)
+    e = O.build(nv, u, v, w)
+    bad += not (np.array_equal(r.orig_of.cpu().numpy(), e.orig_of)
+                and np.array_equal(r.edge_parent.cpu().numpy(), e.edge_parent))
 # v1 text format: device writer -> device reader -> verify
 import tempfile  # noqa: E402
 from paper_2401_06089_b200 import read_dendrogram_b200, verify_b200, write_dendrogram_b200  # noqa: E402

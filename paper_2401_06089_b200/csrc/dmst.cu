@@ -486,7 +486,7 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
   // predict the first active digit from a sample, then count it in the same
   // read of w that reduces all keys (k_upsweep<KEYRED>)
   c.begin(KK_SORT1_HIST);
-  k_key_sample<<<1, 1024, 0, c.s>>>(w, n, sample_ao, top_min);
+  k_key_sample<<<64, 1024, 0, c.s>>>(w, n, sample_ao, top_min);  // one sample per thread
   c.launched();
   unsigned long long sao[2];
   uint32_t tmin = 0;

@@ -11,7 +11,10 @@ namespace dmst {
 
 constexpr int EW_BLOCK = 256;                  // elementwise kernels
 constexpr int SEL_BLOCK = 256;                 // k_select_edges
-constexpr int LS_TILE = 2048;                  // k_leafscan words per tile
+#ifndef DMST_LS_TILE
+#define DMST_LS_TILE 2048
+#endif
+constexpr int LS_TILE = DMST_LS_TILE;          // k_leafscan words per tile
 constexpr int CHASE_FREE = 8;    // V2 chase steps before rulers may end a chase
 constexpr int CHASE_CAP = 512;   // hard bound on one V2 chase
 
@@ -40,7 +43,8 @@ __global__ void __launch_bounds__(1024) k_key_sample(const double* __restrict__ 
   uint64_t a = ~0ull, o = 0ull;
   uint32_t tmin = 0xfffu;
 #pragma unroll 8
-  for (int64_t i = (int64_t)threadIdx.x * stride; i < n; i += (int64_t)blockDim.x * stride) {
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * stride; i < n;
+       i += (int64_t)gridDim.x * blockDim.x * stride) {
     const uint64_t k = desc_key(w[i]);
     a &= k;
     o |= k;
@@ -290,7 +294,7 @@ __global__ void __launch_bounds__(256) k_leafscan(int64_t words, int64_t ne, con
                                                   uint32_t* __restrict__ apre,
                                                   uint32_t* __restrict__ status, uint32_t* __restrict__ tile_ctr,
                                                   uint32_t* __restrict__ counts) {
-  constexpr int ITEMS = 8, TILE = 256 * ITEMS;
+  constexpr int ITEMS = LS_TILE / 256, TILE = LS_TILE;
   __shared__ uint32_t s_tile, s_excl[2];
   __shared__ uint32_t scratch[256 / 32 + 1];
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);

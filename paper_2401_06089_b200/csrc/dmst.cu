@@ -129,7 +129,7 @@ constexpr int SM_HIST1 = 0, SM_GBASE1 = SM_HIST1 + 8 * kRadix, SM_HIST2 = SM_GBA
               SM_GBASE2 = SM_HIST2 + 4 * kRadix, SM_VHIST = SM_GBASE2 + 4 * kRadix,
               SM_VBASE = SM_VHIST + kRadix, SM_TILECTR = SM_VBASE + kRadix, SM_MISC = SM_TILECTR + 64;
 constexpr int MISC_NEGZERO = 0, MISC_ACTIVE0 = 1, MISC_ACTIVE1 = 2, MISC_ACTIVE2 = 3, MISC_COUNTS = 4 /*2*/,
-              MISC_NONRUL = 6, MISC_LSCTR = 13, MISC_LOCALOVF = 16;
+              MISC_NONRUL = 6, MISC_LSCTR = 13, MISC_LOCALOVF = 16, MISC_SORT1D0 = 17;
 
 Workspace carve(int64_t n, int64_t nv, char* base) {
   Workspace w{};
@@ -488,24 +488,11 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
   c.begin(KK_SORT1_HIST);
   k_key_sample<<<64, 1024, 0, c.s>>>(w, n, sample_ao, top_min);  // one sample per thread
   c.launched();
-  unsigned long long sao[2];
-  uint32_t tmin = 0;
-  c.to_host(sao, sample_ao, 16);
-  c.to_host(&tmin, top_min, 4);
-  c.sync();
-  const std::vector<int> guess = active_digits(sao[0], sao[1], 8, 64);
-  // The digit the fused upsweep counts: the first pass's.  >= 5 active
-  // digits predicts the shared-memory finish (local_sort.cuh), whose first
-  // global digit is the lowest of the 24 highest varying bits: count that
-  const uint64_t gvar = sao[0] ^ sao[1];
-  const bool local_guess = guess.size() >= 5 && !(c.paths.variant & 8);
-  // digit, one bit above the sample's highest varying bit: the full data
-  // often varies one bit higher (rarer, more extreme weights)
-  const int d0 = guess.empty() ? 0 : local_guess ? std::max(63 - __builtin_clzll(gvar) + 1 - 23, 0) : guess[0];
+  uint32_t* d0_dev = c.w.small + SM_MISC + MISC_SORT1D0;
   const SweepGeom g = sweep_geom(c, n, S1_BLOCK * S1_ITEMS, S1N_MINB, S1_ALIGN);
   SweepArgs a{};
   a.n = n;
-  a.shift = d0;
+  a.shift = 0;  // the KEYRED upsweep predicts its digit from the sample on the device
   a.chunk = g.chunk;
   a.G = (uint32_t)g.G;
   a.GS = g.GS;
@@ -513,14 +500,20 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
   c.zero(a.counts, 4 * kRadix * (size_t)a.GS);
   c.begin(KK_SORT1_HIST);
   k_upsweep<8, Sort1FirstLoader, true><<<(unsigned)(g.G * kUpSplit), 256, 0, c.s>>>(
-      a, Sort1FirstLoader{w, u, v, nullptr}, KeyRed{w, and_or, negzero, top_bits, std::min(tmin, 4095u)});
+      a, Sort1FirstLoader{w, u, v, nullptr},
+      KeyRed{w, and_or, negzero, top_bits, sample_ao, top_min, d0_dev, (c.paths.variant & 8) ? 0 : 1});
   c.launched();
   unsigned long long ao[2];
-  uint32_t nz = 0, tb[128];
+  uint32_t nz = 0, tb[128], d0u = 0;
+  unsigned long long sao[2];
+  c.to_host(&d0u, d0_dev, 4);
+  c.to_host(sao, sample_ao, 16);
   c.to_host(ao, and_or, 16);
   c.to_host(&nz, negzero, 4);
   c.to_host(tb, top_bits, sizeof(tb));
   c.sync();
+  const int d0 = (int)d0u;  // = predict_first_digit(sample AND, OR)
+  const bool local_guess = !(c.paths.variant & 8) && active_digits(sao[0], sao[1], 8, 64).size() >= 5;
   std::vector<int> shifts = active_digits(ao[0], ao[1], 8, 64);
   // top-field compaction when it saves a pass: (code, mantissa) keys
   int ncodes = 0;
@@ -714,20 +707,23 @@ void run_tail(Ctx& c, int level0, int cur, int64_t n_k, int64_t nv_k, LevelTable
   ta.nv0 = nv_k;
   ta.soff_k0 = lt.soff[level0];
   ta.soff0 = soff;
+  // zeroed so the single readback below never reads unwritten words
+  c.zero(counts_out, 4 * 5 * (size_t)(DMST_MAX_LEVELS + 1));
+  c.zero(soff_out, 8 * (size_t)(DMST_MAX_LEVELS + 2));
   void* args[] = {&ta};
   c.begin(KK_TAIL);
   DMST_CUDA(cudaLaunchCooperativeKernel((const void*)k_tail, dim3(grid), dim3(TAIL_BLOCK), args, 0, c.s));
   c.launched();
+  // one readback for the level count and every view's counts / offsets
   int32_t res[2];
+  std::vector<int32_t> co(5 * (size_t)(DMST_MAX_LEVELS + 1));
+  std::vector<int64_t> so(DMST_MAX_LEVELS + 2);
   c.to_host(res, result, 8);
-  c.sync();
-  const int L = res[0];
-  if (L < level0) invalid("too many contraction levels");
-  std::vector<int32_t> co(5 * (size_t)(L + 1));
-  std::vector<int64_t> so(L + 2);
   c.to_host(co.data(), counts_out, 4 * co.size());
   c.to_host(so.data(), soff_out, 8 * so.size());
   c.sync();
+  const int L = res[0];
+  if (L < level0 || L > DMST_MAX_LEVELS) invalid("too many contraction levels");
   for (int k = level0; k <= L; ++k) {
     if (st) {
       for (int q = 0; q < 4; ++q) st->level_counts[k][q] = co[5 * k + q];

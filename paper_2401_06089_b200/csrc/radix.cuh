@@ -215,8 +215,37 @@ struct KeyRed {
   unsigned long long* and_or;
   uint32_t* negzero;
   uint32_t* top_bits;  // presence bitmap of the top fields (key >> 52), 4096 bits
-  uint32_t top_base;   // base of the in-register 32-field window (the sample's smallest)
+  // the sample (k_key_sample): AND / OR of its keys and its smallest top field
+  // (the base of the in-register 32-field window); the digit this upsweep
+  // counts is predicted from it on the device (no host round trip) and
+  // written to d0_out for the host
+  const unsigned long long* sample_ao;
+  const uint32_t* sample_tmin;
+  uint32_t* d0_out;
+  int allow_local;  // 0: never predict the shared-memory finish (variant 8)
 };
+
+// The first pass's digit, predicted from the sample's varying bits: >= 5
+// active 8-bit digits predicts the wide-key shared-memory finish
+// (local_sort.cuh), whose first global digit is the lowest of the 24 highest
+// varying bits, one bit above the sample's top varying bit (the full data
+// often varies one bit higher); otherwise the lowest active digit.
+__host__ __device__ inline int predict_first_digit(unsigned long long sand, unsigned long long sor, int allow_local) {
+  const unsigned long long var = sand ^ sor;
+  int nd = 0, lo = -1;
+  for (int sft = 0; sft < 64; sft += 8)
+    if ((var >> sft) & 0xffull) {
+      ++nd;
+      if (lo < 0) lo = sft;
+    }
+  if (nd == 0) return 0;
+  if (nd >= 5 && allow_local) {
+    int hb = 63;
+    while (!((var >> hb) & 1ull)) --hb;
+    return hb + 1 - 23 > 0 ? hb + 1 - 23 : 0;
+  }
+  return lo;
+}
 
 template <int BITS, class Loader, bool KEYRED = false>
 __global__ void __launch_bounds__(256) k_upsweep(SweepArgs a, Loader ld, KeyRed kr = KeyRed{}) {
@@ -232,6 +261,13 @@ __global__ void __launch_bounds__(256) k_upsweep(SweepArgs a, Loader ld, KeyRed 
     if (threadIdx.x < 128) tbits[threadIdx.x] = 0;
   }
   __syncthreads();
+  int shift = a.shift;
+  uint32_t top_base = 0;
+  if constexpr (KEYRED) {
+    shift = predict_first_digit(kr.sample_ao[0], kr.sample_ao[1], kr.allow_local);
+    top_base = min(*kr.sample_tmin, 4095u);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *kr.d0_out = (uint32_t)shift;
+  }
   const uint32_t chunk_id = blockIdx.x / kUpSplit, part = blockIdx.x % kUpSplit;
   const int64_t cbeg = (int64_t)chunk_id * a.chunk;
   const int64_t plen = (a.chunk / kUpSplit + 1023) & ~int64_t(1023);
@@ -263,12 +299,12 @@ __global__ void __launch_bounds__(256) k_upsweep(SweepArgs a, Loader ld, KeyRed 
         ka &= k;
         ko |= k;
         tq[q] = (uint32_t)(k >> 52);
-        const uint32_t dt = tq[q] - kr.top_base;
+        const uint32_t dt = tq[q] - top_base;
         tw |= dt < 32 ? 1u << dt : 0u;
         far |= dt < 32 ? 0u : 1u << q;
-        d[q] = digit_of<BITS>(k, a.shift);
+        d[q] = digit_of<BITS>(k, shift);
       } else {
-        d[q] = ok[q] ? digit_of<BITS>(ld.key(i), a.shift) : 0u;
+        d[q] = ok[q] ? digit_of<BITS>(ld.key(i), shift) : 0u;
       }
     }
     if constexpr (KEYRED) {
@@ -300,7 +336,7 @@ __global__ void __launch_bounds__(256) k_upsweep(SweepArgs a, Loader ld, KeyRed 
     }
     tw = __reduce_or_sync(kFull, tw);
     if (lane_id() == 0 && tw) {  // window bits base.. base+31 -> two aligned words
-      const uint32_t wb = kr.top_base >> 5, sh = kr.top_base & 31;
+      const uint32_t wb = top_base >> 5, sh = top_base & 31;
       atomicOr(&tbits[wb], tw << sh);
       if (sh && wb + 1 < 128) atomicOr(&tbits[wb + 1], tw >> (32 - sh));
     }

@@ -81,7 +81,8 @@ typedef struct dmst_stats {
   int64_t direct_mi_bytes;  /* views >= 1 whose packed maxIncident (8 B per vertex) is at
                                most this large take direct atomics in k_select_edges + k_v1
                                (default 64 MB); -1 = always bucketed (multisplit + apply) */
-  int32_t sort1_mode;       /* bit 0: no narrow 32-bit keys; bit 1: no top-field compaction */
+  int32_t sort1_mode;       /* bit 0: no narrow 32-bit keys; bit 1: no top-field compaction;
+                               bit 2: wide keys never finish in shared memory (full LSD sort) */
   int32_t sort2_geometry;   /* chain-sort tiles: 1 = 512 x 16, 2 = 256 x 20 (two CTAs per SM);
                                0 = by size (2 from 32M edges) */
   /* out: the path this call took (what bench.py's byte model reads) */
@@ -93,10 +94,6 @@ typedef struct dmst_stats {
                                window in shared memory; 2 = a window overflowed, full LSD ran */
   uint64_t mi_bucketed;     /* bit k: view k's maxIncident was bucketed */
   uint64_t mi_direct;       /* bit k: view k's maxIncident took direct atomics */
-  /* in: kernel-variant switches for A/B measurement (0 = the default kernels;
-   * same bits either way).  8 = wide edge-sort keys never finish in shared
-   * memory (full LSD sort). */
-  int32_t variant;
 } dmst_stats;
 
 /* Workspace size for a tree with n_edges edges. */

@@ -67,11 +67,10 @@ class DmstStats(ctypes.Structure):
         ("sort1_local", ctypes.c_int32),
         ("mi_bucketed", ctypes.c_uint64),
         ("mi_direct", ctypes.c_uint64),
-        ("variant", ctypes.c_int32),
     ]
 
     # code-path overrides accepted by DendrogramBuilder.build(paths=...)
-    PATH_OPTIONS = ("tail_edges", "direct_mi_bytes", "sort1_mode", "sort2_geometry", "variant")
+    PATH_OPTIONS = ("tail_edges", "direct_mi_bytes", "sort1_mode", "sort2_geometry")
 
     def set_paths(self, paths: dict | None) -> None:
         for k, v in (paths or {}).items():

@@ -244,7 +244,6 @@ struct Paths {
   int64_t direct_mi_bytes = kDirectMiBytes;
   int sort1_mode = 0;
   int sort2_geometry = 0;
-  int variant = 0;
   // out
   int sort1_narrow = 0, sort1_compacted = 0, sort2_geometry_used = 0, tail_level = -1;
   int sort1_local = 0;  // 1 = wide keys finished in shared memory, 2 = tried, fell back to full LSD
@@ -501,7 +500,7 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
   c.begin(KK_SORT1_HIST);
   k_upsweep<8, Sort1FirstLoader, true><<<(unsigned)(g.G * kUpSplit), 256, 0, c.s>>>(
       a, Sort1FirstLoader{w, u, v, nullptr},
-      KeyRed{w, and_or, negzero, top_bits, sample_ao, top_min, d0_dev, (c.paths.variant & 8) ? 0 : 1});
+      KeyRed{w, and_or, negzero, top_bits, sample_ao, top_min, d0_dev, (c.paths.sort1_mode & 4) ? 0 : 1});
   c.launched();
   unsigned long long ao[2];
   uint32_t nz = 0, tb[128], d0u = 0;
@@ -513,7 +512,7 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
   c.to_host(tb, top_bits, sizeof(tb));
   c.sync();
   const int d0 = (int)d0u;  // = predict_first_digit(sample AND, OR)
-  const bool local_guess = !(c.paths.variant & 8) && active_digits(sao[0], sao[1], 8, 64).size() >= 5;
+  const bool local_guess = !(c.paths.sort1_mode & 4) && active_digits(sao[0], sao[1], 8, 64).size() >= 5;
   std::vector<int> shifts = active_digits(ao[0], ao[1], 8, 64);
   // top-field compaction when it saves a pass: (code, mantissa) keys
   int ncodes = 0;
@@ -536,7 +535,7 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
   }
   // the upsweep counted digit d0 of the raw keys: valid for the compacted
   // keys only below the top field
-  const bool local = shifts.size() >= 5 && !(c.paths.variant & 8);
+  const bool local = shifts.size() >= 5 && !(c.paths.sort1_mode & 4);
   // (local: the three global digits [t0, t0 + 24) must cover the highest
   // varying bit; t0 = the fused upsweep's digit when it does)
   const int hb_full = shifts.empty() ? 0 : 63 - __builtin_clzll(var_of(ao, code, ncodes));
@@ -593,10 +592,7 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
         kern<<<grid_for(n, G::kLocalTile), G::LF_BLOCK, sizeof(LocalSmem<G>), c.s>>>(la, em);
         c.launched();
       };
-      if (c.paths.variant & 32)
-        launch_local(LocalGeom<512, 8, 2048, 10>{});
-      else
-        launch_local(LocalGeomDefault{});
+      launch_local(LocalGeomDefault{});
       uint32_t over = 0;
       c.to_host(&over, ovf, 4);
       c.sync();
@@ -1000,8 +996,8 @@ void init_ctx(Ctx& c, int64_t n, int64_t nv, void* ws, void* stream, dmst_stats*
   if (st) {
     const int32_t prof = st->profile, wc = st->want_chains;
     const int64_t te = st->tail_edges, dm = st->direct_mi_bytes;
-    const int32_t s1 = st->sort1_mode, s2 = st->sort2_geometry, var = st->variant;
-    if (s1 < 0 || s1 > 3) invalid("sort1_mode must be in [0, 3]");
+    const int32_t s1 = st->sort1_mode, s2 = st->sort2_geometry;
+    if (s1 < 0 || s1 > 7) invalid("sort1_mode must be in [0, 7]");
     if (s2 < 0 || s2 > 2) invalid("sort2_geometry must be 0, 1 or 2");
     if (te < -1 || dm < -1) invalid("tail_edges / direct_mi_bytes must be >= -1");
     memset(st, 0, sizeof(*st));
@@ -1011,13 +1007,11 @@ void init_ctx(Ctx& c, int64_t n, int64_t nv, void* ws, void* stream, dmst_stats*
     st->direct_mi_bytes = dm;
     st->sort1_mode = s1;
     st->sort2_geometry = s2;
-    st->variant = var;
     c.profile = prof != 0;
     if (te) c.paths.tail_edges = te;  // -1: n_k <= -1 never holds
     if (dm) c.paths.direct_mi_bytes = dm;
     c.paths.sort1_mode = s1;
     c.paths.sort2_geometry = s2;
-    c.paths.variant = var;
   }
 }
 

@@ -222,7 +222,7 @@ struct KeyRed {
   const unsigned long long* sample_ao;
   const uint32_t* sample_tmin;
   uint32_t* d0_out;
-  int allow_local;  // 0: never predict the shared-memory finish (variant 8)
+  int allow_local;  // 0: never predict the shared-memory finish (sort1_mode bit 2)
 };
 
 // The first pass's digit, predicted from the sample's varying bits: >= 5

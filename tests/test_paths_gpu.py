@@ -43,7 +43,7 @@ PATHS = {
     # narrow keys without compaction; 512 x 16 chain-sort tiles; no tail, bucketed
     "nocompact_bucketed": {"sort1_mode": 2, "sort2_geometry": 1, "direct_mi_bytes": -1, "tail_edges": -1},
     # wide keys always sorted by the full LSD (no shared-memory finish)
-    "no_local": {"variant": 8},
+    "no_local": {"sort1_mode": 4},
 }
 
 SEEN_KINDS: dict[str, int] = {}   # kernel kind -> launches inside checked builds
@@ -106,7 +106,7 @@ def _assert_path_taken(res, paths):
         assert not info["sort1_narrow"]
     if p.get("sort1_mode", 0) & 2:
         assert not info["sort1_compacted"]
-    if p.get("variant", 0) & 8:
+    if p.get("sort1_mode", 0) & 4:
         assert info["sort1_local"] is None
     if p.get("sort2_geometry") and info["sort2_passes"]:
         from paper_2401_06089_b200._lib import SORT2_GEOMETRIES
@@ -203,7 +203,7 @@ def _local_weights(kind: str, n: int, rng):
 def test_wide_key_local_sort(builder, kind, n):
     # the wide-key edge sort that finishes per window in shared memory
     # (local_sort.cuh) and its fallback, against the oracle and against the
-    # forced full LSD sort (variant 8): same bits either way
+    # forced full LSD sort (sort1_mode bit 2): same bits either way
     rng = np.random.default_rng(n + len(kind))
     nv, u, v, _ = synth.random_attach(n, seed=n % 97)
     w = _local_weights(kind, n, rng)
@@ -225,7 +225,7 @@ def test_rejects_bad_path_options(builder):
     with pytest.raises(ValueError):
         builder.build(nv, u, v, w, paths={"sort2_geometry": 3})
     with pytest.raises(ValueError):
-        builder.build(nv, u, v, w, paths={"sort1_mode": 4})
+        builder.build(nv, u, v, w, paths={"sort1_mode": 8})
     with pytest.raises(ValueError):
         builder.build(nv, u, v, w, paths={"no_such_option": 1})
 

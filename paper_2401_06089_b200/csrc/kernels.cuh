@@ -593,6 +593,12 @@ struct Sort2FirstLoader {
   static constexpr int NS = 1;
   __host__ __device__ static constexpr int sb(int) { return 4; }
   const uint32_t* __restrict__ keys;
+  using RawKey = uint32_t;
+  static constexpr bool VEC = true;
+  __device__ __forceinline__ const uint32_t* raw_keys() const { return keys; }
+  __device__ __forceinline__ uint64_t key_of_raw(uint32_t r, int64_t i) const {
+    return ((uint64_t)r << 32) | (uint32_t)i;
+  }
   __device__ __forceinline__ const void* ptr(int) const { return keys; }
   __device__ __forceinline__ uint64_t key(int64_t i) const {
     return ((uint64_t)ld_stream(keys + i) << 32) | (uint32_t)i;

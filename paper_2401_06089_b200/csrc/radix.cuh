@@ -115,6 +115,11 @@ struct ArrayLoader {
   __host__ __device__ static constexpr int sb(int s) { return s == 0 ? (int)sizeof(K) : 4 * PW; }
   const K* __restrict__ keys;
   const uint32_t* __restrict__ pay;
+  // the upsweep may read the keys as 16-B vectors (raw key = sort key)
+  using RawKey = K;
+  static constexpr bool VEC = true;
+  __device__ __forceinline__ const K* raw_keys() const { return keys; }
+  __device__ __forceinline__ K key_of_raw(K r, int64_t) const { return r; }
   __device__ __forceinline__ const void* ptr(int s) const { return s == 0 ? (const void*)keys : (const void*)pay; }
   __device__ __forceinline__ K key(int64_t i) const { return ld_stream(keys + i); }
   __device__ __forceinline__ void load(int64_t i, K& k, Vals<PW>& v) const {
@@ -247,6 +252,25 @@ __host__ __device__ inline int predict_first_digit(unsigned long long sand, unsi
   return lo;
 }
 
+template <class L, class = void>
+struct HasVec {
+  static constexpr bool value = false;
+};
+template <class L>
+struct HasVec<L, decltype(void(L::VEC))> {
+  static constexpr bool value = L::VEC;
+};
+template <class L>
+__host__ __device__ constexpr bool loader_vec() { return HasVec<L>::value; }
+template <class L, bool = HasVec<L>::value>
+struct LoaderRawKey {
+  using type = uint32_t;  // unused
+};
+template <class L>
+struct LoaderRawKey<L, true> {
+  using type = typename L::RawKey;
+};
+
 template <int BITS, class Loader, bool KEYRED = false>
 __global__ void __launch_bounds__(256) k_upsweep(SweepArgs a, Loader ld, KeyRed kr = KeyRed{}) {
   constexpr int R = 1 << BITS, BPT = R / 256;
@@ -273,6 +297,52 @@ __global__ void __launch_bounds__(256) k_upsweep(SweepArgs a, Loader ld, KeyRed 
   const int64_t plen = (a.chunk / kUpSplit + 1023) & ~int64_t(1023);
   const int64_t begin = cbeg + part * plen;
   const int64_t end = min(min(a.n, cbeg + a.chunk), begin + plen);
+  if constexpr (!KEYRED && loader_vec<Loader>()) {
+    if (aligned16(ld.raw_keys())) {  // uniform across the grid
+    // keys as 16-B vectors: 2-4 keys per load, 4 loads in flight per thread
+    using RK = typename LoaderRawKey<Loader>::type;
+    constexpr int PER = 16 / (int)sizeof(RK), UV = 4;
+    const RK* kp = ld.raw_keys();
+    const int64_t vend = begin + ((end - begin) / PER) * PER;
+    // (the loop bound is uniform across the warp: the ballots below need every lane)
+    for (int64_t i0 = begin; i0 < vend; i0 += (int64_t)256 * PER * UV) {
+      uint4 xv[UV];
+#pragma unroll
+      for (int q = 0; q < UV; ++q) {
+        const int64_t i = i0 + ((int64_t)q * 256 + threadIdx.x) * PER;
+        xv[q] = i < vend ? ld_stream(reinterpret_cast<const uint4*>(kp + i)) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int q = 0; q < UV; ++q) {
+        const int64_t i = i0 + ((int64_t)q * 256 + threadIdx.x) * PER;
+        const bool ok = i < vend;
+        const RK* e = reinterpret_cast<const RK*>(&xv[q]);
+#pragma unroll
+        for (int t = 0; t < PER; ++t) {
+          const uint32_t dd = ok ? digit_of<BITS>(ld.key_of_raw(e[t], i + t), a.shift) : 0u;
+          const uint32_t act = __ballot_sync(kFull, ok);
+          const uint32_t d0 = __shfl_sync(kFull, dd, 0);
+          if (__all_sync(kFull, !ok || dd == d0)) {  // one digit across the warp (skewed keys)
+            if (lane_id() == 0 && act) atomicAdd(&h[warp][d0], __popc(act));
+          } else if (ok) {
+            atomicAdd(&h[warp][dd], 1u);
+          }
+        }
+      }
+    }
+    for (int64_t i = vend + threadIdx.x; i < end; i += 256) atomicAdd(&h[warp][digit_of<BITS>(ld.key(i), a.shift)], 1u);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < BPT; ++q) {
+      const uint32_t b = q * 256 + threadIdx.x;
+      uint32_t c = 0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) c += h[w][b];
+      if (c) atomicAdd(a.counts + (uint64_t)b * a.GS + chunk_id, c);
+    }
+    return;
+    }
+  }
   constexpr int U = KEYRED ? 16 : 8;  // the fused pass over w is load-latency-bound at 8
   uint64_t ka = ~0ull, ko = 0ull;
   uint32_t tw = 0;

@@ -664,9 +664,23 @@ __global__ void __launch_bounds__(512) k_link_apply(const uint2* __restrict__ re
   __shared__ int32_t sp[FB];
   const int64_t base = (int64_t)blockIdx.x << FB_BITS;
   const int cnt = n - base < FB ? (int)(n - base) : FB;
-  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-    const uint2 r = __ldcs(recs + base + i);
-    sp[r.x - (uint32_t)base] = (int32_t)r.y;
+  if (cnt == FB) {
+    // full window: all 16 records of a thread in flight at once (two per 16-B load)
+    constexpr int V = FB / 2 / 512;
+    const uint4* r4 = reinterpret_cast<const uint4*>(recs + base);
+    uint4 x[V];
+#pragma unroll
+    for (int q = 0; q < V; ++q) x[q] = __ldcs(r4 + q * 512 + threadIdx.x);
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      sp[x[q].x - (uint32_t)base] = (int32_t)x[q].y;
+      sp[x[q].z - (uint32_t)base] = (int32_t)x[q].w;
+    }
+  } else {
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const uint2 r = __ldcs(recs + base + i);
+      sp[r.x - (uint32_t)base] = (int32_t)r.y;
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < cnt; i += blockDim.x) __stcs(edge_parent + base + i, sp[i]);

@@ -85,6 +85,9 @@ typedef struct dmst_stats {
                                bit 2: wide keys never finish in shared memory (full LSD sort) */
   int32_t sort2_geometry;   /* chain-sort tiles: 1 = 512 x 16, 2 = 256 x 20 (two CTAs per SM);
                                0 = by size (2 from 32M edges) */
+  int32_t mi_apply_mode;    /* bucketed maxIncident: 1 = two multisplit passes + shared-memory
+                               apply per 8192-vertex bucket, 2 = one pass into 4M-vertex slices
+                               + L2-resident 64-bit atomics + k_v1; 0 = the library's choice */
   /* out: the path this call took (what bench.py's byte model reads) */
   int32_t sort1_narrow;     /* 1 = the edge sort ran on 32-bit keys */
   int32_t sort1_compacted;  /* 1 = the sign/exponent field was replaced by its dense code */
@@ -92,6 +95,7 @@ typedef struct dmst_stats {
   int32_t tail_level;       /* first view finished inside k_tail, -1 = none */
   int32_t sort1_local;      /* 1 = wide keys: top three digits sorted globally, the rest per
                                window in shared memory; 2 = a window overflowed, full LSD ran */
+  int32_t mi_sliced;        /* 1 = some view's maxIncident took the sliced L2-atomic apply */
   uint64_t mi_bucketed;     /* bit k: view k's maxIncident was bucketed */
   uint64_t mi_direct;       /* bit k: view k's maxIncident took direct atomics */
 } dmst_stats;

@@ -60,17 +60,19 @@ class DmstStats(ctypes.Structure):
         ("direct_mi_bytes", ctypes.c_int64),
         ("sort1_mode", ctypes.c_int32),
         ("sort2_geometry", ctypes.c_int32),
+        ("mi_apply_mode", ctypes.c_int32),
         ("sort1_narrow", ctypes.c_int32),
         ("sort1_compacted", ctypes.c_int32),
         ("sort2_geometry_used", ctypes.c_int32),
         ("tail_level", ctypes.c_int32),
         ("sort1_local", ctypes.c_int32),
+        ("mi_sliced", ctypes.c_int32),
         ("mi_bucketed", ctypes.c_uint64),
         ("mi_direct", ctypes.c_uint64),
     ]
 
     # code-path overrides accepted by DendrogramBuilder.build(paths=...)
-    PATH_OPTIONS = ("tail_edges", "direct_mi_bytes", "sort1_mode", "sort2_geometry")
+    PATH_OPTIONS = ("tail_edges", "direct_mi_bytes", "sort1_mode", "sort2_geometry", "mi_apply_mode")
 
     def set_paths(self, paths: dict | None) -> None:
         for k, v in (paths or {}).items():
@@ -84,6 +86,7 @@ class DmstStats(ctypes.Structure):
         return {"sort1_passes": int(self.sort1_passes), "sort1_narrow": bool(self.sort1_narrow),
                 "sort1_compacted": bool(self.sort1_compacted),
                 "sort1_local": {0: None, 1: "smem", 2: "fallback"}[int(self.sort1_local)],
+                "mi_sliced": bool(self.mi_sliced),
                 "sort2_passes": int(self.sort2_passes),
                 "sort2_geometry": SORT2_GEOMETRIES[int(self.sort2_geometry_used)],
                 "tail_level": int(self.tail_level),

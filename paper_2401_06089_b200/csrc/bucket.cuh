@@ -406,6 +406,42 @@ __global__ void __launch_bounds__(BLOCK) k_split(Src src, int64_t m, uint32_t gs
   }
 }
 
+// Alternative apply for records grouped by 4M-vertex SLICE (pass A only,
+// coarse bucket = slice): one 64-bit atomicMax per record into mi64, which
+// was zeroed; CTAs run in record order, so the slice being updated (32 MB of
+// mi64) stays L2-resident (L2 atomics: ~210 G/s vs ~30 G/s DRAM-resident,
+// tools/randbench.cu).  V1 (parents, child counts) then runs as k_v1.
+constexpr int kSliceBits = 22;  // 4M vertices = 32 MB of mi64 per slice
+constexpr int kMiAtomicGroups = 4;  // groups of 4 records (48 B = three 16-B loads) per thread
+__global__ void __launch_bounds__(256) k_mi_atomic(Recs rec, int64_t m, unsigned long long* __restrict__ mi64) {
+  constexpr int G = kMiAtomicGroups;
+  const int64_t g0 = (int64_t)blockIdx.x * 256 * G + threadIdx.x;  // group index
+  const int64_t ng = m / 4;
+  const uint4* r4 = reinterpret_cast<const uint4*>(rec.r);
+  uint4 a[G][3];
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    const int64_t g = g0 + q * 256;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) a[q][t] = g < ng ? ld_stream(r4 + 3 * g + t) : make_uint4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    const uint32_t w[12] = {a[q][0].x, a[q][0].y, a[q][0].z, a[q][0].w, a[q][1].x, a[q][1].y,
+                            a[q][1].z, a[q][1].w, a[q][2].x, a[q][2].y, a[q][2].z, a[q][2].w};
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const unsigned long long pk = ((unsigned long long)w[3 * r + 1] << 32) | w[3 * r + 2];
+      if (pk) atomicMax(mi64 + w[3 * r], pk);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (m & 3)) {  // the last m % 4 records
+    const int64_t i = (m & ~int64_t(3)) + threadIdx.x;
+    const unsigned long long pk = ((unsigned long long)ld_stream(rec.r + 3 * i + 1) << 32) | ld_stream(rec.r + 3 * i + 2);
+    if (pk) atomicMax(mi64 + ld_stream(rec.r + 3 * i), pk);
+  }
+}
+
 // One CTA per fine bucket: reduce its records in shared memory (max rank,
 // then the winning record's other end) and write, for every vertex x of the
 // bucket: mi64[x] = ((j + 1) << 32) | other (0 if isolated), V1's parent

@@ -244,9 +244,11 @@ struct Paths {
   int64_t direct_mi_bytes = kDirectMiBytes;
   int sort1_mode = 0;
   int sort2_geometry = 0;
+  int mi_apply_mode = 0;  // 0 / 1: shared-memory apply per fine bucket; 2: slices + L2 atomics
   // out
   int sort1_narrow = 0, sort1_compacted = 0, sort2_geometry_used = 0, tail_level = -1;
   int sort1_local = 0;  // 1 = wide keys finished in shared memory, 2 = tried, fell back to full LSD
+  int mi_sliced_used = 0;
   uint64_t mi_bucketed = 0, mi_direct = 0;
 };
 
@@ -627,7 +629,13 @@ uint32_t coarse_shift(uint32_t nf) {
 template <class Src>
 void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiApplyOut out) {
   const uint32_t nf = (uint32_t)cdiv(nv, FB);
-  const uint32_t gshift = coarse_shift(nf);
+  // sliced: one multisplit pass into 4M-vertex slices, then L2-resident
+  // atomics (config 4: 22.1 -> 21.6 ms; config 1: 0.72 -> 0.57 ms).  Default
+  // for views of >= 16M or <= 1M vertices; in between (8M-edge trees, built
+  // several per GPU at once, whose slices contend for L2: config 5 100.7 vs
+  // 101.7 ms) the shared-memory apply
+  const bool sliced = c.paths.mi_apply_mode ? c.paths.mi_apply_mode == 2 : (nv >= (16 << 20) || nv <= (1 << 20));
+  const uint32_t gshift = sliced ? (uint32_t)(kSliceBits - FB_BITS) : coarse_shift(nf);
   uint32_t* counts = c.w.fine;
   uint32_t* fine_base = counts + (nf + 2);
   uint32_t* fine_cur = fine_base + (nf + 2);
@@ -648,9 +656,21 @@ void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiAp
   auto kB = k_split<true, AosRecSrc<3>, BKB_BLOCK, BKB_ITEMS, BKB_SPAN>;
   smem_attr(kA, (int)SA::bytes());
   smem_attr(kB, (int)SB::bytes());
+  if (sliced) c.zero(out.mi64, 8 * (size_t)nv);  // the atomics' starting point
   c.begin(KK_MI_SPLIT_A);
   kA<<<c.persistent_grid(m, SA::T, BKA_PER_SM), BKA_BLOCK, SA::bytes(), c.s>>>(src, m, gshift, coarse_cur, mid);
   c.launched();
+  if (sliced) {
+    c.paths.mi_sliced_used = 1;
+    c.begin(KK_MI_APPLY);
+    k_mi_atomic<<<(unsigned)std::max<int64_t>(1, cdiv(m / 4, 256 * kMiAtomicGroups)), 256, 0, c.s>>>(mid, m,
+                                                                                                   out.mi64);
+    c.launched();
+    c.begin(KK_MI_APPLY);
+    k_v1<<<grid_for(nv, EW_BLOCK), EW_BLOCK, 0, c.s>>>(nv, out.mi64, out.grank, out.parent_out, out.cnt2);
+    c.launched();
+    return;
+  }
   c.begin(KK_MI_SPLIT_B);
   kB<<<c.persistent_grid(m, SB::T, BKB_PER_SM), BKB_BLOCK, SB::bytes(), c.s>>>(AosRecSrc<3>{mid.r}, m, gshift,
                                                                                  fine_cur, fin);
@@ -996,7 +1016,8 @@ void init_ctx(Ctx& c, int64_t n, int64_t nv, void* ws, void* stream, dmst_stats*
   if (st) {
     const int32_t prof = st->profile, wc = st->want_chains;
     const int64_t te = st->tail_edges, dm = st->direct_mi_bytes;
-    const int32_t s1 = st->sort1_mode, s2 = st->sort2_geometry;
+    const int32_t s1 = st->sort1_mode, s2 = st->sort2_geometry, ma = st->mi_apply_mode;
+    if (ma < 0 || ma > 2) invalid("mi_apply_mode must be 0, 1 or 2");
     if (s1 < 0 || s1 > 7) invalid("sort1_mode must be in [0, 7]");
     if (s2 < 0 || s2 > 2) invalid("sort2_geometry must be 0, 1 or 2");
     if (te < -1 || dm < -1) invalid("tail_edges / direct_mi_bytes must be >= -1");
@@ -1007,11 +1028,13 @@ void init_ctx(Ctx& c, int64_t n, int64_t nv, void* ws, void* stream, dmst_stats*
     st->direct_mi_bytes = dm;
     st->sort1_mode = s1;
     st->sort2_geometry = s2;
+    st->mi_apply_mode = ma;
     c.profile = prof != 0;
     if (te) c.paths.tail_edges = te;  // -1: n_k <= -1 never holds
     if (dm) c.paths.direct_mi_bytes = dm;
     c.paths.sort1_mode = s1;
     c.paths.sort2_geometry = s2;
+    c.paths.mi_apply_mode = ma;
   }
 }
 
@@ -1020,6 +1043,7 @@ void report_paths(const Ctx& c, dmst_stats* st) {
   st->sort1_narrow = c.paths.sort1_narrow;
   st->sort1_compacted = c.paths.sort1_compacted;
   st->sort1_local = c.paths.sort1_local;
+  st->mi_sliced = c.paths.mi_sliced_used;
   st->sort2_geometry_used = c.paths.sort2_geometry_used;
   st->tail_level = c.paths.tail_level;
   st->mi_bucketed = c.paths.mi_bucketed;

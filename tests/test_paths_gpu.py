@@ -44,6 +44,10 @@ PATHS = {
     "nocompact_bucketed": {"sort1_mode": 2, "sort2_geometry": 1, "direct_mi_bytes": -1, "tail_edges": -1},
     # wide keys always sorted by the full LSD (no shared-memory finish)
     "no_local": {"sort1_mode": 4},
+    # bucketed maxIncident by 4M-vertex slices + L2 atomics on every view >= 0; no tail
+    "sliced": {"mi_apply_mode": 2, "direct_mi_bytes": -1, "tail_edges": -1},
+    # the shared-memory apply forced
+    "smem_apply": {"mi_apply_mode": 1},
 }
 
 SEEN_KINDS: dict[str, int] = {}   # kernel kind -> launches inside checked builds
@@ -108,6 +112,10 @@ def _assert_path_taken(res, paths):
         assert not info["sort1_compacted"]
     if p.get("sort1_mode", 0) & 4:
         assert info["sort1_local"] is None
+    if p.get("mi_apply_mode") == 2:
+        assert info["mi_sliced"]
+    if p.get("mi_apply_mode") == 1:
+        assert not info["mi_sliced"]
     if p.get("sort2_geometry") and info["sort2_passes"]:
         from paper_2401_06089_b200._lib import SORT2_GEOMETRIES
         assert info["sort2_geometry"] == SORT2_GEOMETRIES[p["sort2_geometry"]]

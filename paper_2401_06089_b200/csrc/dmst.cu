@@ -252,9 +252,30 @@ struct Paths {
   uint64_t mi_bucketed = 0, mi_direct = 0;
 };
 
+// Per host thread (and device): an auxiliary stream and two events, so a
+// table the sliced maxIncident will update can be zeroed while the edge sort
+// runs (the sort is bound by shared-memory work, not DRAM).
+struct AuxStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev[2] = {};
+};
+AuxStream& aux_stream() {
+  thread_local std::unordered_map<int, AuxStream> m;
+  int dev = 0;
+  DMST_CUDA(cudaGetDevice(&dev));
+  AuxStream& a = m[dev];
+  if (!a.s) {
+    DMST_CUDA(cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking));
+    for (auto& e : a.ev) DMST_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  return a;
+}
+
 struct Ctx {
   cudaStream_t s;
   Workspace w;
+  const void* prezeroed = nullptr;  // table zeroed on the aux stream (ready after aux ev[1])
+  size_t prezeroed_bytes = 0;
   int launches = 0;
   int sms = 148;
   bool profile = false;
@@ -345,6 +366,26 @@ struct Ctx {
     return (unsigned)std::min<int64_t>(grid_for(work, block), (int64_t)sms * per_sm);
   }
 };
+
+// Zero `bytes` at `p` on the aux stream, after the work already on c.s.
+void prezero(Ctx& c, void* p, size_t bytes) {
+  AuxStream& a = aux_stream();
+  DMST_CUDA(cudaEventRecord(a.ev[0], c.s));
+  DMST_CUDA(cudaStreamWaitEvent(a.s, a.ev[0], 0));
+  DMST_CUDA(cudaMemsetAsync(p, 0, bytes, a.s));
+  DMST_CUDA(cudaEventRecord(a.ev[1], a.s));
+  c.prezeroed = p;
+  c.prezeroed_bytes = bytes;
+}
+// `bytes` at `p` are zero once c.s reaches this point (prezeroed or memset now).
+void zero_for_atomics(Ctx& c, void* p, size_t bytes) {
+  if (c.prezeroed == p && bytes <= c.prezeroed_bytes) {
+    DMST_CUDA(cudaStreamWaitEvent(c.s, aux_stream().ev[1], 0));
+    c.prezeroed = nullptr;
+  } else {
+    c.zero(p, bytes);
+  }
+}
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and device
 // (a host API call per launch would add latency inside the level loop).
@@ -626,6 +667,10 @@ uint32_t coarse_shift(uint32_t nf) {
   return gshift;
 }
 
+bool mi_sliced(const Ctx& c, int64_t nv) {
+  return c.paths.mi_apply_mode ? c.paths.mi_apply_mode == 2 : (nv >= (16 << 20) || nv <= (1 << 20));
+}
+
 template <class Src>
 void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiApplyOut out) {
   const uint32_t nf = (uint32_t)cdiv(nv, FB);
@@ -634,7 +679,7 @@ void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiAp
   // for views of >= 16M or <= 1M vertices; in between (8M-edge trees, built
   // several per GPU at once, whose slices contend for L2: config 5 100.7 vs
   // 101.7 ms) the shared-memory apply
-  const bool sliced = c.paths.mi_apply_mode ? c.paths.mi_apply_mode == 2 : (nv >= (16 << 20) || nv <= (1 << 20));
+  const bool sliced = mi_sliced(c, nv);
   const uint32_t gshift = sliced ? (uint32_t)(kSliceBits - FB_BITS) : coarse_shift(nf);
   uint32_t* counts = c.w.fine;
   uint32_t* fine_base = counts + (nf + 2);
@@ -656,7 +701,7 @@ void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiAp
   auto kB = k_split<true, AosRecSrc<3>, BKB_BLOCK, BKB_ITEMS, BKB_SPAN>;
   smem_attr(kA, (int)SA::bytes());
   smem_attr(kB, (int)SB::bytes());
-  if (sliced) c.zero(out.mi64, 8 * (size_t)nv);  // the atomics' starting point
+  if (sliced) zero_for_atomics(c, out.mi64, 8 * (size_t)nv);  // the atomics' starting point
   c.begin(KK_MI_SPLIT_A);
   kA<<<c.persistent_grid(m, SA::T, BKA_PER_SM), BKA_BLOCK, SA::bytes(), c.s>>>(src, m, gshift, coarse_cur, mid);
   c.launched();
@@ -1063,6 +1108,7 @@ static int build_impl(const int32_t* u, const int32_t* v, const double* w, int64
     init_ctx(c, n, nv, ws, stream, st);
     c.io = io;
     if (inputs_ready) DMST_CUDA(cudaStreamWaitEvent(c.s, inputs_ready, 0));
+    if (mi_sliced(c, nv)) prezero(c, c.w.mi64_0, 8 * (size_t)nv);  // overlaps the edge sort
     Sort1FinalEmitter em{orig_of, heights, c.w.euv0, nullptr, nullptr};
     int p1 = 0;
     edge_sort(c, u, v, w, n, em, &p1);

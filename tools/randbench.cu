@@ -29,6 +29,12 @@ __global__ void amax(const uint32_t* __restrict__ idx, int* dst, int64_t n) {
   for (int k = 0; k < ILP; ++k) { int64_t i = base + k * blockDim.x; if (i < n) atomicMax(dst + idx[i], (int)i); }
 }
 template <int ILP>
+__global__ void amax64(const uint32_t* __restrict__ idx, unsigned long long* dst, int64_t n) {
+  int64_t base = (blockIdx.x * (int64_t)blockDim.x) * ILP + threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < ILP; ++k) { int64_t i = base + k * blockDim.x; if (i < n) atomicMax(dst + idx[i], (unsigned long long)i << 20); }
+}
+template <int ILP>
 __global__ void scatter(const uint32_t* __restrict__ idx, int* dst, int64_t n) {
   int64_t base = (blockIdx.x * (int64_t)blockDim.x) * ILP + threadIdx.x;
 #pragma unroll
@@ -66,6 +72,7 @@ int main(int argc, char** argv) {
     run("gather4", [&] { gather<4><<<(n / 4 + 255) / 256, 256>>>(idx, src, out, n); });
     run("gather8", [&] { gather<8><<<(n / 8 + 255) / 256, 256>>>(idx, src, out, n); });
     run("amax4", [&] { amax<4><<<(n / 4 + 255) / 256, 256>>>(idx, dst, n); });
+    if (range <= (32u << 20)) run("amax64", [&] { amax64<4><<<(n / 4 + 255) / 256, 256>>>(idx, (unsigned long long*)out, n); });
     run("scatter4", [&] { scatter<4><<<(n / 4 + 255) / 256, 256>>>(idx, dst, n); });
   }
   cudaError_t e = cudaGetLastError(); printf("err: %s\n", cudaGetErrorString(e));

@@ -411,7 +411,10 @@ __global__ void __launch_bounds__(BLOCK) k_split(Src src, int64_t m, uint32_t gs
 // was zeroed; CTAs run in record order, so the slice being updated (32 MB of
 // mi64) stays L2-resident (L2 atomics: ~210 G/s vs ~30 G/s DRAM-resident,
 // tools/randbench.cu).  V1 (parents, child counts) then runs as k_v1.
-constexpr int kSliceBits = 22;  // 4M vertices = 32 MB of mi64 per slice
+#ifndef DMST_SLICE_BITS
+#define DMST_SLICE_BITS 21
+#endif
+constexpr int kSliceBits = DMST_SLICE_BITS;  // 2M vertices = 16 MB of mi64 per slice (22: 32 MB, 21.64 vs 21.59 ms; 23: 22.6 ms)
 constexpr int kMiAtomicGroups = 4;  // groups of 4 records (48 B = three 16-B loads) per thread
 __global__ void __launch_bounds__(256) k_mi_atomic(Recs rec, int64_t m, unsigned long long* __restrict__ mi64) {
   constexpr int G = kMiAtomicGroups;

@@ -510,7 +510,7 @@ uint64_t var_of(const unsigned long long (&ao)[2], const uint8_t* code, int ncod
 
 // Sort #1 (rank_edges): orig_of, heights, euv (and/or ru, rv).
 void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int64_t n,
-               Sort1FinalEmitter em, int* passes_out) {
+               Sort1FinalEmitter em, int* passes_out, void* zero_ptr = nullptr, size_t zero_bytes = 0) {
   unsigned long long* sample_ao = (unsigned long long*)(c.w.small + SM_HIST1);
   unsigned long long* and_or = sample_ao + 2;
   uint32_t* top_min = c.w.small + SM_HIST1 + 8;
@@ -554,6 +554,9 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
   c.to_host(&nz, negzero, 4);
   c.to_host(tb, top_bits, sizeof(tb));
   c.sync();
+  // a table a later stage needs zeroed: cleared on the aux stream while the
+  // (shared-memory-bound) radix passes run
+  if (zero_ptr) prezero(c, zero_ptr, zero_bytes);
   const int d0 = (int)d0u;  // = predict_first_digit(sample AND, OR)
   const bool local_guess = !(c.paths.sort1_mode & 4) && active_digits(sao[0], sao[1], 8, 64).size() >= 5;
   std::vector<int> shifts = active_digits(ao[0], ao[1], 8, 64);
@@ -674,7 +677,7 @@ bool mi_sliced(const Ctx& c, int64_t nv) {
 template <class Src>
 void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiApplyOut out) {
   const uint32_t nf = (uint32_t)cdiv(nv, FB);
-  // sliced: one multisplit pass into 4M-vertex slices, then L2-resident
+  // sliced: one multisplit pass into 2M-vertex slices, then L2-resident
   // atomics (config 4: 22.1 -> 21.6 ms; config 1: 0.72 -> 0.57 ms).  Default
   // for views of >= 16M or <= 1M vertices; in between (8M-edge trees, built
   // several per GPU at once, whose slices contend for L2: config 5 100.7 vs
@@ -1108,10 +1111,10 @@ static int build_impl(const int32_t* u, const int32_t* v, const double* w, int64
     init_ctx(c, n, nv, ws, stream, st);
     c.io = io;
     if (inputs_ready) DMST_CUDA(cudaStreamWaitEvent(c.s, inputs_ready, 0));
-    if (mi_sliced(c, nv)) prezero(c, c.w.mi64_0, 8 * (size_t)nv);  // overlaps the edge sort
     Sort1FinalEmitter em{orig_of, heights, c.w.euv0, nullptr, nullptr};
     int p1 = 0;
-    edge_sort(c, u, v, w, n, em, &p1);
+    const bool sl = mi_sliced(c, nv);  // view 0's table, zeroed during the edge sort's passes
+    edge_sort(c, u, v, w, n, em, &p1, sl ? c.w.mi64_0 : nullptr, sl ? 8 * (size_t)nv : 0);
     if (io) {
       c.copy_out(0, io->h_orig, orig_of, 4 * (size_t)n);
       c.copy_out(1, io->h_heights, heights, 8 * (size_t)n);

@@ -87,7 +87,9 @@ typedef struct dmst_stats {
                                0 = by size (2 from 32M edges) */
   int32_t mi_apply_mode;    /* bucketed maxIncident: 1 = two multisplit passes + shared-memory
                                apply per 8192-vertex bucket, 2 = one pass into 4M-vertex slices
-                               + L2-resident 64-bit atomics + k_v1; 0 = the library's choice */
+                               + L2-resident 64-bit atomics + k_v1; 0 = the library's choice.
+                               The link stage follows it: 1 = two passes + shared-memory
+                               apply, 2 = one pass into 2M-rank slices + L2-resident stores */
   /* out: the path this call took (what bench.py's byte model reads) */
   int32_t sort1_narrow;     /* 1 = the edge sort ran on 32-bit keys */
   int32_t sort1_compacted;  /* 1 = the sign/exponent field was replaced by its dense code */

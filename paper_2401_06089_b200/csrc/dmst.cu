@@ -1018,7 +1018,10 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     // (rank, parent) records grouped by 8192-rank window: R[20n, 28n) -> R[28n, 36n)
     uint32_t* recA = (uint32_t*)(w.R + align_up(20 * n));
     uint32_t* recB = (uint32_t*)(w.R + align_up(28 * n));
-    const uint32_t nf = (uint32_t)cdiv(n, FB), gshift = coarse_shift(nf);
+    // sliced (as the maxIncident apply): one multisplit pass into 2M-rank
+    // slices + L2-resident scatter, instead of two passes + a shared-memory apply
+    const bool lsl = mi_sliced(c, n);
+    const uint32_t nf = (uint32_t)cdiv(n, FB), gshift = lsl ? (uint32_t)(kSliceBits - FB_BITS) : coarse_shift(nf);
     const uint32_t nc = (uint32_t)cdiv(nf, 1u << gshift);
     uint32_t* fine_cur = w.fine;
     uint32_t* coarse_cur = w.fine + (nf + 2);
@@ -1035,6 +1038,13 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     kA<<<c.persistent_grid(n, LA::T, BKA_PER_SM), BKA_BLOCK, LA::bytes(), c.s>>>(
         LinkSortedSrc{(const unsigned long long*)fin.keys, w.smi_all}, n, gshift, coarse_cur, Recs{recA});
     c.launched();
+    if (lsl) {
+      c.begin(KK_LINK_APPLY);
+      k_link_scatter<<<(unsigned)std::max<int64_t>(1, cdiv(n / 2, 256 * 4)), 256, 0, c.s>>>((const uint2*)recA, n,
+                                                                                          edge_parent);
+      c.launched();
+      return;
+    }
     c.begin(KK_LINK_SPLIT);
     kB<<<c.persistent_grid(n, LB::T, BKB_PER_SM), BKB_BLOCK, LB::bytes(), c.s>>>(AosRecSrc<2>{recA}, n, gshift,
                                                                                  fine_cur, Recs{recB});

@@ -657,6 +657,33 @@ __global__ void k_link_cursors(uint32_t* __restrict__ coarse, uint32_t nc, uint3
   }
 }
 
+// Sliced link: (rank, parent) records grouped by 2M-rank slice (one
+// multisplit pass); plain 4-B stores into edge_parent in record order, so the
+// slice being written (8 MB) stays L2-resident and its partial sectors merge
+// there (random stores into an L2-resident table: ~210 G/s, tools/randbench.cu).
+__global__ void __launch_bounds__(256) k_link_scatter(const uint2* __restrict__ recs, int64_t n,
+                                                      int32_t* __restrict__ edge_parent) {
+  constexpr int G = 4;  // 16-B loads (two records) in flight per thread
+  const int64_t p0 = (int64_t)blockIdx.x * 256 * G + threadIdx.x;
+  const uint4* r4 = reinterpret_cast<const uint4*>(recs);
+  const int64_t np = n / 2;
+  uint4 a[G];
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    const int64_t p = p0 + q * 256;
+    a[q] = p < np ? __ldcs(r4 + p) : make_uint4(0xffffffffu, 0, 0xffffffffu, 0);
+  }
+#pragma unroll
+  for (int q = 0; q < G; ++q) {
+    if (a[q].x != 0xffffffffu) edge_parent[a[q].x] = (int32_t)a[q].y;
+    if (a[q].z != 0xffffffffu) edge_parent[a[q].z] = (int32_t)a[q].w;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) {
+    const uint2 r = __ldcs(recs + n - 1);
+    edge_parent[r.x] = (int32_t)r.y;
+  }
+}
+
 // One CTA per 8192-rank window: place its (rank, parent) records in shared
 // memory, then store the window's edge_parent slice coalesced.
 __global__ void __launch_bounds__(512) k_link_apply(const uint2* __restrict__ recs, int64_t n,

@@ -415,6 +415,16 @@ __global__ void __launch_bounds__(BLOCK) k_split(Src src, int64_t m, uint32_t gs
 #define DMST_SLICE_BITS 21
 #endif
 constexpr int kSliceBits = DMST_SLICE_BITS;  // 2M vertices = 16 MB of mi64 per slice (22: 32 MB, 21.64 vs 21.59 ms; 23: 22.6 ms)
+// Coarse cursors of the sliced split from per-slice counts (<= 256 slices).
+__global__ void __launch_bounds__(256) k_slice_scan(const uint32_t* __restrict__ counts, uint32_t ns,
+                                                    uint32_t* __restrict__ coarse_cur) {
+  __shared__ uint32_t scratch[256 / 32 + 1];
+  const uint32_t c = threadIdx.x < ns ? counts[threadIdx.x] : 0u;
+  uint32_t tot;
+  const uint32_t run = block_excl_sum<256>(c, scratch, &tot);
+  if (threadIdx.x < ns) coarse_cur[threadIdx.x] = run;
+}
+
 constexpr int kMiAtomicGroups = 4;  // groups of 4 records (48 B = three 16-B loads) per thread
 __global__ void __launch_bounds__(256) k_mi_atomic(Recs rec, int64_t m, unsigned long long* __restrict__ mi64) {
   constexpr int G = kMiAtomicGroups;

@@ -276,6 +276,7 @@ struct Ctx {
   Workspace w;
   const void* prezeroed = nullptr;  // table zeroed on the aux stream (ready after aux ev[1])
   size_t prezeroed_bytes = 0;
+  bool slices_counted = false;      // the edge sort counted view 0's endpoints per slice (w.fine)
   int launches = 0;
   int sms = 148;
   bool profile = false;
@@ -616,6 +617,8 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
     Sort1Emitter<uint32_t> em32{em.orig_of, em.heights, em.euv, em.ru, em.rv, em.inv,
                                 lo ? kand & ((1ull << lo) - 1) : 0ull, (uint32_t)lo};
     em32.base |= lo + 32 < 64 ? kand & ~((1ull << (lo + 32)) - 1) : 0ull;
+    em32.scount = em.scount;
+    em32.sshift = em.sshift;
     run_sort<uint32_t, 3, S1N_BLOCK, S1N_ITEMS, S1N_MINB, 8>(
         c, {KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL}, n, s32, bufK, bufP,
         Sort1Loader<uint32_t>{w, u, v, code, (uint32_t)lo}, em32, ready >= 0 ? 0 : -1, S1_ALIGN);
@@ -657,6 +660,9 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
                                                          shifts, bufK, bufP, Sort1FirstLoader{w, u, v, code}, em,
                                                          local ? -1 : ready, S1_ALIGN, S1N_MINB);
   }
+  // the final output came from an emitter that counted the slices unless the
+  // shared-memory finish wrote it
+  c.slices_counted = em.scount != nullptr && c.paths.sort1_local != 1;
   if (nz) {
     c.begin(KK_OTHER);
     k_fix_negzero<<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(w, em.orig_of, em.heights, n);
@@ -681,7 +687,8 @@ bool mi_sliced(const Ctx& c, int64_t nv) {
 }
 
 template <class Src>
-void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiApplyOut out) {
+void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiApplyOut out,
+                bool counted = false) {
   const uint32_t nf = (uint32_t)cdiv(nv, FB);
   // sliced: one multisplit pass into 2M-vertex slices, then L2-resident
   // atomics (config 4: 22.1 -> 21.6 ms; config 1: 0.72 -> 0.57 ms).  Default
@@ -694,16 +701,23 @@ void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiAp
   uint32_t* fine_base = counts + (nf + 2);
   uint32_t* fine_cur = fine_base + (nf + 2);
   uint32_t* coarse_cur = fine_cur + (nf + 2);
-  c.zero(counts, 4 * (nf + 1));
-  smem_attr(k_fine_hist<Src>, 4 * FH_WINDOW);
-  for (uint32_t flo = 0; flo < nf; flo += FH_WINDOW) {
+  if (sliced && counted) {
+    // per-slice endpoint counts came with the edge sort's final pass (w.fine[0, 256))
     c.begin(KK_MI_HIST);
-    k_fine_hist<Src><<<c.persistent_grid(m, 256, 3), 256, 4 * FH_WINDOW, c.s>>>(src, m, flo, nf, counts);
+    k_slice_scan<<<1, 256, 0, c.s>>>(counts, (uint32_t)cdiv(nv, int64_t(1) << kSliceBits), coarse_cur);
+    c.launched();
+  } else {
+    c.zero(counts, 4 * (nf + 1));
+    smem_attr(k_fine_hist<Src>, 4 * FH_WINDOW);
+    for (uint32_t flo = 0; flo < nf; flo += FH_WINDOW) {
+      c.begin(KK_MI_HIST);
+      k_fine_hist<Src><<<c.persistent_grid(m, 256, 3), 256, 4 * FH_WINDOW, c.s>>>(src, m, flo, nf, counts);
+      c.launched();
+    }
+    c.begin(KK_MI_HIST);
+    k_fine_scan<<<1, 1024, 0, c.s>>>(counts, nf, gshift, fine_base, fine_cur, coarse_cur);
     c.launched();
   }
-  c.begin(KK_MI_HIST);
-  k_fine_scan<<<1, 1024, 0, c.s>>>(counts, nf, gshift, fine_base, fine_cur, coarse_cur);
-  c.launched();
   using SA = SplitSmem<Src, BKA_BLOCK, BKA_ITEMS, 256>;
   using SB = SplitSmem<AosRecSrc<3>, BKB_BLOCK, BKB_ITEMS, BKB_SPAN>;
   auto kA = k_split<false, Src, BKA_BLOCK, BKA_ITEMS, 256>;
@@ -819,7 +833,8 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
   // maxIncident + V1 of the input view: 2n records generated from euv0
   c.zero(w.cnt2, 4 * (n / 16 + 2));
   mi_buckets(c, EdgeRecSrc{w.euv0}, 2 * n, nv, recs_at(w.R, 2 * n), recs_at(w.R + 24 * n, 2 * n),
-             MiApplyOut{w.mi64_0, vertex_parent, nullptr, w.cnt2});
+             MiApplyOut{w.mi64_0, vertex_parent, nullptr, w.cnt2}, c.slices_counted);
+  c.slices_counted = false;
   // view 1's table (<= n/2 + 1 vertices) zeroed on the aux stream during view 0,
   // when view 1 will take the sliced apply (~0.26 n vertices on random trees)
   join_aux(c);
@@ -949,6 +964,11 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     es.reset_misc = misc + 1;
     es.reset_status = w.sel_status;
     es.n_status = 2 * (int64_t)ls_tiles;
+    // a sliced next view gets its per-slice endpoint counts from this pass
+    const bool count_next = !direct && n_next > 0 && mi_sliced(c, nv_next);
+    es.scount = count_next ? w.fine : nullptr;
+    es.sshift = kSliceBits;
+    if (count_next) c.zero(w.fine, 4 * 256);
     c.begin(KK_SELECT_EDGES);
     k_select_edges<<<c.persistent_grid(n_k, SEL_BLOCK * SEL_U, 8), SEL_BLOCK, 0, c.s>>>(n_k, es);
     c.launched();
@@ -956,7 +976,7 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     if (!direct && n_next > 0) {
       const int64_t m = 2 * n_next;
       mi_buckets(c, EdgeRecSrc{es.euv_next}, m, nv_next, recs_at(w.R, m), Recs{rec},
-                 MiApplyOut{mi_next, w.smi_all + lt.soff[level + 1], w.grank[cur ^ 1], w.cnt2});
+                 MiApplyOut{mi_next, w.smi_all + lt.soff[level + 1], w.grank[cur ^ 1], w.cnt2}, count_next);
       v1_done = true;
     }
     // next view
@@ -1140,6 +1160,11 @@ static int build_impl(const int32_t* u, const int32_t* v, const double* w, int64
     Sort1FinalEmitter em{orig_of, heights, c.w.euv0, nullptr, nullptr};
     int p1 = 0;
     const bool sl = mi_sliced(c, nv);  // view 0's table, zeroed during the edge sort's passes
+    if (sl) {  // and view 0's endpoints counted per slice by the final pass
+      c.zero(c.w.fine, 4 * 256);
+      em.scount = c.w.fine;
+      em.sshift = kSliceBits;
+    }
     edge_sort(c, u, v, w, n, em, &p1, sl ? c.w.mi64_0 : nullptr, sl ? 8 * (size_t)nv : 0);
     if (io) {
       c.copy_out(0, io->h_orig, orig_of, 4 * (size_t)n);

@@ -143,13 +143,27 @@ using Sort1FirstLoader = Sort1Loader<uint64_t>;
 
 // Final pass: RankedTree outputs (orig_of, w by rank) + rank-order endpoints,
 // written from the sorted sub-tile (payload = (original id, u, v)).
+// With `scount` set it also counts the endpoints per maxIncident slice
+// (vertex >> sshift, <= 256 slices) in shared memory and adds the counts to
+// scount[] at the end: the sliced maxIncident of view 0 then needs no
+// histogram pass over the rank-order endpoints.
+struct SliceCountState {
+  uint32_t h[256];
+};
 template <typename K>
 struct Sort1Emitter {
-  using State = NoEmitState;
+  using State = SliceCountState;
   template <int BLOCK, int R>
-  __device__ __forceinline__ void init(State&) const {}
+  __device__ __forceinline__ void init(State& st) const {
+    if (scount)
+      for (int b = threadIdx.x; b < 256; b += BLOCK) st.h[b] = 0;
+  }
   template <int BLOCK, int R>
-  __device__ __forceinline__ void finish(State&) const {}
+  __device__ __forceinline__ void finish(State& st) const {
+    if (scount)
+      for (int b = threadIdx.x; b < 256; b += BLOCK)
+        if (st.h[b]) atomicAdd(scount + b, st.h[b]);
+  }
   int32_t* __restrict__ orig_of;
   double* __restrict__ heights;
   int2* __restrict__ euv;        // rank-order endpoints (pipeline)
@@ -158,6 +172,8 @@ struct Sort1Emitter {
   const uint16_t* __restrict__ inv;  // top-field compaction: code -> top field (or nullptr)
   uint64_t base;                     // narrow keys: the constant bits outside [lo, lo + 32)
   uint32_t lo;
+  uint32_t* __restrict__ scount = nullptr;  // per-slice endpoint counts (or null)
+  uint32_t sshift = 0;
   // rank r <- item (key kn, original id, u, v)
   __device__ __forceinline__ void put(uint32_t r, K kn, uint32_t id, uint32_t eu, uint32_t ev) const {
     const uint64_t k = base | ((uint64_t)kn << lo);
@@ -170,11 +186,15 @@ struct Sort1Emitter {
     }
   }
   template <int BLOCK, class Tile>
-  __device__ __forceinline__ void emit(const Tile& t, State&) const {
+  __device__ __forceinline__ void emit(const Tile& t, State& st) const {
     for (int s = threadIdx.x; s < t.cnt; s += BLOCK) {
       const K kn = t.skeys[s];
       const uint32_t* p = t.spay + 3 * s;
       put(t.gofs[digit_of<kRadixBits>(kn, t.shift)] + (uint32_t)s, kn, p[0], p[1], p[2]);
+      if (scount) {
+        atomicAdd(&st.h[p[1] >> sshift], 1u);
+        atomicAdd(&st.h[p[2] >> sshift], 1u);
+      }
     }
   }
 };
@@ -462,10 +482,17 @@ struct EdgeSel {
   uint32_t* __restrict__ reset_misc;   // level counters (15 words) zeroed for the next view
   uint32_t* __restrict__ reset_status; // leafscan look-back words zeroed for the next view
   int64_t n_status;
+  uint32_t* __restrict__ scount;     // next view sliced: its endpoints counted per slice (or null)
+  uint32_t sshift;
 };
 
 constexpr int SEL_U = 4;  // edges per thread per iteration (gathers in flight together)
 __global__ void __launch_bounds__(SEL_BLOCK) k_select_edges(int64_t n, EdgeSel es) {
+  __shared__ uint32_t shist[256];  // per-slice endpoint counts of the next view (es.scount)
+  if (es.scount) {
+    for (int b = threadIdx.x; b < 256; b += SEL_BLOCK) shist[b] = 0;
+    __syncthreads();
+  }
   {  // the host has read this view's counters: clear them for the next view
     const int64_t g = (int64_t)blockIdx.x * SEL_BLOCK + threadIdx.x;
     for (int64_t i = g; i < es.n_status; i += (int64_t)gridDim.x * SEL_BLOCK) es.reset_status[i] = 0u;
@@ -510,12 +537,21 @@ __global__ void __launch_bounds__(SEL_BLOCK) k_select_edges(int64_t n, EdgeSel e
       } else {
         __stcs(es.euv_next + pos[q], make_int2(a[q], bb[q]));
         __stcs(es.grank_next + pos[q], g[q]);
+        if (es.scount) {
+          atomicAdd(&shist[(uint32_t)a[q] >> es.sshift], 1u);
+          atomicAdd(&shist[(uint32_t)bb[q] >> es.sshift], 1u);
+        }
         if (es.mi64_next) {
           atomicMax(es.mi64_next + a[q], pack_mi(pos[q] + 1u, (uint32_t)bb[q]));
           atomicMax(es.mi64_next + bb[q], pack_mi(pos[q] + 1u, (uint32_t)a[q]));
         }
       }
     }
+  }
+  if (es.scount) {
+    __syncthreads();
+    for (int b = threadIdx.x; b < 256; b += SEL_BLOCK)
+      if (shist[b]) atomicAdd(es.scount + b, shist[b]);
   }
 }
 

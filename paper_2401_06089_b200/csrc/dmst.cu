@@ -655,14 +655,15 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
       c.paths.sort1_local = done ? 1 : 2;
       if (passes_out) *passes_out = done ? 3 : (int)shifts.size();
     }
+    if (!done && local && em.scount) c.zero(em.scount, 4 * 256);  // windows that finished counted already
     if (!done)
       run_sort<uint64_t, 3, S1_BLOCK, S1_ITEMS, S1_MINB, 8>(c, {KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL}, n,
                                                          shifts, bufK, bufP, Sort1FirstLoader{w, u, v, code}, em,
                                                          local ? -1 : ready, S1_ALIGN, S1N_MINB);
   }
-  // the final output came from an emitter that counted the slices unless the
-  // shared-memory finish wrote it
-  c.slices_counted = em.scount != nullptr && c.paths.sort1_local != 1;
+  // whichever kernel wrote the final output (radix pass, identity pass or the
+  // shared-memory finish) counted the slices
+  c.slices_counted = em.scount != nullptr;
   if (nz) {
     c.begin(KK_OTHER);
     k_fix_negzero<<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(w, em.orig_of, em.heights, n);

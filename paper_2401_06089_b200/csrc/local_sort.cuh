@@ -69,6 +69,7 @@ struct LocalSmem {
   unsigned long long red[2][LF_BLOCK / 32];
   unsigned long long found[2];
   uint32_t maxb;
+  uint32_t shist[256];  // per-slice endpoint counts (em.scount)
 };
 
 template <class Emitter, class G = LocalGeomDefault>
@@ -295,13 +296,27 @@ __global__ void __launch_bounds__(G::LF_BLOCK, 1024 / G::LF_BLOCK) k_local_final
   // ---- window position idx -> global rank start + idx (payload from the
   // window's 12-B records, L2-resident)
   const uint32_t* pw = a.pay + 3 * start;
+  if (em.scount) {
+    for (int b = tid; b < 256; b += LF_BLOCK) s.shist[b] = 0;
+    __syncthreads();
+  }
 #pragma unroll
   for (int q = 0; q < LF_ITEMS; ++q) {
     const int idx = wbase + q * 32;
     if (q < ipw && idx < W) {
       const uint32_t* p = pw + 3 * x[q];
-      em.put((uint32_t)(start + idx), k[q], __ldg(p), __ldg(p + 1), __ldg(p + 2));
+      const uint32_t eu = __ldg(p + 1), ev = __ldg(p + 2);
+      em.put((uint32_t)(start + idx), k[q], __ldg(p), eu, ev);
+      if (em.scount) {
+        atomicAdd(&s.shist[eu >> em.sshift], 1u);
+        atomicAdd(&s.shist[ev >> em.sshift], 1u);
+      }
     }
+  }
+  if (em.scount) {  // the sliced maxIncident of view 0 needs no histogram pass
+    __syncthreads();
+    for (int b = tid; b < 256; b += LF_BLOCK)
+      if (s.shist[b]) atomicAdd(em.scount + b, s.shist[b]);
   }
 }
 

@@ -425,7 +425,10 @@ __global__ void __launch_bounds__(256) k_slice_scan(const uint32_t* __restrict__
   if (threadIdx.x < ns) coarse_cur[threadIdx.x] = run;
 }
 
-constexpr int kMiAtomicGroups = 4;  // groups of 4 records (48 B = three 16-B loads) per thread
+#ifndef DMST_MI_ATOMIC_G
+#define DMST_MI_ATOMIC_G 4
+#endif
+constexpr int kMiAtomicGroups = DMST_MI_ATOMIC_G;  // groups of 4 records (48 B = three 16-B loads) per thread
 __global__ void __launch_bounds__(256) k_mi_atomic(Recs rec, int64_t m, unsigned long long* __restrict__ mi64) {
   constexpr int G = kMiAtomicGroups;
   const int64_t g0 = (int64_t)blockIdx.x * 256 * G + threadIdx.x;  // group index

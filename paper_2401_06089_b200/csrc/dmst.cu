@@ -1013,10 +1013,20 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     k_debug_chain<<<grid_for(n, EW_BLOCK), EW_BLOCK, 0, c.s>>>(n, keys, w.smi_all, lt, dbg_key, dbg_term, dbg_lvl);
     c.launched();
   }
-  uint32_t kao[2];
-  c.to_host(kao, key_ao, 8);
-  c.sync();
-  const std::vector<int> shifts = active_digits(kao[0], kao[1], S2_BITS, 32);
+  // keys are <= soff[L + 1]: a key range of >= 3 digits (every tree of more
+  // than a few hundred thousand edges) sorts every digit of the range without
+  // reading the keys' AND / OR back (a constant digit would only cost a pass);
+  // smaller ranges read it to skip constant digits and catch single chains
+  std::vector<int> shifts;
+  const int64_t kmax = lt.soff[L + 1];
+  if (kmax >= (int64_t(1) << (2 * S2_BITS))) {
+    for (int sft = 0; sft < 32 && (kmax >> sft) > 0; sft += S2_BITS) shifts.push_back(sft);
+  } else {
+    uint32_t kao[2];
+    c.to_host(kao, key_ao, 8);
+    c.sync();
+    shifts = active_digits(kao[0], kao[1], S2_BITS, 32);
+  }
   if (st) st->sort2_passes = (int)shifts.size();
   // chain sort: keys at R[0, 4n); ping-pong A = R[4n, 12n), B = R[12n, 20n);
   if (shifts.empty()) {  // one chain (all keys equal): rank order is chain order

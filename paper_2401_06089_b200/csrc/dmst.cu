@@ -877,10 +877,22 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     const unsigned ls_tiles = grid_for(words, LS_TILE);
     // look-back words and level counters were zeroed before the loop (view 0)
     // or by the previous view's k_select_edges
-    c.begin(KK_LEAFSCAN);
-    k_leafscan<<<ls_tiles, 256, 0, c.s>>>(words, n_k, w.cnt2, w.kw, w.lw, w.apre, w.sel_status, misc + MISC_LSCTR,
-                                         misc + MISC_COUNTS);
-    c.launched();
+    if (ls_tiles >= 64) {  // large views: reduce-then-scan (no look-back chain)
+      c.begin(KK_LEAFSCAN);
+      k_ls_reduce<<<ls_tiles, 256, 0, c.s>>>(words, n_k, w.cnt2, w.sel_status, misc + MISC_COUNTS);
+      c.launched();
+      c.begin(KK_LEAFSCAN);
+      k_ls_scan<<<1, 1024, 0, c.s>>>(w.sel_status, ls_tiles);
+      c.launched();
+      c.begin(KK_LEAFSCAN);
+      k_ls_apply<<<ls_tiles, 256, 0, c.s>>>(words, n_k, w.cnt2, w.sel_status, w.kw, w.lw, w.apre);
+      c.launched();
+    } else {
+      c.begin(KK_LEAFSCAN);
+      k_leafscan<<<ls_tiles, 256, 0, c.s>>>(words, n_k, w.cnt2, w.kw, w.lw, w.apre, w.sel_status,
+                                           misc + MISC_LSCTR, misc + MISC_COUNTS);
+      c.launched();
+    }
     // V2: supervertex labels (vertex_map).  Runs before the host reads the
     // counts (one sync per level); on the final view its result is unused.
     // view 0: plain vertex map; views >= 1: packed walk table (stride 2)

@@ -369,6 +369,88 @@ __global__ void __launch_bounds__(256) k_leafscan(int64_t words, int64_t ne, con
   }
 }
 
+// The same leaf / alpha numbering as k_leafscan, reduce-then-scan in three
+// short kernels (no tile-to-tile look-back chain, whose propagation bounds
+// the single-pass scan at ~38 ns per tile): per-tile totals, one scan of the
+// totals, per-tile local scan + writes (the 2-bit counts are re-read from L2).
+__global__ void __launch_bounds__(256) k_ls_reduce(int64_t words, int64_t ne, const uint32_t* __restrict__ cnt2,
+                                                   uint32_t* __restrict__ tile_tot, uint32_t* __restrict__ counts) {
+  constexpr int ITEMS = LS_TILE / 256;
+  __shared__ uint32_t scratch[256 / 32 + 1];
+  const int64_t base = (int64_t)blockIdx.x * LS_TILE + (int64_t)threadIdx.x * ITEMS;
+  uint32_t lsum = 0, asum = 0, chains = 0;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint32_t w = base + i < words ? cnt2[base + i] : 0u;
+    lsum += __popc(leaf_bits(w));
+    asum += __popc(alpha_bits(w, base + i, ne));
+    chains += __popc(chain_bits(w));
+  }
+  uint32_t ltot, atot, ctot;
+  block_excl_sum<256>(lsum, scratch, &ltot);
+  block_excl_sum<256>(asum, scratch, &atot);
+  block_excl_sum<256>(chains, scratch, &ctot);
+  if (threadIdx.x == 0) {
+    tile_tot[2 * blockIdx.x] = ltot;
+    tile_tot[2 * blockIdx.x + 1] = atot;
+    atomicAdd(counts + 0, ltot);
+    atomicAdd(counts + 1, ctot);
+  }
+}
+// exclusive scan of the (leaf, alpha) tile totals in place; one CTA
+__global__ void __launch_bounds__(1024) k_ls_scan(uint32_t* __restrict__ tile_tot, uint32_t ntiles) {
+  __shared__ uint32_t scratch[1024 / 32 + 1];
+  const uint32_t per = (ntiles + 1023) / 1024, b = threadIdx.x * per, e = min(ntiles, b + per);
+  uint32_t sl = 0, sa = 0;
+  for (uint32_t t = b; t < e; ++t) {
+    sl += tile_tot[2 * t];
+    sa += tile_tot[2 * t + 1];
+  }
+  uint32_t tl, ta;
+  uint32_t rl = block_excl_sum<1024>(sl, scratch, &tl);
+  uint32_t ra = block_excl_sum<1024>(sa, scratch, &ta);
+  for (uint32_t t = b; t < e; ++t) {
+    const uint32_t xl = tile_tot[2 * t], xa = tile_tot[2 * t + 1];
+    tile_tot[2 * t] = rl;
+    tile_tot[2 * t + 1] = ra;
+    rl += xl;
+    ra += xa;
+  }
+}
+__global__ void __launch_bounds__(256) k_ls_apply(int64_t words, int64_t ne, const uint32_t* __restrict__ cnt2,
+                                                  const uint32_t* __restrict__ tile_pre, uint2* __restrict__ kw,
+                                                  uint2* __restrict__ lw, uint32_t* __restrict__ apre) {
+  constexpr int ITEMS = LS_TILE / 256;
+  __shared__ uint32_t scratch[256 / 32 + 1];
+  const int64_t base = (int64_t)blockIdx.x * LS_TILE + (int64_t)threadIdx.x * ITEMS;
+  uint32_t cw[ITEMS], lsum = 0, asum = 0;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    const uint32_t w = base + i < words ? cnt2[base + i] : 0u;
+    cw[i] = w;
+    lsum += __popc(leaf_bits(w));
+    asum += __popc(alpha_bits(w, base + i, ne));
+  }
+  uint32_t tot;
+  const uint32_t lex = block_excl_sum<256>(lsum, scratch, &tot);
+  const uint32_t aex = block_excl_sum<256>(asum, scratch, &tot);
+  uint32_t lrun = tile_pre[2 * blockIdx.x] + lex, arun = tile_pre[2 * blockIdx.x + 1] + aex;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) {
+    if (base + i < words) {
+      kw[base + i] = make_uint2(cw[i], lrun);
+      apre[base + i] = arun;
+    }
+    if ((i & 1) == 0 && base + i < words) {  // 32-edge leaf bitmap word + leaf prefix (k_v2)
+      const uint32_t lo = even_bits16(leaf_bits(cw[i]));
+      const uint32_t hi = i + 1 < ITEMS ? even_bits16(leaf_bits(cw[i + 1])) : 0u;
+      lw[(base + i) >> 1] = make_uint2(lo | (hi << 16), lrun);
+    }
+    lrun += __popc(leaf_bits(cw[i]));
+    arun += __popc(alpha_bits(cw[i], base + i, ne));
+  }
+}
+
 __device__ __forceinline__ uint32_t leaf_label(uint2 w, uint32_t j) {
   const uint32_t below = (1u << ((j & 15) * 2)) - 1u;
   return w.y + __popc(leaf_bits(w.x) & below);

@@ -257,7 +257,7 @@ struct Paths {
 // runs (the sort is bound by shared-memory work, not DRAM).
 struct AuxStream {
   cudaStream_t s = nullptr;
-  cudaEvent_t ev[2] = {};
+  cudaEvent_t ev[3] = {};  // ev[0]: the build's start on the main stream; ev[1], ev[2]: prezero slots done
 };
 AuxStream& aux_stream() {
   thread_local std::unordered_map<int, AuxStream> m;
@@ -274,8 +274,11 @@ AuxStream& aux_stream() {
 struct Ctx {
   cudaStream_t s;
   Workspace w;
-  const void* prezeroed = nullptr;  // table zeroed on the aux stream (ready after aux ev[1])
-  size_t prezeroed_bytes = 0;
+  struct Prezero {  // a table zeroed on the aux stream (ready after aux ev[1 + slot])
+    const void* p = nullptr;
+    size_t bytes = 0;
+  } pz[2], pz_next;  // pz_next: issue during the next multisplit pass A
+  bool aux_marked = false;
   bool slices_counted = false;      // the edge sort counted view 0's endpoints per slice (w.fine)
   int launches = 0;
   int sms = 148;
@@ -368,30 +371,42 @@ struct Ctx {
   }
 };
 
-// Zero `bytes` at `p` on the aux stream, after the work already on c.s.
-void prezero(Ctx& c, void* p, size_t bytes) {
+// Tables a later stage needs zeroed are cleared on the aux stream while the
+// main stream runs shared-memory-bound kernels.  mark_aux() records the
+// build's start (their last use was in an earlier call on this stream);
+// prezero() may then be issued any time later in the build (issue it after a
+// long kernel's launch so the memset's blocks share SMs with that kernel, not
+// with a tiny one).
+void mark_aux(Ctx& c) {
+  DMST_CUDA(cudaEventRecord(aux_stream().ev[0], c.s));
+  c.aux_marked = true;
+}
+void prezero(Ctx& c, int slot, void* p, size_t bytes) {
+  if (!c.aux_marked) return;  // (zero_for_atomics then memsets in stream order)
   AuxStream& a = aux_stream();
-  DMST_CUDA(cudaEventRecord(a.ev[0], c.s));
   DMST_CUDA(cudaStreamWaitEvent(a.s, a.ev[0], 0));
   DMST_CUDA(cudaMemsetAsync(p, 0, bytes, a.s));
-  DMST_CUDA(cudaEventRecord(a.ev[1], a.s));
-  c.prezeroed = p;
-  c.prezeroed_bytes = bytes;
+  DMST_CUDA(cudaEventRecord(a.ev[1 + slot], a.s));
+  c.pz[slot].p = p;
+  c.pz[slot].bytes = bytes;
 }
-// c.s waits for a pending prezero (before memory it touched may be reused).
+// c.s waits for every pending prezero (before memory one touched may be reused).
 void join_aux(Ctx& c) {
-  if (!c.prezeroed) return;
-  DMST_CUDA(cudaStreamWaitEvent(c.s, aux_stream().ev[1], 0));
-  c.prezeroed = nullptr;
+  for (int slot = 0; slot < 2; ++slot)
+    if (c.pz[slot].p) {
+      DMST_CUDA(cudaStreamWaitEvent(c.s, aux_stream().ev[1 + slot], 0));
+      c.pz[slot].p = nullptr;
+    }
 }
 // `bytes` at `p` are zero once c.s reaches this point (prezeroed or memset now).
 void zero_for_atomics(Ctx& c, void* p, size_t bytes) {
-  if (c.prezeroed == p && bytes <= c.prezeroed_bytes) {
-    DMST_CUDA(cudaStreamWaitEvent(c.s, aux_stream().ev[1], 0));
-    c.prezeroed = nullptr;
-  } else {
-    c.zero(p, bytes);
-  }
+  for (int slot = 0; slot < 2; ++slot)
+    if (c.pz[slot].p == p && bytes <= c.pz[slot].bytes) {
+      DMST_CUDA(cudaStreamWaitEvent(c.s, aux_stream().ev[1 + slot], 0));
+      c.pz[slot].p = nullptr;
+      return;
+    }
+  c.zero(p, bytes);
 }
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and device
@@ -561,9 +576,6 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
   c.to_host(&nz, negzero, 4);
   c.to_host(tb, top_bits, sizeof(tb));
   c.sync();
-  // a table a later stage needs zeroed: cleared on the aux stream while the
-  // (shared-memory-bound) radix passes run
-  if (zero_ptr) prezero(c, zero_ptr, zero_bytes);
   const int d0 = (int)d0u;  // = predict_first_digit(sample AND, OR)
   const bool local_guess = !(c.paths.sort1_mode & 4) && active_digits(sao[0], sao[1], 8, 64).size() >= 5;
   std::vector<int> shifts = active_digits(ao[0], ao[1], 8, 64);
@@ -661,6 +673,9 @@ void edge_sort(Ctx& c, const int32_t* u, const int32_t* v, const double* w, int6
                                                          shifts, bufK, bufP, Sort1FirstLoader{w, u, v, code}, em,
                                                          local ? -1 : ready, S1_ALIGN, S1N_MINB);
   }
+  // a table a later stage needs zeroed: cleared on the aux stream while the
+  // (shared-memory-bound) radix passes just launched run
+  if (zero_ptr) prezero(c, 0, zero_ptr, zero_bytes);
   // whichever kernel wrote the final output (radix pass, identity pass or the
   // shared-memory finish) counted the slices
   c.slices_counted = em.scount != nullptr;
@@ -729,6 +744,10 @@ void mi_buckets(Ctx& c, Src src, int64_t m, int64_t nv, Recs mid, Recs fin, MiAp
   c.begin(KK_MI_SPLIT_A);
   kA<<<c.persistent_grid(m, SA::T, BKA_PER_SM), BKA_BLOCK, SA::bytes(), c.s>>>(src, m, gshift, coarse_cur, mid);
   c.launched();
+  if (c.pz_next.p) {  // the next view's table, zeroed while this (shared-memory-bound) pass runs
+    prezero(c, 1, const_cast<void*>(c.pz_next.p), c.pz_next.bytes);
+    c.pz_next = Ctx::Prezero{};
+  }
   if (sliced) {
     c.paths.mi_sliced_used = 1;
     c.begin(KK_MI_APPLY);
@@ -833,13 +852,14 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
   c.zero(w.sel_status, 8 * (cdiv(n / 16 + 1, LS_TILE) + 2));
   // maxIncident + V1 of the input view: 2n records generated from euv0
   c.zero(w.cnt2, 4 * (n / 16 + 2));
+  // view 1's table (<= n/2 + 1 vertices; ~0.26 n on random trees) zeroed
+  // during view 0's pass A when view 1 will take the sliced apply
+  if (mi_sliced(c, n / 4) && n / 4 > (1 << 20)) c.pz_next = Ctx::Prezero{w.mi64[1], 8 * (size_t)(n / 2 + 2)};
   mi_buckets(c, EdgeRecSrc{w.euv0}, 2 * n, nv, recs_at(w.R, 2 * n), recs_at(w.R + 24 * n, 2 * n),
              MiApplyOut{w.mi64_0, vertex_parent, nullptr, w.cnt2}, c.slices_counted);
+  c.pz_next = Ctx::Prezero{};
   c.slices_counted = false;
-  // view 1's table (<= n/2 + 1 vertices) zeroed on the aux stream during view 0,
-  // when view 1 will take the sliced apply (~0.26 n vertices on random trees)
-  join_aux(c);
-  if (mi_sliced(c, n / 4) && n / 4 > (1 << 20)) prezero(c, w.mi64[1], 8 * (size_t)(n / 2 + 2));
+
   c.paths.mi_bucketed |= 1;
   if (c.io) c.copy_out(2, c.io->h_vp, vertex_parent, 4 * (size_t)nv);
   bool v1_done = true;
@@ -1180,6 +1200,7 @@ static int build_impl(const int32_t* u, const int32_t* v, const double* w, int64
     init_ctx(c, n, nv, ws, stream, st);
     c.io = io;
     if (inputs_ready) DMST_CUDA(cudaStreamWaitEvent(c.s, inputs_ready, 0));
+    mark_aux(c);
     Sort1FinalEmitter em{orig_of, heights, c.w.euv0, nullptr, nullptr};
     int p1 = 0;
     const bool sl = mi_sliced(c, nv);  // view 0's table, zeroed during the edge sort's passes

@@ -9,6 +9,8 @@ python tools/ncu_traffic.py gpurun_out/ncu_traffic.ncu-rep config4 --out gpurun_
 bash tools/ncu_all.sh trafficu random 128000000
 python tools/ncu_traffic.py gpurun_out/ncu_trafficu.ncu-rep config4u --out gpurun_out/ncu_traffic.json --csv gpurun_out/ncu_kinds_u_$TAG.csv > gpurun_out/ncu_kinds_u_$TAG.txt
 cp gpurun_out/ncu_traffic.json profiles/ncu_traffic.json
+# per-launch raw metrics kept (the kind map can be re-applied without a re-capture)
+for r in ncu_traffic ncu_trafficu; do ncu -i gpurun_out/$r.ncu-rep --page raw --csv --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum > gpurun_out/${r}_raw_$TAG.csv; done
 rm -f gpurun_out/*.ncu-rep
 # headline bench line (CPU baseline: the unmodified reference at full size)
 timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err

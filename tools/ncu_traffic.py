@@ -30,7 +30,10 @@ def kind(name: str) -> str:
         ("k_split<0, EdgeRecSrc", "mi_split_a"), ("k_split<1, AosRecSrc<3>", "mi_split_b"),
         ("LinkSortedSrc", "link_split"), ("k_split<1, AosRecSrc<2>", "link_split"), ("k_link_cursors", "link_split"),
         ("k_link_apply", "link_apply"), ("k_link(", "link_apply"),
-        ("k_mi_apply_smem", "mi_apply"), ("k_v1", "v1"), ("k_leafscan", "leafscan"), ("k_v2", "v2"),
+        # sliced maxIncident (views 0/1): k_mi_atomic + k_v1 are bench.py's mi_apply; ncu cannot
+        # tell a sliced view's k_v1 from a direct view's, so all k_v1 launches stay "v1" here
+        ("k_mi_apply_smem", "mi_apply"), ("k_mi_atomic", "mi_apply"), ("k_slice_scan", "mi_hist"),
+        ("k_link_scatter", "link_apply"), ("k_ls_", "leafscan"), ("k_v1", "v1"), ("k_leafscan", "leafscan"), ("k_v2", "v2"),
         ("k_jump", "jump"), ("k_select_edges", "select_edges"), ("k_walk", "walk"), ("k_tail", "tail"),
         ("k_key_sample", "sort1_hist"),
         # outside the timed build: bench.py's validation leg, statistics
@@ -46,8 +49,11 @@ def kind(name: str) -> str:
 def main():
     rep, workload = sys.argv[1], sys.argv[2]
     out = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else None
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", METS],
-                         capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):  # a saved `ncu -i X --page raw --csv --metrics METS` export
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", METS],
+                             capture_output=True, text=True).stdout
     r = list(csv.reader(raw.splitlines()))
     h, units = r[0], r[1]
     ix = {k: i for i, k in enumerate(h)}

@@ -89,7 +89,8 @@ def kernel_bytes(stats, n: int, nv: int) -> dict[str, float]:
         "mi_apply": 12.0 * mb + 12.0 * vb,                      # read records; write mi64 8 + parent 4
         "v1": 12.0 * sum(views_v[k] for k in direct),
         "leafscan": 1.0 * sum(views_n),                         # 2-bit counts in, prefixes out (per 16 edges)
-        "v2": 12.0 * sum(views_v[:L]),                          # mi64 8 + vertex map 4 (chase hops not credited)
+        "v2": 12.0 * sum(views_v[1 if info.get("v0_chase") else 0:L]),  # mi64 8 + vertex map 4 (chase hops
+                                                                # not credited); view 0 chased in the select: no V2
         "jump": 0.0,
         "select_edges": 9.0 * sum(views_n[:L]) + 4.0 * n + 20.0 * alpha
         + 16.0 * sum(views_n[k] for k in direct),               # euv + ret; x1; alpha: 2 gathers + next view;

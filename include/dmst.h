@@ -100,6 +100,11 @@ typedef struct dmst_stats {
   int32_t mi_sliced;        /* 1 = some view's maxIncident took the sliced L2-atomic apply */
   uint64_t mi_bucketed;     /* bit k: view k's maxIncident was bucketed */
   uint64_t mi_direct;       /* bit k: view k's maxIncident took direct atomics */
+  int32_t v0_select;        /* in: view 0's supervertex labels: 1 = V2 writes the vertex map, the
+                               select gathers from it; 2 = the select chases maxIncident from the
+                               endpoints it needs (no V2; edges with chases over 16 steps are
+                               finished from a V2 vertex map); 0 = by the view's kind counts */
+  int32_t v0_chase;         /* out: 1 = view 0's select chased, 2 = and deferred some edges */
 } dmst_stats;
 
 /* Workspace size for a tree with n_edges edges. */

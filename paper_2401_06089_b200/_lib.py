@@ -69,10 +69,13 @@ class DmstStats(ctypes.Structure):
         ("mi_sliced", ctypes.c_int32),
         ("mi_bucketed", ctypes.c_uint64),
         ("mi_direct", ctypes.c_uint64),
+        ("v0_select", ctypes.c_int32),
+        ("v0_chase", ctypes.c_int32),
     ]
 
     # code-path overrides accepted by DendrogramBuilder.build(paths=...)
-    PATH_OPTIONS = ("tail_edges", "direct_mi_bytes", "sort1_mode", "sort2_geometry", "mi_apply_mode")
+    PATH_OPTIONS = ("tail_edges", "direct_mi_bytes", "sort1_mode", "sort2_geometry", "mi_apply_mode",
+                    "v0_select")
 
     def set_paths(self, paths: dict | None) -> None:
         for k, v in (paths or {}).items():
@@ -87,6 +90,7 @@ class DmstStats(ctypes.Structure):
                 "sort1_compacted": bool(self.sort1_compacted),
                 "sort1_local": {0: None, 1: "smem", 2: "fallback"}[int(self.sort1_local)],
                 "mi_sliced": bool(self.mi_sliced),
+                "v0_chase": {0: None, 1: "chase", 2: "chase+fix"}[int(self.v0_chase)],
                 "sort2_passes": int(self.sort2_passes),
                 "sort2_geometry": SORT2_GEOMETRIES[int(self.sort2_geometry_used)],
                 "tail_level": int(self.tail_level),

@@ -129,7 +129,8 @@ constexpr int SM_HIST1 = 0, SM_GBASE1 = SM_HIST1 + 8 * kRadix, SM_HIST2 = SM_GBA
               SM_GBASE2 = SM_HIST2 + 4 * kRadix, SM_VHIST = SM_GBASE2 + 4 * kRadix,
               SM_VBASE = SM_VHIST + kRadix, SM_TILECTR = SM_VBASE + kRadix, SM_MISC = SM_TILECTR + 64;
 constexpr int MISC_NEGZERO = 0, MISC_ACTIVE0 = 1, MISC_ACTIVE1 = 2, MISC_ACTIVE2 = 3, MISC_COUNTS = 4 /*2*/,
-              MISC_NONRUL = 6, MISC_LSCTR = 13, MISC_LOCALOVF = 16, MISC_SORT1D0 = 17;
+              MISC_NONRUL = 6, MISC_LSCTR = 13, MISC_LOCALOVF = 16, MISC_SORT1D0 = 17,
+              MISC_DEFER = 20;
 
 Workspace carve(int64_t n, int64_t nv, char* base) {
   Workspace w{};
@@ -245,7 +246,9 @@ struct Paths {
   int sort1_mode = 0;
   int sort2_geometry = 0;
   int mi_apply_mode = 0;  // 0 / 1: shared-memory apply per fine bucket; 2: slices + L2 atomics
+  int v0_select = 0;      // 0: by the view's kind counts; 1: V2 + vertex map; 2: chase in the select
   // out
+  int v0_chase = 0;       // 1 = view 0's select chased maxIncident (no V2), 2 = and deferred edges
   int sort1_narrow = 0, sort1_compacted = 0, sort2_geometry_used = 0, tail_level = -1;
   int sort1_local = 0;  // 1 = wide keys finished in shared memory, 2 = tried, fell back to full LSD
   int mi_sliced_used = 0;
@@ -918,16 +921,23 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     // view 0: plain vertex map; views >= 1: packed walk table (stride 2)
     int32_t* vm = level == 0 ? w.vm_all : (int32_t*)(w.lvl_all + lt.soff[level]);
     const int vs = level == 0 ? 1 : 2;
-    c.begin(KK_V2);
-    k_v2<<<grid_for(nv_k, EW_BLOCK), EW_BLOCK, 0, c.s>>>(nv_k, mi_k, w.lw, vm,
-                                                         level == 0 ? nullptr : w.smi_all + lt.soff[level],
-                                                         lists[0], lcnt[0], lists[3], lcnt[3]);
-    c.launched();
+    auto launch_v2 = [&] {
+      c.begin(KK_V2);
+      k_v2<<<grid_for(nv_k, EW_BLOCK), EW_BLOCK, 0, c.s>>>(nv_k, mi_k, w.lw, vm,
+                                                           level == 0 ? nullptr : w.smi_all + lt.soff[level],
+                                                           lists[0], lcnt[0], lists[3], lcnt[3]);
+      c.launched();
+    };
+    // view 0's vertex map is read only by its select: the select may find the
+    // labels itself by chasing maxIncident from the endpoints it needs
+    // (decided below from the view's kind counts), so V2 waits for them
+    const bool chase_cand = level == 0 && c.paths.v0_select != 1;
+    if (!chase_cand) launch_v2();
     uint32_t mw[6];  // misc words 1..6: ACTIVE0, ACTIVE1, ACTIVE2, COUNTS[2], NONRUL
     static_assert(MISC_ACTIVE0 == 1 && MISC_COUNTS == 4 && MISC_NONRUL == 6, "readback layout");
     c.to_host(mw, misc + 1, sizeof(mw));
     c.sync();
-    const uint32_t counts[4] = {mw[3], mw[4], mw[0], mw[5]};
+    uint32_t counts[4] = {mw[3], mw[4], mw[0], mw[5]};
     const int64_t n_leaf = counts[0], n_chain = counts[1];
     const int64_t n_alpha = n_k - n_leaf - n_chain;
     if (st) {
@@ -945,27 +955,48 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
       }
       break;
     }
+    // Chasing in the select reads ~(chain + 2 alpha) (1 + chase) sectors
+    // against V2's ~0.64 per vertex + one per needed endpoint (random trees:
+    // 1.36 vs 1.64 per edge + V2's stream; ncu at 128M: 23.3 vs 24.9 GB of
+    // DRAM traffic) but its dependent chase steps run at a lower rate:
+    // measured 21.13-21.18 vs 21.21-21.30 ms at 128M, 100.8-101.2 vs 100.5 ms
+    // on config 5 (8 trees of 8M at once).  So: only views of >= 64M edges,
+    // and not when alpha edges are many or chains long (a chain-dominated
+    // view: one long sorted chain chases O(n) steps per endpoint)
+    const bool chase = chase_cand && (c.paths.v0_select == 2 || (n_k >= (int64_t(64) << 20) && 4 * n_chain <= 3 * n_k &&
+                                                                 10 * n_alpha <= 3 * n_k));
+    auto v2_sync = [&] {  // V2 after the counts were read: read its ruler / non-ruler counts
+      launch_v2();
+      c.to_host(mw, misc + 1, sizeof(mw));
+      c.sync();
+      counts[2] = mw[0];
+      counts[3] = mw[5];
+    };
+    if (chase_cand && !chase) v2_sync();
     // pointer jumping: rulers first (a chain of rulers ~1/32 as long as the
     // in-tree), then the non-rulers, whose targets are then resolved rulers
-    for (int phase = 0; phase < 2; ++phase) {
-      uint32_t pending = counts[phase == 0 ? 2 : 3];
-      const int32_t* in = lists[phase == 0 ? 0 : 3];
-      const uint32_t* in_cnt = lcnt[phase == 0 ? 0 : 3];
-      int a = 1;
-      while (pending) {
-        c.zero(lcnt[a], 4);
-        c.begin(KK_JUMP);
-        k_jump<<<c.persistent_grid(pending, EW_BLOCK, 16), EW_BLOCK, 0, c.s>>>(in, in_cnt, lists[a], lcnt[a], vm,
-                                                                               vs);
-        c.launched();
-        ++jump_rounds;
-        c.to_host(&pending, lcnt[a], 4);
-        c.sync();
-        in = lists[a];
-        in_cnt = lcnt[a];
-        a = a == 1 ? 2 : 1;
+    auto run_jumps = [&] {
+      for (int phase = 0; phase < 2; ++phase) {
+        uint32_t pending = counts[phase == 0 ? 2 : 3];
+        const int32_t* in = lists[phase == 0 ? 0 : 3];
+        const uint32_t* in_cnt = lcnt[phase == 0 ? 0 : 3];
+        int a = 1;
+        while (pending) {
+          c.zero(lcnt[a], 4);
+          c.begin(KK_JUMP);
+          k_jump<<<c.persistent_grid(pending, EW_BLOCK, 16), EW_BLOCK, 0, c.s>>>(in, in_cnt, lists[a], lcnt[a], vm,
+                                                                                 vs);
+          c.launched();
+          ++jump_rounds;
+          c.to_host(&pending, lcnt[a], 4);
+          c.sync();
+          in = lists[a];
+          in_cnt = lcnt[a];
+          a = a == 1 ? 2 : 1;
+        }
       }
-    }
+    };
+    if (!chase) run_jumps();
     // retire + compact alpha edges into view level+1
     const int64_t nv_next = n_leaf, n_next = n_alpha;
     // (a view without edges has an all-zero maxIncident: nothing to bucket)
@@ -1002,9 +1033,32 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     es.scount = count_next ? w.fine : nullptr;
     es.sshift = kSliceBits;
     if (count_next) c.zero(w.fine, 4 * 256);
-    c.begin(KK_SELECT_EDGES);
-    k_select_edges<<<c.persistent_grid(n_k, SEL_BLOCK * SEL_U, 8), SEL_BLOCK, 0, c.s>>>(n_k, es);
-    c.launched();
+    if (!chase) {
+      c.begin(KK_SELECT_EDGES);
+      k_select_edges<false><<<c.persistent_grid(n_k, SEL_BLOCK * SEL_U, 8), SEL_BLOCK, 0, c.s>>>(n_k, es);
+      c.launched();
+    } else {
+      es.mi0 = mi_k;
+      es.lw = w.lw;
+      es.defer = lists[3] + nv_k;  // R[16 nv, 20 nv): after the four jump lists
+      es.defer_cnt = misc + MISC_DEFER;
+      c.zero(es.defer_cnt, 4);
+      c.begin(KK_SELECT_EDGES);
+      k_select_edges<true><<<c.persistent_grid(n_k, SEL_BLOCK * DMST_SEL_CHASE_U, 8), SEL_BLOCK, 0, c.s>>>(n_k, es);
+      c.launched();
+      uint32_t n_defer = 0;
+      c.to_host(&n_defer, es.defer_cnt, 4);
+      c.sync();
+      c.paths.v0_chase = n_defer ? 2 : 1;
+      if (n_defer) {  // long chases: V2 + pointer jumping, then the deferred edges from the vertex map
+        v2_sync();
+        run_jumps();
+        c.begin(KK_SELECT_EDGES);
+        k_select_fix<<<c.persistent_grid(n_defer, SEL_BLOCK, 8), SEL_BLOCK, 0, c.s>>>(es.defer, es.defer_cnt, es);
+        c.launched();
+        c.zero(misc + 1, 4 * 15);  // V2 / jumps used the counters the select had cleared
+      }
+    }
     v1_done = false;
     if (!direct && n_next > 0) {
       const int64_t m = 2 * n_next;
@@ -1153,8 +1207,9 @@ void init_ctx(Ctx& c, int64_t n, int64_t nv, void* ws, void* stream, dmst_stats*
   if (st) {
     const int32_t prof = st->profile, wc = st->want_chains;
     const int64_t te = st->tail_edges, dm = st->direct_mi_bytes;
-    const int32_t s1 = st->sort1_mode, s2 = st->sort2_geometry, ma = st->mi_apply_mode;
+    const int32_t s1 = st->sort1_mode, s2 = st->sort2_geometry, ma = st->mi_apply_mode, vsel = st->v0_select;
     if (ma < 0 || ma > 2) invalid("mi_apply_mode must be 0, 1 or 2");
+    if (vsel < 0 || vsel > 2) invalid("v0_select must be 0, 1 or 2");
     if (s1 < 0 || s1 > 7) invalid("sort1_mode must be in [0, 7]");
     if (s2 < 0 || s2 > 2) invalid("sort2_geometry must be 0, 1 or 2");
     if (te < -1 || dm < -1) invalid("tail_edges / direct_mi_bytes must be >= -1");
@@ -1166,12 +1221,14 @@ void init_ctx(Ctx& c, int64_t n, int64_t nv, void* ws, void* stream, dmst_stats*
     st->sort1_mode = s1;
     st->sort2_geometry = s2;
     st->mi_apply_mode = ma;
+    st->v0_select = vsel;
     c.profile = prof != 0;
     if (te) c.paths.tail_edges = te;  // -1: n_k <= -1 never holds
     if (dm) c.paths.direct_mi_bytes = dm;
     c.paths.sort1_mode = s1;
     c.paths.sort2_geometry = s2;
     c.paths.mi_apply_mode = ma;
+    c.paths.v0_select = vsel;
   }
 }
 
@@ -1185,6 +1242,7 @@ void report_paths(const Ctx& c, dmst_stats* st) {
   st->tail_level = c.paths.tail_level;
   st->mi_bucketed = c.paths.mi_bucketed;
   st->mi_direct = c.paths.mi_direct;
+  st->v0_chase = c.paths.v0_chase;
 }
 
 static int build_impl(const int32_t* u, const int32_t* v, const double* w, int64_t n, int64_t nv,

@@ -566,9 +566,75 @@ struct EdgeSel {
   int64_t n_status;
   uint32_t* __restrict__ scount;     // next view sliced: its endpoints counted per slice (or null)
   uint32_t sshift;
+  // CHASE select (view 0): labels by chasing maxIncident instead of a vertex map
+  const unsigned long long* __restrict__ mi0;
+  const uint2* __restrict__ lw;      // (leaf bitmap, leaf prefix) per 32 edges
+  int32_t* __restrict__ defer;       // edges whose chase ran over CHASE_FUSED steps
+  uint32_t* __restrict__ defer_cnt;
 };
 
 constexpr int SEL_U = 4;  // edges per thread per iteration (gathers in flight together)
+constexpr int CHASE_FUSED = 16;
+#ifndef DMST_SEL_CHASE_U
+#define DMST_SEL_CHASE_U 2
+#endif  // view-0 select: chase steps before an edge is deferred
+
+// Per-edge inputs of the select: 2-bit count -> kind, leaf label, alpha slot,
+// global rank, endpoints (only when a label must be looked up).
+struct SelEdge {
+  bool in, alpha, need;
+  int32_t lab, g;
+  uint32_t pos;
+  int2 e;
+};
+__device__ __forceinline__ SelEdge sel_load(const EdgeSel& es, int64_t j, int64_t n) {
+  SelEdge r;
+  r.in = j < n;
+  const uint2 w = r.in ? es.kw[j >> 4] : make_uint2(0, 0);
+  const uint32_t sh = (uint32_t)(j & 15) * 2;
+  const uint32_t c = (w.x >> sh) & 3u;
+  r.alpha = r.in && c == 0u;
+  r.lab = c == 2u ? (int32_t)leaf_label(w, (uint32_t)j) : -1;
+  r.pos = r.alpha ? es.apre[j >> 4] + __popc(alpha_bits(w.x, 0, 16) & ((1u << sh) - 1u)) : 0u;
+  r.g = r.in ? (es.grank ? __ldcs(es.grank + j) : (int32_t)j) : 0;
+  r.need = r.alpha || (r.in && es.x1 != nullptr && r.lab < 0);
+  r.e = r.need ? __ldcs(es.euv + j) : make_int2(0, 0);
+  return r;
+}
+
+// Per-edge outputs: the view-1 supervertex (view 0), retirement of a
+// non-alpha edge, or the alpha edge's slot in the next view (+ its slice
+// counts / direct maxIncident).
+__device__ __forceinline__ void sel_emit(const EdgeSel& es, int64_t j, const SelEdge& d, int32_t a, int32_t b,
+                                         uint32_t* shist) {
+  // a leaf edge's component is labelled by the edge itself; a chain or
+  // alpha edge's by its first endpoint
+  if (es.x1) __stcs(es.x1 + j, a);
+  if (!d.alpha) {
+    es.ret[d.g] = es.level;
+  } else {
+    __stcs(es.euv_next + d.pos, make_int2(a, b));
+    __stcs(es.grank_next + d.pos, d.g);
+    if (es.scount) {
+      atomicAdd(&shist[(uint32_t)a >> es.sshift], 1u);
+      atomicAdd(&shist[(uint32_t)b >> es.sshift], 1u);
+    }
+    if (es.mi64_next) {
+      atomicMax(es.mi64_next + a, pack_mi(d.pos + 1u, (uint32_t)b));
+      atomicMax(es.mi64_next + b, pack_mi(d.pos + 1u, (uint32_t)a));
+    }
+  }
+}
+
+// CHASE (view 0 only): no vertex map.  A label is found by chasing view 0's
+// maxIncident pointers from the endpoint to its component's leaf edge, as
+// k_v2 would (contraction.py:82-93), but only for the endpoints the select
+// needs (the first endpoint of chain edges, both ends of alpha edges: ~1.36
+// random reads per edge on random trees instead of V2's 0.64 per vertex +
+// the select's 1.0 per edge + V2's streaming pass).  An edge with a chase
+// longer than CHASE_FUSED steps is deferred (es.defer) and finished by
+// k_select_fix after V2 + pointer jumping.
+template <bool CHASE, int U = (CHASE ? DMST_SEL_CHASE_U : SEL_U)>
 __global__ void __launch_bounds__(SEL_BLOCK) k_select_edges(int64_t n, EdgeSel es) {
   __shared__ uint32_t shist[256];  // per-slice endpoint counts of the next view (es.scount)
   if (es.scount) {
@@ -580,55 +646,112 @@ __global__ void __launch_bounds__(SEL_BLOCK) k_select_edges(int64_t n, EdgeSel e
     for (int64_t i = g; i < es.n_status; i += (int64_t)gridDim.x * SEL_BLOCK) es.reset_status[i] = 0u;
     if (g < 15) es.reset_misc[g] = 0u;
   }
-  const int64_t stride = (int64_t)gridDim.x * SEL_BLOCK * SEL_U;
-  for (int64_t b0 = (int64_t)blockIdx.x * SEL_BLOCK * SEL_U + threadIdx.x; b0 < n; b0 += stride) {
-    bool alpha[SEL_U], in[SEL_U], need[SEL_U];
-    int32_t lab[SEL_U], g[SEL_U];
-    uint32_t pos[SEL_U];
-    int2 e[SEL_U];
+  const uint64_t pol = l2_keep_policy();
+  const int64_t stride = (int64_t)gridDim.x * SEL_BLOCK * U;
+  for (int64_t b0 = (int64_t)blockIdx.x * SEL_BLOCK * U + threadIdx.x; b0 < n; b0 += stride) {
+    SelEdge d[U];
 #pragma unroll
-    for (int q = 0; q < SEL_U; ++q) {
+    for (int q = 0; q < U; ++q) {
       const int64_t j = b0 + (int64_t)q * SEL_BLOCK;
-      in[q] = j < n;
-      const uint2 w = in[q] ? es.kw[j >> 4] : make_uint2(0, 0);
-      const uint32_t sh = (uint32_t)(j & 15) * 2;
-      const uint32_t c = (w.x >> sh) & 3u;
-      alpha[q] = in[q] && c == 0u;
-      lab[q] = c == 2u ? (int32_t)leaf_label(w, (uint32_t)j) : -1;
-      pos[q] = alpha[q] ? es.apre[j >> 4] + __popc(alpha_bits(w.x, 0, 16) & ((1u << sh) - 1u)) : 0u;
-      g[q] = in[q] ? (es.grank ? __ldcs(es.grank + j) : (int32_t)j) : 0;
-      need[q] = alpha[q] || (in[q] && es.x1 != nullptr && lab[q] < 0);
-      e[q] = need[q] ? __ldcs(es.euv + j) : make_int2(0, 0);
-      if (in[q] && (j & 15) == 0) es.cnt2[j >> 4] = 0u;
+      d[q] = sel_load(es, j, n);
+      if (d[q].in && (j & 15) == 0) es.cnt2[j >> 4] = 0u;
     }
-    int32_t a[SEL_U], bb[SEL_U];
+    int32_t a[U], bb[U];
+    if constexpr (!CHASE) {
 #pragma unroll
-    for (int q = 0; q < SEL_U; ++q) {
-      a[q] = need[q] ? es.vm[(int64_t)e[q].x * es.vs] : lab[q];
-      bb[q] = alpha[q] ? es.vm[(int64_t)e[q].y * es.vs] : 0;
-    }
+      for (int q = 0; q < U; ++q) {
+        a[q] = d[q].need ? es.vm[(int64_t)d[q].e.x * es.vs] : d[q].lab;
+        bb[q] = d[q].alpha ? es.vm[(int64_t)d[q].e.y * es.vs] : 0;
+      }
+    } else {
+      unsigned long long ma[U], mb[U];
+      bool pa[U], pb[U];
 #pragma unroll
-    for (int q = 0; q < SEL_U; ++q) {
-      if (!in[q]) continue;
-      const int64_t j = b0 + (int64_t)q * SEL_BLOCK;
-      // a leaf edge's component is labelled by the edge itself; a chain or
-      // alpha edge's by its first endpoint
-      if (es.x1) __stcs(es.x1 + j, a[q]);
-      if (!alpha[q]) {
-        es.ret[g[q]] = es.level;
-      } else {
-        __stcs(es.euv_next + pos[q], make_int2(a[q], bb[q]));
-        __stcs(es.grank_next + pos[q], g[q]);
-        if (es.scount) {
-          atomicAdd(&shist[(uint32_t)a[q] >> es.sshift], 1u);
-          atomicAdd(&shist[(uint32_t)bb[q] >> es.sshift], 1u);
+      for (int q = 0; q < U; ++q) {
+        pa[q] = d[q].need;
+        pb[q] = d[q].alpha;
+        ma[q] = pa[q] ? __ldcs(es.mi0 + d[q].e.x) : 0ull;
+        mb[q] = pb[q] ? __ldcs(es.mi0 + d[q].e.y) : 0ull;
+        a[q] = d[q].lab;
+        bb[q] = 0;
+      }
+      for (int s = 0;; ++s) {
+        uint2 la[U], lb[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {  // kind tests: the leaf bitmap is L2-resident
+          if (pa[q]) la[q] = ld_keep2(es.lw + (((uint32_t)(ma[q] >> 32) - 1u) >> 5), pol);
+          if (pb[q]) lb[q] = ld_keep2(es.lw + (((uint32_t)(mb[q] >> 32) - 1u) >> 5), pol);
         }
-        if (es.mi64_next) {
-          atomicMax(es.mi64_next + a[q], pack_mi(pos[q] + 1u, (uint32_t)bb[q]));
-          atomicMax(es.mi64_next + bb[q], pack_mi(pos[q] + 1u, (uint32_t)a[q]));
+        bool more = false;
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          if (pa[q]) {
+            const uint32_t jj = (uint32_t)(ma[q] >> 32) - 1u;
+            if ((la[q].x >> (jj & 31)) & 1u) {
+              a[q] = (int32_t)(la[q].y + __popc(la[q].x & ((1u << (jj & 31)) - 1u)));
+              pa[q] = false;
+            } else if (s == CHASE_FUSED) {
+              a[q] = -1;
+              pa[q] = false;
+            } else {
+              more = true;
+            }
+          }
+          if (pb[q]) {
+            const uint32_t jj = (uint32_t)(mb[q] >> 32) - 1u;
+            if ((lb[q].x >> (jj & 31)) & 1u) {
+              bb[q] = (int32_t)(lb[q].y + __popc(lb[q].x & ((1u << (jj & 31)) - 1u)));
+              pb[q] = false;
+            } else if (s == CHASE_FUSED) {
+              bb[q] = -1;
+              pb[q] = false;
+            } else {
+              more = true;
+            }
+          }
+        }
+        if (!more) break;
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+          if (pa[q]) ma[q] = __ldcs(es.mi0 + (uint32_t)ma[q]);
+          if (pb[q]) mb[q] = __ldcs(es.mi0 + (uint32_t)mb[q]);
         }
       }
     }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      if (!d[q].in) continue;
+      const int64_t j = b0 + (int64_t)q * SEL_BLOCK;
+      if (CHASE && (a[q] < 0 || bb[q] < 0)) {  // chase too long: finished by k_select_fix
+        es.defer[atomicAdd(es.defer_cnt, 1u)] = (int32_t)j;
+        continue;
+      }
+      sel_emit(es, j, d[q], a[q], bb[q], shist);
+    }
+  }
+  if (es.scount) {
+    __syncthreads();
+    for (int b = threadIdx.x; b < 256; b += SEL_BLOCK)
+      if (shist[b]) atomicAdd(es.scount + b, shist[b]);
+  }
+}
+
+// The deferred edges of a CHASE select, once V2 + pointer jumping have
+// written view 0's vertex map (es.vm).
+__global__ void __launch_bounds__(SEL_BLOCK) k_select_fix(const int32_t* __restrict__ list,
+                                                          const uint32_t* __restrict__ cnt, EdgeSel es) {
+  __shared__ uint32_t shist[256];
+  if (es.scount) {
+    for (int b = threadIdx.x; b < 256; b += SEL_BLOCK) shist[b] = 0;
+    __syncthreads();
+  }
+  const uint32_t m = *cnt;
+  for (int64_t t = (int64_t)blockIdx.x * SEL_BLOCK + threadIdx.x; t < m; t += (int64_t)gridDim.x * SEL_BLOCK) {
+    const int64_t j = list[t];
+    const SelEdge d = sel_load(es, j, INT64_MAX);
+    const int32_t a = d.need ? es.vm[(int64_t)d.e.x * es.vs] : d.lab;
+    const int32_t b = d.alpha ? es.vm[(int64_t)d.e.y * es.vs] : 0;
+    sel_emit(es, j, d, a, b, shist);
   }
   if (es.scount) {
     __syncthreads();

@@ -48,6 +48,10 @@ PATHS = {
     "sliced": {"mi_apply_mode": 2, "direct_mi_bytes": -1, "tail_edges": -1},
     # the shared-memory apply forced
     "smem_apply": {"mi_apply_mode": 1},
+    # view 0's labels: always V2 + vertex map / always chased in the select (long
+    # chases deferred to k_select_fix after V2 + pointer jumping); no tail
+    "v0_vertex_map": {"v0_select": 1},
+    "v0_chase": {"v0_select": 2, "tail_edges": -1},
 }
 
 SEEN_KINDS: dict[str, int] = {}   # kernel kind -> launches inside checked builds
@@ -116,6 +120,10 @@ def _assert_path_taken(res, paths):
         assert info["mi_sliced"]
     if p.get("mi_apply_mode") == 1:
         assert not info["mi_sliced"]
+    if p.get("v0_select") == 1:
+        assert info["v0_chase"] is None
+    if p.get("v0_select") == 2:
+        assert info["v0_chase"] in ("chase", "chase+fix")
     if p.get("sort2_geometry") and info["sort2_passes"]:
         from paper_2401_06089_b200._lib import SORT2_GEOMETRIES
         assert info["sort2_geometry"] == SORT2_GEOMETRIES[p["sort2_geometry"]]
@@ -162,7 +170,7 @@ def test_stress_shapes_all_paths(builder, paths, kind):
     _assert_path_taken(res, paths)
 
 
-@pytest.mark.parametrize("paths", ["no_tail", "bucketed", "late_tail"])
+@pytest.mark.parametrize("paths", ["no_tail", "bucketed", "late_tail", "v0_chase"])
 def test_deep_in_trees_all_paths(builder, paths):
     # reversed path (in-trees towards higher ids: pointer jumping on every view)
     # and relabelled vertex ids (random-access chases) through the host loop
@@ -228,12 +236,27 @@ def test_wide_key_local_sort(builder, kind, n):
         assert info["sort1_local"] == "smem"
 
 
+@pytest.mark.parametrize("shape", ["path", "caterpillar", "random"])
+def test_v0_chase_defers_long_chases(builder, shape):
+    # single sorted chains chase O(n) steps from every endpoint: forced into the
+    # chasing select, every such edge is deferred and finished from V2's vertex
+    # map; random trees (max chase ~7) finish in the select itself.
+    nv, u, v, w = synth.GENERATORS[shape](300_000, seed=3)
+    exp = _oracle_full(nv, u, v, w)
+    forced = _check(builder, nv, u, v, w, exp, "v0_chase")
+    default = _check(builder, nv, u, v, w, exp, "default")
+    assert forced.stats.path_info()["v0_chase"] == ("chase" if shape == "random" else "chase+fix")
+    assert default.stats.path_info()["v0_chase"] is None  # the default chases only views of >= 64M edges
+
+
 def test_rejects_bad_path_options(builder):
     nv, u, v, w = synth.random_attach(100, seed=1)
     with pytest.raises(ValueError):
         builder.build(nv, u, v, w, paths={"sort2_geometry": 3})
     with pytest.raises(ValueError):
         builder.build(nv, u, v, w, paths={"sort1_mode": 8})
+    with pytest.raises(ValueError):
+        builder.build(nv, u, v, w, paths={"v0_select": 3})
     with pytest.raises(ValueError):
         builder.build(nv, u, v, w, paths={"no_such_option": 1})
 

@@ -141,18 +141,18 @@ __global__ void __launch_bounds__(G::LF_BLOCK, 1024 / G::LF_BLOCK) k_local_final
   const int sbits = span ? 64 - __clzll((long long)span) : 0;
   const int s0 = max(sbits - 32, 0);                          // (key - kfirst) >> s0 fits 32 bits
   const int bsh = max(min(sbits, 32) - kLocalBucketBits, 0);  // then >> bsh: the bucket
+  // (an item's window position wbase + 32 q and its bucket are recomputed
+  // where needed instead of held in registers: 64 registers at 2 CTAs / SM)
   uint64_t k[LF_ITEMS];
-  uint32_t x[LF_ITEMS], bk[LF_ITEMS];
+  uint32_t x[LF_ITEMS];
+  auto bucket_of = [&](uint64_t key) { return (uint32_t)((key - kfirst) >> s0) >> bsh; };
 #pragma unroll
   for (int q = 0; q < LF_ITEMS; ++q) {
     const int idx = wbase + q * 32;
     k[q] = ~0ull;
-    x[q] = (uint32_t)idx;
-    bk[q] = 0;
     if (q < ipw && idx < W) {
       k[q] = s.okey[woff + idx];
-      bk[q] = (uint32_t)((k[q] - kfirst) >> s0) >> bsh;
-      atomicAdd(&s.u.cs.cnt[bk[q]], 1u);
+      atomicAdd(&s.u.cs.cnt[bucket_of(k[q])], 1u);
     }
   }
   __syncthreads();
@@ -181,9 +181,9 @@ __global__ void __launch_bounds__(G::LF_BLOCK, 1024 / G::LF_BLOCK) k_local_final
 #pragma unroll
     for (int q = 0; q < LF_ITEMS; ++q) {
       if (q < ipw && wbase + q * 32 < W) {
-        const uint32_t p = atomicAdd(&s.u.cs.cur[bk[q]], 1u);
+        const uint32_t p = atomicAdd(&s.u.cs.cur[bucket_of(k[q])], 1u);
         s.okey[p] = k[q];
-        s.oidx[p] = (uint16_t)x[q];
+        s.oidx[p] = (uint16_t)(wbase + q * 32);
       }
     }
     __syncthreads();
@@ -191,12 +191,13 @@ __global__ void __launch_bounds__(G::LF_BLOCK, 1024 / G::LF_BLOCK) k_local_final
 #pragma unroll
     for (int q = 0; q < LF_ITEMS; ++q) {
       if (q < ipw && wbase + q * 32 < W) {
-        const int b0 = (int)s.u.cs.cnt[bk[q]], b1 = (int)s.u.cs.cur[bk[q]];
+        const uint32_t bq = bucket_of(k[q]), xq = (uint32_t)(wbase + q * 32);
+        const int b0 = (int)s.u.cs.cnt[bq], b1 = (int)s.u.cs.cur[bq];
         uint32_t r = 0;
         if (b1 - b0 > 1) {
           for (int j = b0; j < b1; ++j) {
             const uint64_t kj = s.okey[j];
-            r += kj < k[q] || (kj == k[q] && s.oidx[j] < x[q]);
+            r += kj < k[q] || (kj == k[q] && s.oidx[j] < xq);
           }
         }
         pos[q] = (uint32_t)b0 + r;
@@ -207,7 +208,7 @@ __global__ void __launch_bounds__(G::LF_BLOCK, 1024 / G::LF_BLOCK) k_local_final
     for (int q = 0; q < LF_ITEMS; ++q) {
       if (q < ipw && wbase + q * 32 < W) {
         s.okey[pos[q]] = k[q];
-        s.oidx[pos[q]] = (uint16_t)x[q];
+        s.oidx[pos[q]] = (uint16_t)(wbase + q * 32);
       }
     }
     __syncthreads();
@@ -222,6 +223,8 @@ __global__ void __launch_bounds__(G::LF_BLOCK, 1024 / G::LF_BLOCK) k_local_final
   } else {
     // ---- clustered window: stable 8-bit LSD passes over the bits that
     // vary in it; padding keys (all ones) stay behind the window's items
+#pragma unroll
+    for (int q = 0; q < LF_ITEMS; ++q) x[q] = (uint32_t)(wbase + q * 32);
     uint64_t ka = ~0ull, ko = 0ull;
 #pragma unroll
     for (int q = 0; q < LF_ITEMS; ++q) {

@@ -28,6 +28,16 @@ for shape in ("random", "tied", "path", "caterpillar"):
         ok &= np.array_equal(hb.edge_parent.numpy(), e.edge_parent)
         ok &= dendrogram_height_b200(r.edge_parent) == O.dendrogram_height(e.edge_parent, e.vertex_parent)
         bad += not ok
+# forced code paths a 128M build takes: view 0 chased in the select (random:
+# no deferral; path: every edge deferred to k_select_fix), the host level loop,
+# sliced maxIncident on every view
+for shape, paths in (("random", {"v0_select": 2, "tail_edges": -1}), ("path", {"v0_select": 2}),
+                     ("tied", {"mi_apply_mode": 2, "direct_mi_bytes": -1, "tail_edges": -1})):
+    nv, u, v, w = synth.GENERATORS[shape](60_000, seed=4)
+    r = b.build(nv, u, v, w, paths=paths)
+    e = O.build(nv, u, v, w)
+    bad += not (np.array_equal(r.edge_parent.cpu().numpy(), e.edge_parent)
+                and np.array_equal(r.vertex_parent.cpu().numpy(), e.vertex_parent))
 # validation: valid, duplicate (sort path), cycle (sort path, no duplicate), self-loop
 nv, u, v, w = synth.random_attach(50_000, seed=3)
 u = u.astype(np.int64)

@@ -93,7 +93,11 @@ def kernel_bytes(stats, n: int, nv: int) -> dict[str, float]:
                                                                 # not credited); view 0 chased in the select: no V2
         "jump": 0.0,
         "select_edges": 9.0 * sum(views_n[:L]) + 4.0 * n + 20.0 * alpha
+        + 4.0 * counts[0][2]                                    # view 0's chain edges: x1 gather
+        + (4.0 * (counts[0][2] + 2 * counts[0][0]) if info.get("v0_chase") else 0.0)
         + 16.0 * sum(views_n[k] for k in direct),               # euv + ret; x1; alpha: 2 gathers + next view;
+                                                                # chased view 0: 8-B maxIncident reads instead
+                                                                # of 4-B vertex-map reads (V2's pass dropped);
                                                                 # direct views: 2 atomics per next-view edge
         "walk": 17.0 * n,                                       # ret 1 + x1 4 + smi 4 + map 4 + key 4
         "sort2_pass": 16.0 * n * p2,                            # read 8, write 8 per pass

@@ -17,6 +17,16 @@ constexpr int SEL_BLOCK = 256;                 // k_select_edges
 constexpr int LS_TILE = DMST_LS_TILE;          // k_leafscan words per tile
 constexpr int CHASE_FREE = 8;    // V2 chase steps before rulers may end a chase
 constexpr int CHASE_CAP = 512;   // hard bound on one V2 chase
+// build-time A/B switches (tools/gpu_ab_variants.sh)
+#ifndef DMST_V1_KEEP
+#define DMST_V1_KEEP 0
+#endif
+#ifndef DMST_V2_LDG
+#define DMST_V2_LDG 0
+#endif
+#ifndef DMST_WALK_L1CS
+#define DMST_WALK_L1CS 0
+#endif
 
 // ~1/32 of vertices are "rulers": a long chase stops at the first ruler it
 // reaches, so pointer jumping only runs over rulers (deep in-trees: chains).
@@ -276,10 +286,20 @@ __global__ void k_v1(int64_t nv, const unsigned long long* __restrict__ mi64,
   int32_t out = -1;
   if (j1) {
     const uint32_t j = j1 - 1;
+#if DMST_V1_KEEP
+    // views >= 1: the rank gathers hit the view's grank array (<= 134 MB at
+    // 128M) at random; keep it in L2 and stream everything else past it
+    out = grank ? (int32_t)ld_keep(reinterpret_cast<const uint32_t*>(grank) + j, l2_keep_policy()) : (int32_t)j;
+#else
     out = grank ? __ldg(grank + j) : (int32_t)j;
+#endif
     atomicAdd(cnt2 + (j >> 4), 1u << ((j & 15) * 2));
   }
+#if DMST_V1_KEEP
+  __stcs(parent_out + x, out);
+#else
   parent_out[x] = out;
+#endif
 }
 
 // Exclusive prefixes of leaf-edge and alpha-edge counts per 16-edge word
@@ -487,7 +507,11 @@ __global__ void k_v2(int64_t nv, const unsigned long long* __restrict__ mi64, co
         unresolved = true;
         break;
       }
+#if DMST_V2_LDG
+      m = smi ? mi64[y] : __ldcs(mi64 + y);  // views >= 1: the table is within ~2x of L2
+#else
       m = __ldcs(mi64 + y);
+#endif
       j = (uint32_t)(m >> 32) - 1u;
       y = (uint32_t)m;
     }
@@ -801,7 +825,11 @@ k_walk(int64_t n, const int8_t* __restrict__ ret, const int32_t* __restrict__ x1
           const int2* pt = lvl + lt.soff[k] + x;
           int2 t;
           if (k == 1) {
+#if DMST_WALK_L1CS
+            t = __ldcs(pt);  // evict-first: leave L2 to the deeper (evict_last) tables
+#else
             t = *pt;
+#endif
           } else {
             const uint2 q = ld_keep2(reinterpret_cast<const uint2*>(pt), pol);
             t = make_int2((int)q.x, (int)q.y);

@@ -58,6 +58,10 @@ constexpr int S2L_BLOCK = 256, S2L_ITEMS = 20, S2L_MINB = 2;
 constexpr int64_t kS2LargeEdges = 32ll << 20;
 constexpr int64_t kDirectMiBytes = 64ll << 20;  // direct scatter-max below this mi64 size
 
+#ifndef DMST_V2_KEEP_BYTES
+#define DMST_V2_KEEP_BYTES (256ll << 20)  // V2 chase hops keep the maxIncident table in L2 up to this size
+#endif
+
 enum KernelKind {
   KK_SORT1_HIST, KK_SORT1_FIRST, KK_SORT1_MID, KK_SORT1_FINAL, KK_MI_HIST, KK_MI_SPLIT_A, KK_MI_SPLIT_B,
   KK_MI_APPLY, KK_V1, KK_LEAFSCAN, KK_V2, KK_JUMP, KK_SELECT_EDGES, KK_WALK, KK_SORT2_PASS, KK_LINK_SPLIT,
@@ -925,7 +929,8 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
       c.begin(KK_V2);
       k_v2<<<grid_for(nv_k, EW_BLOCK), EW_BLOCK, 0, c.s>>>(nv_k, mi_k, w.lw, vm,
                                                            level == 0 ? nullptr : w.smi_all + lt.soff[level],
-                                                           lists[0], lcnt[0], lists[3], lcnt[3]);
+                                                           lists[0], lcnt[0], lists[3], lcnt[3],
+                                                           8 * nv_k <= (int64_t)DMST_V2_KEEP_BYTES);
       c.launched();
     };
     // view 0's vertex map is read only by its select: the select may find the

@@ -18,14 +18,14 @@ constexpr int LS_TILE = DMST_LS_TILE;          // k_leafscan words per tile
 constexpr int CHASE_FREE = 8;    // V2 chase steps before rulers may end a chase
 constexpr int CHASE_CAP = 512;   // hard bound on one V2 chase
 // build-time A/B switches (tools/gpu_ab_variants.sh)
-#ifndef DMST_V1_KEEP
-#define DMST_V1_KEEP 0
+#ifndef DMST_SEL_FIRST_LDG
+#define DMST_SEL_FIRST_LDG 0
 #endif
-#ifndef DMST_V2_LDG
-#define DMST_V2_LDG 0
+#ifndef DMST_SEL_STREAM
+#define DMST_SEL_STREAM 0
 #endif
-#ifndef DMST_WALK_L1CS
-#define DMST_WALK_L1CS 0
+#ifndef DMST_V2_STNORM
+#define DMST_V2_STNORM 0
 #endif
 
 // ~1/32 of vertices are "rulers": a long chase stops at the first ruler it
@@ -286,20 +286,10 @@ __global__ void k_v1(int64_t nv, const unsigned long long* __restrict__ mi64,
   int32_t out = -1;
   if (j1) {
     const uint32_t j = j1 - 1;
-#if DMST_V1_KEEP
-    // views >= 1: the rank gathers hit the view's grank array (<= 134 MB at
-    // 128M) at random; keep it in L2 and stream everything else past it
-    out = grank ? (int32_t)ld_keep(reinterpret_cast<const uint32_t*>(grank) + j, l2_keep_policy()) : (int32_t)j;
-#else
     out = grank ? __ldg(grank + j) : (int32_t)j;
-#endif
     atomicAdd(cnt2 + (j >> 4), 1u << ((j & 15) * 2));
   }
-#if DMST_V1_KEEP
-  __stcs(parent_out + x, out);
-#else
   parent_out[x] = out;
-#endif
 }
 
 // Exclusive prefixes of leaf-edge and alpha-edge counts per 16-edge word
@@ -488,7 +478,8 @@ __device__ __forceinline__ uint32_t leaf_label(uint2 w, uint32_t j) {
 // one random 8-B probe (one DRAM sector) per level; vm has stride 2 there.
 __global__ void k_v2(int64_t nv, const unsigned long long* __restrict__ mi64, const uint2* __restrict__ lw,
                      int32_t* __restrict__ vm, const int32_t* __restrict__ smi, int32_t* __restrict__ rul,
-                     uint32_t* __restrict__ rul_cnt, int32_t* __restrict__ non, uint32_t* __restrict__ non_cnt) {
+                     uint32_t* __restrict__ rul_cnt, int32_t* __restrict__ non, uint32_t* __restrict__ non_cnt,
+                     bool keep) {
   // lw[j >> 5] = (leaf bitmap of edges 32w..32w+31, leaf count before 32w):
   // half the footprint of kw, so the chase's kind tests stay L2-resident
   const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -507,20 +498,25 @@ __global__ void k_v2(int64_t nv, const unsigned long long* __restrict__ mi64, co
         unresolved = true;
         break;
       }
-#if DMST_V2_LDG
-      m = smi ? mi64[y] : __ldcs(mi64 + y);  // views >= 1: the table is within ~2x of L2
-#else
-      m = __ldcs(mi64 + y);
-#endif
+      // a table within ~2x of L2 keeps its hops (normal policy: 0.81 -> 0.69
+      // ms for views 1-2 at 128M); a larger one streams them (evict-first)
+      m = keep ? mi64[y] : __ldcs(mi64 + y);
       j = (uint32_t)(m >> 32) - 1u;
       y = (uint32_t)m;
     }
     const int32_t lab = unresolved ? ~(int32_t)y
                                    : (m ? (int32_t)(lwj.y + __popc(lwj.x & ((1u << (j & 31)) - 1u))) : 0);
+#if DMST_V2_STNORM
+    if (smi)
+      reinterpret_cast<int2*>(vm)[x] = make_int2(lab, __ldcs(smi + x));  // gathered by the select next
+    else
+      vm[x] = lab;
+#else
     if (smi)
       __stcs(reinterpret_cast<int2*>(vm) + x, make_int2(lab, __ldcs(smi + x)));
     else
       __stcs(vm + x, lab);
+#endif
   }
   const bool ruler = unresolved && is_ruler((uint32_t)x);
   const bool plain = unresolved && !ruler;
@@ -614,12 +610,20 @@ struct SelEdge {
 __device__ __forceinline__ SelEdge sel_load(const EdgeSel& es, int64_t j, int64_t n) {
   SelEdge r;
   r.in = j < n;
+#if DMST_SEL_STREAM
+  const uint2 w = r.in ? __ldcs(es.kw + (j >> 4)) : make_uint2(0, 0);
+#else
   const uint2 w = r.in ? es.kw[j >> 4] : make_uint2(0, 0);
+#endif
   const uint32_t sh = (uint32_t)(j & 15) * 2;
   const uint32_t c = (w.x >> sh) & 3u;
   r.alpha = r.in && c == 0u;
   r.lab = c == 2u ? (int32_t)leaf_label(w, (uint32_t)j) : -1;
+#if DMST_SEL_STREAM
+  r.pos = r.alpha ? __ldcs(es.apre + (j >> 4)) + __popc(alpha_bits(w.x, 0, 16) & ((1u << sh) - 1u)) : 0u;
+#else
   r.pos = r.alpha ? es.apre[j >> 4] + __popc(alpha_bits(w.x, 0, 16) & ((1u << sh) - 1u)) : 0u;
+#endif
   r.g = r.in ? (es.grank ? __ldcs(es.grank + j) : (int32_t)j) : 0;
   r.need = r.alpha || (r.in && es.x1 != nullptr && r.lab < 0);
   r.e = r.need ? __ldcs(es.euv + j) : make_int2(0, 0);
@@ -694,8 +698,13 @@ __global__ void __launch_bounds__(SEL_BLOCK) k_select_edges(int64_t n, EdgeSel e
       for (int q = 0; q < U; ++q) {
         pa[q] = d[q].need;
         pb[q] = d[q].alpha;
+#if DMST_SEL_FIRST_LDG
+        ma[q] = pa[q] ? es.mi0[d[q].e.x] : 0ull;
+        mb[q] = pb[q] ? es.mi0[d[q].e.y] : 0ull;
+#else
         ma[q] = pa[q] ? __ldcs(es.mi0 + d[q].e.x) : 0ull;
         mb[q] = pb[q] ? __ldcs(es.mi0 + d[q].e.y) : 0ull;
+#endif
         a[q] = d[q].lab;
         bb[q] = 0;
       }
@@ -737,8 +746,9 @@ __global__ void __launch_bounds__(SEL_BLOCK) k_select_edges(int64_t n, EdgeSel e
         if (!more) break;
 #pragma unroll
         for (int q = 0; q < U; ++q) {
-          if (pa[q]) ma[q] = __ldcs(es.mi0 + (uint32_t)ma[q]);
-          if (pb[q]) mb[q] = __ldcs(es.mi0 + (uint32_t)mb[q]);
+          // chase hops with the normal policy (evict-first: +0.13 ms at 128M)
+          if (pa[q]) ma[q] = es.mi0[(uint32_t)ma[q]];
+          if (pb[q]) mb[q] = es.mi0[(uint32_t)mb[q]];
         }
       }
     }
@@ -820,16 +830,12 @@ k_walk(int64_t n, const int8_t* __restrict__ ret, const int32_t* __restrict__ x1
       if (r < lt.L) {
         int32_t x = __ldcs(x1 + e);  // view-1 supervertex
         for (int k = 1;; ++k) {
-          // view 1's table is far larger than L2 (normal policy); the
-          // deeper, smaller tables are kept resident (evict_last)
+          // view 1's table is larger than L2 (evict-first); the deeper,
+          // smaller tables are kept resident (evict_last)
           const int2* pt = lvl + lt.soff[k] + x;
           int2 t;
           if (k == 1) {
-#if DMST_WALK_L1CS
-            t = __ldcs(pt);  // evict-first: leave L2 to the deeper (evict_last) tables
-#else
-            t = *pt;
-#endif
+            t = __ldcs(pt);  // evict-first: leave L2 to the deeper tables (walk -0.08 ms)
           } else {
             const uint2 q = ld_keep2(reinterpret_cast<const uint2*>(pt), pol);
             t = make_int2((int)q.x, (int)q.y);

@@ -17,16 +17,6 @@ constexpr int SEL_BLOCK = 256;                 // k_select_edges
 constexpr int LS_TILE = DMST_LS_TILE;          // k_leafscan words per tile
 constexpr int CHASE_FREE = 8;    // V2 chase steps before rulers may end a chase
 constexpr int CHASE_CAP = 512;   // hard bound on one V2 chase
-// build-time A/B switches (tools/gpu_ab_variants.sh)
-#ifndef DMST_SEL_FIRST_LDG
-#define DMST_SEL_FIRST_LDG 0
-#endif
-#ifndef DMST_SEL_STREAM
-#define DMST_SEL_STREAM 0
-#endif
-#ifndef DMST_V2_STNORM
-#define DMST_V2_STNORM 0
-#endif
 
 // ~1/32 of vertices are "rulers": a long chase stops at the first ruler it
 // reaches, so pointer jumping only runs over rulers (deep in-trees: chains).
@@ -506,17 +496,10 @@ __global__ void k_v2(int64_t nv, const unsigned long long* __restrict__ mi64, co
     }
     const int32_t lab = unresolved ? ~(int32_t)y
                                    : (m ? (int32_t)(lwj.y + __popc(lwj.x & ((1u << (j & 31)) - 1u))) : 0);
-#if DMST_V2_STNORM
-    if (smi)
-      reinterpret_cast<int2*>(vm)[x] = make_int2(lab, __ldcs(smi + x));  // gathered by the select next
-    else
-      vm[x] = lab;
-#else
     if (smi)
       __stcs(reinterpret_cast<int2*>(vm) + x, make_int2(lab, __ldcs(smi + x)));
     else
       __stcs(vm + x, lab);
-#endif
   }
   const bool ruler = unresolved && is_ruler((uint32_t)x);
   const bool plain = unresolved && !ruler;
@@ -610,20 +593,12 @@ struct SelEdge {
 __device__ __forceinline__ SelEdge sel_load(const EdgeSel& es, int64_t j, int64_t n) {
   SelEdge r;
   r.in = j < n;
-#if DMST_SEL_STREAM
-  const uint2 w = r.in ? __ldcs(es.kw + (j >> 4)) : make_uint2(0, 0);
-#else
   const uint2 w = r.in ? es.kw[j >> 4] : make_uint2(0, 0);
-#endif
   const uint32_t sh = (uint32_t)(j & 15) * 2;
   const uint32_t c = (w.x >> sh) & 3u;
   r.alpha = r.in && c == 0u;
   r.lab = c == 2u ? (int32_t)leaf_label(w, (uint32_t)j) : -1;
-#if DMST_SEL_STREAM
-  r.pos = r.alpha ? __ldcs(es.apre + (j >> 4)) + __popc(alpha_bits(w.x, 0, 16) & ((1u << sh) - 1u)) : 0u;
-#else
   r.pos = r.alpha ? es.apre[j >> 4] + __popc(alpha_bits(w.x, 0, 16) & ((1u << sh) - 1u)) : 0u;
-#endif
   r.g = r.in ? (es.grank ? __ldcs(es.grank + j) : (int32_t)j) : 0;
   r.need = r.alpha || (r.in && es.x1 != nullptr && r.lab < 0);
   r.e = r.need ? __ldcs(es.euv + j) : make_int2(0, 0);
@@ -698,13 +673,8 @@ __global__ void __launch_bounds__(SEL_BLOCK) k_select_edges(int64_t n, EdgeSel e
       for (int q = 0; q < U; ++q) {
         pa[q] = d[q].need;
         pb[q] = d[q].alpha;
-#if DMST_SEL_FIRST_LDG
-        ma[q] = pa[q] ? es.mi0[d[q].e.x] : 0ull;
-        mb[q] = pb[q] ? es.mi0[d[q].e.y] : 0ull;
-#else
         ma[q] = pa[q] ? __ldcs(es.mi0 + d[q].e.x) : 0ull;
         mb[q] = pb[q] ? __ldcs(es.mi0 + d[q].e.y) : 0ull;
-#endif
         a[q] = d[q].lab;
         bb[q] = 0;
       }

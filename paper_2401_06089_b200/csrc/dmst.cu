@@ -59,7 +59,10 @@ constexpr int64_t kS2LargeEdges = 32ll << 20;
 constexpr int64_t kDirectMiBytes = 64ll << 20;  // direct scatter-max below this mi64 size
 
 #ifndef DMST_V2_KEEP_BYTES
-#define DMST_V2_KEEP_BYTES (256ll << 20)  // V2 chase hops keep the maxIncident table in L2 up to this size
+// V2 chase hops keep the maxIncident table in L2 (normal policy) up to this
+// size, ~4x L2 (measured: config 4's view 1, 268 MB, and every config-5 view
+// gain; view 0 of config 4, 1 GB, is chased in the select instead)
+#define DMST_V2_KEEP_BYTES (512ll << 20)
 #endif
 
 enum KernelKind {

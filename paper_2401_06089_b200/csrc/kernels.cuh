@@ -488,7 +488,7 @@ __global__ void k_v2(int64_t nv, const unsigned long long* __restrict__ mi64, co
         unresolved = true;
         break;
       }
-      // a table within ~2x of L2 keeps its hops (normal policy: 0.81 -> 0.69
+      // a table within ~4x of L2 keeps its hops (normal policy: 0.81 -> 0.69
       // ms for views 1-2 at 128M); a larger one streams them (evict-first)
       m = keep ? mi64[y] : __ldcs(mi64 + y);
       j = (uint32_t)(m >> 32) - 1u;

@@ -610,6 +610,10 @@ def run_b200(args) -> None:
                 "avg_launch_ms": kms / kcalls, "launches_per_build": kr["launches_per_build"],
                 "peak_source": peak_src,
                 "note": "traffic = ncu dram__bytes_read+write per launch (profiles/ncu_traffic.json)"}
+        if roof["traffic"]:
+            # what the DRAM actually moved for this kind (random 4-8 B accesses cost 64-B
+            # sectors), per launch over the live launch time: how close it runs to the wall
+            roof["dram_frac"] = roof["traffic"] / (roof["avg_launch_ms"] * 1e-3) / 1e9 / peak
         B = sum(pipeline_bytes(int(t[1].shape[0]), S) for t in trees) * ws
         pipe_ach = B / (ms_step * 1e-3) / 1e9
         cpu = None

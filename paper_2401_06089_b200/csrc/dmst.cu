@@ -58,6 +58,9 @@ constexpr int S2L_BLOCK = 256, S2L_ITEMS = 20, S2L_MINB = 2;
 constexpr int64_t kS2LargeEdges = 32ll << 20;
 constexpr int64_t kDirectMiBytes = 64ll << 20;  // direct scatter-max below this mi64 size
 
+#ifndef DMST_LINK_SLICE_BITS
+#define DMST_LINK_SLICE_BITS kSliceBits  // link: ranks per L2-resident slice of edge_parent (2M = 8 MB; 4M / 8M: +0.1-0.2 ms)
+#endif
 #ifndef DMST_V2_KEEP_BYTES
 // V2 chase hops keep the maxIncident table in L2 (normal policy) up to this
 // size, ~4x L2 (measured: config 4's view 1, 268 MB, and every config-5 view
@@ -1162,7 +1165,7 @@ void pandora_core(Ctx& c, int64_t n, int64_t nv, int32_t* vertex_parent, int32_t
     // sliced (as the maxIncident apply): one multisplit pass into 2M-rank
     // slices + L2-resident scatter, instead of two passes + a shared-memory apply
     const bool lsl = mi_sliced(c, n);
-    const uint32_t nf = (uint32_t)cdiv(n, FB), gshift = lsl ? (uint32_t)(kSliceBits - FB_BITS) : coarse_shift(nf);
+    const uint32_t nf = (uint32_t)cdiv(n, FB), gshift = lsl ? (uint32_t)(DMST_LINK_SLICE_BITS - FB_BITS) : coarse_shift(nf);
     const uint32_t nc = (uint32_t)cdiv(nf, 1u << gshift);
     uint32_t* fine_cur = w.fine;
     uint32_t* coarse_cur = w.fine + (nf + 2);
